@@ -1,0 +1,320 @@
+"""Benchmark of the B200 RPLU pivot loop (BASELINE.json metric).
+
+Default workload (N=1): BASELINE configs[2], dense fp64 32768 x 32768, rank
+512 — the config the metric's "dense Schur step HBM GB/s vs B200 peak" is
+quoted on (configs[0] is the reference's CPU-sized case, configs[1] a
+latency-bound Cauchy case; both are parity-test cases).
+
+One bench "step" = one full RPLU run of `rank` pivot steps on the resident
+input (eliminate(): copy A into the residual buffer, then the device loop).
+value = pivot steps / s over the K timed runs (inputs in HBM, CUDA events);
+e2e   = the same metric through the public drop-in call with HOST buffers
+        (pinned numpy A in, numpy L/U/pivots out, copies inside the region).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                [--config c3f64|c3f32|c1] [--n N] [--rank R]
+Under torchrun (N>1) the residual is row-block sharded across ranks
+(paper_2601_22344_b200.distributed); rank 0 prints one JSON line.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    "c3f64": dict(desc="C3 dense fp64 32768x32768 rank 512 (BASELINE configs[2])",
+                  n=32768, rank=512, dtype="f64", seed=0),
+    "c3f32": dict(desc="C3 dense fp32 32768x32768 rank 512 (BASELINE configs[2])",
+                  n=32768, rank=512, dtype="f32", seed=0),
+    "c1": dict(desc="C1 dense fp64 2000x2000 rank 100 (BASELINE configs[0])",
+               n=2000, rank=100, dtype="f64", seed=0, kind="c1"),
+}
+METRIC = "RPLU pivot steps/sec at rank k; dense Schur step HBM GB/s vs B200 peak"
+UNIT = "pivot steps/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("RPLU_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend)
+        return dist, dist.get_rank(), ws
+    return None, 0, 1
+
+
+def _cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return model, len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(A_host, rank, seed, n_steps, threads):
+    """Oracle port (TEST INFRASTRUCTURE; timed here as the CPU baseline only):
+    `n_steps` pivot steps of the real-fp64 restatement of Alg 1 on the same
+    bytes, `threads` host threads over row blocks."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.eliminate_real(A_host, "rplu", n_steps, seed=seed, threads=threads,
+                          block_rows=max(256, A_host.shape[0] // (4 * threads)), copy=False)
+    dt = time.perf_counter() - t0
+    return n_steps / dt, dt
+
+
+def run_reference_arm(args, cfg, rank_id):
+    """--impl reference: the reference's algorithm on the host cores (oracle
+    port; the reference is pure Python/numpy and cannot travel to the box)."""
+    if rank_id != 0:
+        return
+    from paper_2601_22344_b200 import gen
+    n, rank = cfg["n"], cfg["rank"]
+    model, cores = _cpu_info()
+    t0 = time.perf_counter()
+    if cfg["n"] <= 4096 and cfg.get("kind") == "c1":
+        A = gen.c1_dense(cfg["seed"], n=n)
+    else:
+        A = gen.c3_dense_host_wy(cfg["seed"], n=n)
+    gen_s = time.perf_counter() - t0
+    import oracle
+    g = oracle.uniform_stream(cfg["seed"])
+    dtype = np.float32 if cfg["dtype"] == "f32" else np.float64
+    R = A.astype(dtype, copy=False)
+    # W warm-up pivot steps, then K timed pivot steps, continuing one elimination
+    oracle.eliminate_real(R, "rplu", args.warmup, gen=g, threads=cores, dtype=dtype,
+                          block_rows=max(256, n // (4 * cores)), copy=False)
+    t0 = time.perf_counter()
+    oracle.eliminate_real(R, "rplu", args.steps, gen=g, threads=cores, dtype=dtype,
+                          block_rows=max(256, n // (4 * cores)), copy=False)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": cfg["dtype"], "data": "synthetic (seeded, BASELINE construction)",
+        "config": {"workload": cfg["desc"], "n": n, "rank": rank, "seed": cfg["seed"],
+                   "step": "one pivot step of the full-size elimination (bounded sample)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} timed pivot steps after {args.warmup} warm-up "
+                                   f"steps at full size n={n} (input build {gen_s:.1f}s untimed); "
+                                   f"CPU: {model}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_arm(args, cfg, dist, rank_id, world):
+    import torch
+
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import gen
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, rank, seed = cfg["n"], cfg["rank"], cfg["seed"]
+    tdtype = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    esize = 4 if cfg["dtype"] == "f32" else 8
+
+    if world > 1:
+        from paper_2601_22344_b200 import distributed as rdist
+        return rdist.bench_sharded(args, cfg, dist, rank_id, world, dev, METRIC, UNIT)
+
+    if cfg["n"] <= 4096 and cfg.get("kind") == "c1":
+        A = torch.from_numpy(gen.c1_dense(seed, n=n)).to(dev)
+    else:
+        A = gen.c3_dense_device(seed, n=n, dtype=tdtype, device=dev)
+    torch.cuda.synchronize()
+
+    def one_run(time_kernels=False):
+        return rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(seed)), rank,
+                            compute_dtype=tdtype, time_kernels=time_kernels)
+
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    stats = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(args.steps):
+        tr = one_run(time_kernels=True)
+        stats.append(tr.kernel_stats)
+    ev1.record()
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    pivots_done = tr.steps
+    value = args.steps * pivots_done / (total_ms / 1e3)
+
+    sweep_ms = sum(s["sweep_ms"] for s in stats)
+    sweep_n = sum(s["sweep_launches"] for s in stats)
+    select_ms = sum(s["select_ms"] for s in stats)
+    launches = sum(s["kernel_launches"] for s in stats)
+    bytes_per_launch = 2.0 * n * n * esize
+    avg_s = (sweep_ms / sweep_n) / 1e3
+    achieved = bytes_per_launch / avg_s / 1e9
+    peak, peak_src = _peaks()
+
+    # e2e: public drop-in call with host buffers (pinned numpy in, numpy out)
+    host_t = torch.empty((n, n), dtype=tdtype, pin_memory=True)
+    host_t.copy_(A)
+    A_host = host_t.numpy()
+    torch.cuda.synchronize()
+    e2e_runs = max(1, min(args.steps, 3))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_runs):
+        tr_h = rp.eliminate(A_host, rp.PivotRule("rplu", rp.RngState(seed)), rank,
+                            compute_dtype=tdtype)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_value = e2e_runs * tr_h.steps / (e2e_ms / 1e3)
+    h2d = n * n * esize
+    d2h = tr_h.L.nbytes + tr_h.U.nbytes + 16 * tr_h.steps + 8 * (tr_h.steps + 1)
+    same = tr_h.pivots == tr.pivots
+
+    # CPU baseline: oracle port on the same bytes, bounded sample (2 pivot steps)
+    model, cores = _cpu_info()
+    cpu_steps = 2 if n > 8192 else 10
+    A64 = A_host.astype(np.float64) if tdtype == torch.float32 else A_host.copy()
+    del host_t
+    cb_v, cb_dt = cpu_baseline(A64, rank, seed, cpu_steps, cores)
+    del A64
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (seeded BASELINE construction, built on device with cuBLAS)",
+        "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": rank, "seed": seed,
+                   "step": f"one full elimination of {rank} pivot steps",
+                   "l2": f"inputs larger than L2 ({n * n * esize / 1e9:.1f} GB residual)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "dense_sweep_kernel (K3 fused Schur update + row masses)",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src},
+        "step_breakdown_ms": {"sweep_per_pivot": sweep_ms / sweep_n,
+                              "select_per_pivot": select_ms / (args.steps * (pivots_done + 1)),
+                              "total_per_pivot": total_ms / (args.steps * pivots_done)},
+        "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{cpu_steps} pivot steps of the oracle real-fp64 port on the "
+                                   f"same {n}x{n} bytes ({cb_dt:.1f}s), row blocks over "
+                                   f"{cores} threads; CPU: {model}"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "runs": e2e_runs, "ms_per_run": e2e_ms / e2e_runs,
+                "pivots_match_device_run": same},
+        "gpu_launches": launches,
+        "near_boundary_draws": tr.near_boundary_draws,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3f64", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--rank", type=int, default=None)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+        cfg["desc"] += f" [n overridden to {args.n}]"
+    if args.rank:
+        cfg["rank"] = args.rank
+    dist, rank_id, world = _dist()
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank_id)
+    else:
+        run_b200_arm(args, cfg, dist, rank_id, world)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,130 @@
+/*
+ * rplu_b200.h — C ABI of the B200-native Randomly Pivoted LU pivot loop.
+ *
+ * The reference (`rplu` 0.1.0, pure Python/numpy) has no FFI; this ABI is the
+ * drop-in boundary its three hot entry points bind to through ctypes
+ * (see INTEGRATION.md):
+ *
+ *   rplu_dense_run   replaces the loop of rplu.dense_pivots.eliminate
+ *                    (pkg/src/rplu/dense_pivots.py:129-209, rank-1 rules
+ *                    rplu / c2plu / cplu, _draw_rank1_pivot :103-126)
+ *   rplu_cauchy_run  replaces rplu.cauchy.structured_eliminate with plan=None
+ *                    (pkg/src/rplu/cauchy.py:177-256) and exact_row_norms
+ *                    (cauchy.py:129-137)
+ *   rplu_cur_run     replaces rplu.lowmem_cur.cur_build
+ *                    (pkg/src/rplu/lowmem_cur.py:212-300) for device
+ *                    operators (dense matrix, Gaussian kernel on points)
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes, no exceptions cross the ABI.
+ *   - Every call returns an int status: RPLU_OK (0) or a negative error class;
+ *     rplu_last_error() returns a thread-local message for the last failure.
+ *   - "device" pointers are CUDA device addresses on the context's GPU; the
+ *     library never frees caller memory.  "host" pointers are CPU memory.
+ *   - The caller's uniform stream is passed as a host array of doubles in
+ *     [0,1) drawn in order from the reference's RngState; the call reports how
+ *     many it consumed so the caller can advance its generator exactly.
+ *   - Calls are synchronous with respect to the host: on return all results
+ *     are in the caller's buffers.  One context per host thread.
+ */
+#ifndef RPLU_B200_H
+#define RPLU_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RPLU_B200_ABI_VERSION 1
+
+/* status codes (negative = error class; mapped to Python exceptions) */
+#define RPLU_OK 0
+#define RPLU_ERR_ARG (-1)        /* ValueError        (bad argument / range) */
+#define RPLU_ERR_ZERO_PIVOT (-2) /* ZeroDivisionError (pivot zero after resample) */
+#define RPLU_ERR_CAPABILITY (-3) /* CapabilityError   (unsupported operation) */
+#define RPLU_ERR_CUDA (-4)       /* RuntimeError      (CUDA failure) */
+
+/* element types of the residual / generators */
+#define RPLU_F32 1
+#define RPLU_F64 2
+#define RPLU_C128 3
+
+/* flags */
+#define RPLU_FLAG_TIME_KERNELS 1 /* bracket K2/K3 launches with CUDA events */
+
+/* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
+#define RPLU_RULE_RPLU 0
+#define RPLU_RULE_C2PLU 1
+#define RPLU_RULE_CPLU 2
+
+typedef struct rplu_ctx rplu_ctx;
+
+int rplu_abi_version(void);
+const char* rplu_last_error(void);
+
+/* Create a context bound to CUDA device `device` (workspace is grown lazily). */
+int rplu_ctx_create(int device, rplu_ctx** out);
+int rplu_ctx_destroy(rplu_ctx* ctx);
+
+/* ------------------------------------------------------------------------ */
+/* Dense Alg 1 (eliminate).                                                  */
+
+typedef struct rplu_dense_args {
+  int32_t dtype;          /* RPLU_F32 | RPLU_F64 | RPLU_C128 */
+  int32_t rule;           /* RPLU_RULE_* */
+  int64_t n, m;           /* residual shape */
+  int64_t ld;             /* row stride of R in elements (>= m) */
+  int64_t steps;          /* pivots requested, 0 <= steps <= min(n, m) */
+  double stop_tol;        /* >= 0; tol stop when ||R||_F <= stop_tol*||A||_F */
+  void* R;                /* device: n x ld, row-major, overwritten by the residual */
+  void* Lt;               /* device: steps x n; row t holds column t of L */
+  void* U;                /* device: steps x ldu; row t of U */
+  int64_t ldu;            /* row stride of U in elements (>= m) */
+  const double* uniforms; /* host: uniform stream (rule rplu), may be NULL otherwise */
+  int64_t n_uniforms;     /* length of `uniforms` (4*steps always suffices) */
+  void* stream;           /* cudaStream_t to run on (NULL = legacy default) */
+  int32_t flags;          /* RPLU_FLAG_* */
+  int32_t reserved;
+} rplu_dense_args;
+
+typedef struct rplu_dense_out {
+  int64_t* pivots;              /* host, caller-owned, >= 2*steps: i0,j0,i1,j1,... */
+  double* resid_fro;            /* host, caller-owned, >= steps+1 */
+  int64_t steps_done;           /* pivots taken */
+  int64_t uniforms_consumed;    /* uniforms read from the stream */
+  int64_t near_boundary_draws;  /* draws within 1e-12 relative of a CDF boundary */
+  int32_t clean_early_stop;     /* residual exactly zero before `steps` */
+  int32_t tol_stop;             /* stop_tol reached */
+  int64_t zero_pivot_i;         /* set with RPLU_ERR_ZERO_PIVOT */
+  int64_t zero_pivot_j;
+  /* with RPLU_FLAG_TIME_KERNELS: CUDA-event time summed over the launches of
+   * the fused Schur-update kernel (K3) and of the select kernel (K2), and the
+   * number of library kernels launched by the call */
+  double sweep_ms;
+  double select_ms;
+  int64_t sweep_launches;
+  int64_t kernel_launches;
+} rplu_dense_out;
+
+int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* out);
+
+/* Squared row masses sum_j |R_ij|^2 of a device matrix (K1), written to the
+ * device array `masses` (n doubles).  Used by the sharded driver for step 0
+ * and by accessors' row_norms(). */
+int rplu_row_masses(rplu_ctx* ctx, int32_t dtype, const void* R, int64_t n, int64_t m,
+                    int64_t ld, double* masses, void* stream);
+
+/* sample_index(weights, u) on a device weight vector (rng.py:50-74):
+ * first index whose running sum exceeds u*total, top clamp, walk-back over
+ * zero weights.  RPLU_ERR_ARG for empty / negative / all-zero weights.
+ * *near_boundary (optional) is set to 1 if the draw is within 1e-12*total of
+ * a CDF boundary. */
+int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
+                      int64_t* out_index, int32_t* near_boundary, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RPLU_B200_H */

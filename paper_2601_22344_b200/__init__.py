@@ -1,0 +1,22 @@
+"""B200-native Randomly Pivoted LU (arXiv 2601.22344) — the RPLU pivot loop.
+
+Drop-in for the hot entry points of the reference package ``rplu`` 0.1.0
+(``pkg/src/rplu/__init__.py:14-36`` re-exports): the same names, signatures,
+exception classes and uniform-stream consumption, computed by hand-written
+sm_100a kernels in ``librplu_b200.so`` (C ABI: ``include/rplu_b200.h``).
+
+There is no CPU fallback: without the built extension or a CUDA device the
+entry points raise.
+"""
+
+__version__ = "0.1.0"
+
+from .accessors import CallableOperator, CapabilityError, DenseMatrix, MatrixAccessor, materialize
+from .dense_pivots import EliminationTrace, PivotRule, eliminate
+from .rng import RngState, sample_index
+
+__all__ = [
+    "CallableOperator", "CapabilityError", "DenseMatrix", "MatrixAccessor", "materialize",
+    "EliminationTrace", "PivotRule", "eliminate",
+    "RngState", "sample_index",
+]

@@ -1,0 +1,146 @@
+"""ctypes binding of ``librplu_b200.so`` (the C ABI in ``include/rplu_b200.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).
+There is no fallback: if the shared object is missing or a CUDA device is not
+present, the public entry points raise instead of computing on the CPU.
+
+Status codes map onto the reference's exception classes
+(SURVEY §8(b)): ARG -> ValueError, ZERO_PIVOT -> ZeroDivisionError,
+CAPABILITY -> CapabilityError, CUDA -> RuntimeError.
+"""
+
+import ctypes
+import os
+import threading
+
+from .accessors import CapabilityError
+
+LIB_NAME = "librplu_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+RPLU_OK = 0
+RPLU_ERR_ARG = -1
+RPLU_ERR_ZERO_PIVOT = -2
+RPLU_ERR_CAPABILITY = -3
+RPLU_ERR_CUDA = -4
+
+RPLU_F32 = 1
+RPLU_F64 = 2
+RPLU_C128 = 3
+
+RULE_IDS = {"rplu": 0, "c2plu": 1, "cplu": 2}
+
+FLAG_TIME_KERNELS = 1
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+
+class DenseArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", c_i32), ("rule", c_i32),
+        ("n", c_i64), ("m", c_i64), ("ld", c_i64), ("steps", c_i64),
+        ("stop_tol", c_dbl),
+        ("R", c_vp), ("Lt", c_vp), ("U", c_vp), ("ldu", c_i64),
+        ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
+        ("stream", c_vp), ("flags", c_i32), ("reserved", c_i32),
+    ]
+
+
+class DenseOut(ctypes.Structure):
+    _fields_ = [
+        ("pivots", ctypes.POINTER(c_i64)), ("resid_fro", ctypes.POINTER(c_dbl)),
+        ("steps_done", c_i64), ("uniforms_consumed", c_i64),
+        ("near_boundary_draws", c_i64),
+        ("clean_early_stop", c_i32), ("tol_stop", c_i32),
+        ("zero_pivot_i", c_i64), ("zero_pivot_j", c_i64),
+        ("sweep_ms", c_dbl), ("select_ms", c_dbl), ("sweep_launches", c_i64),
+        ("kernel_launches", c_i64),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/rplu_b200.h
+SIGNATURES = {
+    "rplu_abi_version": (ctypes.c_int, []),
+    "rplu_last_error": (ctypes.c_char_p, []),
+    "rplu_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(c_vp)]),
+    "rplu_ctx_destroy": (ctypes.c_int, [c_vp]),
+    "rplu_dense_run": (ctypes.c_int, [c_vp, ctypes.POINTER(DenseArgs), ctypes.POINTER(DenseOut)]),
+    "rplu_row_masses": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "rplu_sample_index": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_i64),
+                                         ctypes.POINTER(c_i32), c_vp]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+class ExtensionMissingError(RuntimeError):
+    """The CUDA extension has not been built (there is no CPU fallback)."""
+
+
+def load_library(path=LIB_PATH):
+    """Load and type the shared library (no GPU needed to load it)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ExtensionMissingError(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (nvcc, sm_100a). The B200 path has no CPU fallback.")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(status):
+    """Raise the reference's exception class for a non-zero status."""
+    if status == RPLU_OK:
+        return
+    msg = load_library().rplu_last_error().decode(errors="replace")
+    if status == RPLU_ERR_ARG:
+        raise ValueError(msg)
+    if status == RPLU_ERR_ZERO_PIVOT:
+        raise ZeroDivisionError(msg)
+    if status == RPLU_ERR_CAPABILITY:
+        raise CapabilityError(msg)
+    raise RuntimeError(msg)
+
+
+class Context:
+    """One ``rplu_ctx`` (workspace + device binding) per (thread, device)."""
+
+    def __init__(self, device):
+        lib = load_library()
+        h = c_vp()
+        check(lib.rplu_ctx_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        self._lib = lib
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.rplu_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def context(device):
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(int(device))
+    if c is None:
+        c = ctxs[int(device)] = Context(device)
+    return c

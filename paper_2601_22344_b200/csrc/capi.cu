@@ -1,0 +1,187 @@
+// C ABI entry points (include/rplu_b200.h): context, errors, argument
+// validation with the reference's error classes, dispatch to the paths.
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "rplu_internal.h"
+
+namespace rplu {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                 cudaGetErrorString(e) + ") at " + where;
+  return RPLU_ERR_CUDA;
+}
+
+int DevBuf::ensure(size_t want) {
+  if (want <= bytes && ptr) return RPLU_OK;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+  size_t b = want < 256 ? 256 : want;
+  cudaError_t e = cudaMalloc(&ptr, b);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+  bytes = b;
+  return RPLU_OK;
+}
+
+void DevBuf::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out);
+int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long long m,
+                    long long ld, double* masses, cudaStream_t s);
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
+                      int* near, cudaStream_t s);
+
+// Bind the calling thread to the context's device for the duration of a call.
+struct DeviceGuard {
+  int prev = -1;
+  int rc = RPLU_OK;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) {
+      cudaError_t e = cudaSetDevice(dev);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaSetDevice");
+    }
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace rplu
+
+using namespace rplu;
+
+extern "C" {
+
+int rplu_abi_version(void) { return RPLU_B200_ABI_VERSION; }
+
+const char* rplu_last_error(void) { return g_last_error.c_str(); }
+
+int rplu_ctx_create(int device, rplu_ctx** out) {
+  if (!out) { set_error("rplu_ctx_create: out is NULL"); return RPLU_ERR_ARG; }
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) {
+    set_error("rplu_ctx_create: device " + std::to_string(device) + " out of range [0, " +
+              std::to_string(ndev) + ")");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(device);
+  if (g.rc) return g.rc;
+  rplu_ctx* c = new rplu_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return RPLU_OK;
+}
+
+int rplu_ctx_destroy(rplu_ctx* ctx) {
+  if (!ctx) return RPLU_OK;
+  {
+    DeviceGuard g(ctx->device);
+    ctx->state.release();
+    ctx->masses.release();
+    ctx->rowmax.release();
+    ctx->rowarg.release();
+    ctx->uniforms.release();
+    ctx->pivots.release();
+    ctx->resid.release();
+    for (auto& b : ctx->scratch) b.release();
+  }
+  delete ctx;
+  return RPLU_OK;
+}
+
+// Argument validation mirrors eliminate (dense_pivots.py:142-145) and
+// PivotRule (:56-59); the Python wrapper raises the same exception classes.
+int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out) {
+  if (!ctx || !a || !out) { set_error("rplu_dense_run: NULL argument"); return RPLU_ERR_ARG; }
+  if (a->dtype != RPLU_F32 && a->dtype != RPLU_F64 && a->dtype != RPLU_C128) {
+    set_error("rplu_dense_run: unknown dtype " + std::to_string(a->dtype));
+    return RPLU_ERR_ARG;
+  }
+  if (a->rule != RPLU_RULE_RPLU && a->rule != RPLU_RULE_C2PLU && a->rule != RPLU_RULE_CPLU) {
+    set_error("unknown pivot rule id " + std::to_string(a->rule));
+    return RPLU_ERR_ARG;
+  }
+  if (a->n < 1 || a->m < 1 || a->ld < a->m || a->ldu < a->m) {
+    set_error("rplu_dense_run: bad shape n=" + std::to_string(a->n) + " m=" +
+              std::to_string(a->m) + " ld=" + std::to_string(a->ld));
+    return RPLU_ERR_ARG;
+  }
+  const int64_t kmax = a->n < a->m ? a->n : a->m;
+  if (a->steps < 0 || a->steps > kmax) {
+    set_error("steps " + std::to_string(a->steps) + " out of range [0, " + std::to_string(kmax) +
+              "]");
+    return RPLU_ERR_ARG;
+  }
+  if (!(a->stop_tol >= 0.0)) { set_error("stop_tol must be nonnegative"); return RPLU_ERR_ARG; }
+  if (!a->R || (a->steps > 0 && (!a->Lt || !a->U))) {
+    set_error("rplu_dense_run: NULL device buffer");
+    return RPLU_ERR_ARG;
+  }
+  if (a->rule == RPLU_RULE_RPLU && a->steps > 0 && (!a->uniforms || a->n_uniforms < 2)) {
+    set_error("rule 'rplu' needs an RngState (uniform stream)");
+    return RPLU_ERR_ARG;
+  }
+  if (!out->pivots && a->steps > 0) { set_error("rplu_dense_run: out->pivots is NULL"); return RPLU_ERR_ARG; }
+  if (!out->resid_fro) { set_error("rplu_dense_run: out->resid_fro is NULL"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  int st = dense_run_impl(ctx, a, out);
+  if (st == RPLU_ERR_CUDA || st == RPLU_ERR_ARG) return st;
+  if (st == kZeroPivot) {
+    set_error("pivot (" + std::to_string(out->zero_pivot_i) + ", " +
+              std::to_string(out->zero_pivot_j) + ") has exactly zero value after resampling");
+    return RPLU_ERR_ZERO_PIVOT;
+  }
+  if (st == kUniformsExhausted) {
+    set_error("uniform stream exhausted (pass at least 4*steps uniforms)");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+int rplu_row_masses(rplu_ctx* ctx, int32_t dtype, const void* R, int64_t n, int64_t m, int64_t ld,
+                    double* masses, void* stream) {
+  if (!ctx || !R || !masses || n < 0 || m < 0 || ld < m) {
+    set_error("rplu_row_masses: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return row_masses_impl(ctx, dtype, R, n, m, ld, masses, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
+                      int64_t* out_index, int32_t* near_boundary, void* stream) {
+  if (!ctx || !out_index) { set_error("rplu_sample_index: NULL argument"); return RPLU_ERR_ARG; }
+  if (n <= 0 || !weights) { set_error("weights must be a nonempty 1-D array"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  long long idx = -1;
+  int near = 0;
+  int rc = sample_index_impl(ctx, weights, n, u, &idx, &near, reinterpret_cast<cudaStream_t>(stream));
+  if (rc) return rc;
+  *out_index = idx;
+  if (near_boundary) *near_boundary = near;
+  return RPLU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,556 @@
+// Dense RPLU pivot loop (Alg 1) — K1 row masses, K2 two-stage pivot
+// selection, K3 fused rank-1 Schur update + next-step row masses.
+//
+// Reference: rplu.dense_pivots.eliminate (pkg/src/rplu/dense_pivots.py:129-209)
+//   per step: norms = einsum(R*conj R) (:115), i = sample_index(norms, u1),
+//   j = sample_index(|R[i]|^2, u2) (:116-117), zero-pivot resample (:178-184),
+//   col = R[:,j]/a, row = R[i].copy(), R -= outer(col,row) (:185-187),
+//   L[:,t] = col, U[t] = row (:188-189), resid_fro = ||R||_F (:192),
+//   clean stop on zero residual (:162-164), tol stop (:195-197).
+//
+// B200 layout: R is row-major n x ld in HBM and is streamed exactly once per
+// step by K3 (read + write = 2*n*m*sizeof(T) bytes, the algorithmic traffic);
+// the pivot row U[t,:] (<= 512 KB) stays L2-resident while every CTA re-reads
+// it; row masses for step t+1 fall out of the same pass, so there is no
+// separate reduction pass over R.  K2 is a single CTA (1024 threads) that
+// scans the n masses and the m pivot-row weights; it never leaves the device,
+// so the whole loop runs without a host round trip.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "rplu_common.cuh"
+#include "rplu_internal.h"
+
+namespace rplu {
+
+struct DenseParams {
+  void* R;
+  long long ld, n, m;
+  void* Lt;
+  void* U;
+  long long ldu;
+  double* masses;
+  double* rowmax;
+  long long* rowarg;
+  DevState* st;
+  long long t, steps;
+  const double* uniforms;
+  long long n_uniforms;
+  double* resid;
+  long long* pivots;
+  double stop_tol;
+  int rule;
+};
+
+template <typename T, int VEC>
+struct alignas(sizeof(T) * VEC) VecT {
+  T v[VEC];
+};
+
+template <typename T> __device__ __forceinline__ typename Scalar<T>::coef_t load_coef(const DevState* st);
+template <> __device__ __forceinline__ double load_coef<double>(const DevState* st) { return st->inv_d; }
+template <> __device__ __forceinline__ float load_coef<float>(const DevState* st) { return st->inv_f; }
+template <> __device__ __forceinline__ CDivCoef load_coef<double2>(const DevState* st) {
+  CDivCoef c;
+  c.rat = st->rat;
+  c.scl = st->scl;
+  c.branch = st->branch;
+  return c;
+}
+
+template <typename T> __device__ __forceinline__ void store_coef(DevState* st, T a);
+template <> __device__ __forceinline__ void store_coef<double>(DevState* st, double a) {
+  st->inv_d = Scalar<double>::make_coef(a);
+  st->a_re = a;
+  st->a_im = 0.0;
+}
+template <> __device__ __forceinline__ void store_coef<float>(DevState* st, float a) {
+  st->inv_f = Scalar<float>::make_coef(a);
+  st->a_re = a;
+  st->a_im = 0.0;
+}
+template <> __device__ __forceinline__ void store_coef<double2>(DevState* st, double2 a) {
+  CDivCoef c = cdiv_coef(a);
+  st->rat = c.rat;
+  st->scl = c.scl;
+  st->branch = c.branch;
+  st->a_re = a.x;
+  st->a_im = a.y;
+}
+
+// ---------------------------------------------------------------------------
+// K1 / K3: one CTA owns RB consecutive rows and streams them in 16-byte
+// vectors.  UPDATE=false: masses only (step 0).  UPDATE=true: in-place
+// R[k,:] -= (R[k,j]/a) * U[t,:] fused with the masses of the updated rows.
+// The pivot-column entries R[k,j] are captured before any write of the row
+// (WAR hazard), L[:,t] is written transposed (Lt[t,k]) so the
+// store is coalesced.
+template <typename T, int VEC, int RB, bool UPDATE, bool TRACK_MAX>
+__global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  constexpr int NT = 256;
+  if (UPDATE && !p.st->active) return;
+  const long long row0 = (long long)blockIdx.x * RB;
+  const long long n = p.n, m = p.m, ld = p.ld;
+  T* R = reinterpret_cast<T*>(p.R);
+  __shared__ T lval[RB];
+  if (UPDATE) {
+    if (threadIdx.x < RB) {
+      long long k = row0 + threadIdx.x;
+      T lv = S::zero();
+      if (k < n) {
+        typename S::coef_t cf = load_coef<T>(p.st);
+        lv = S::scale(R[k * ld + p.st->pj], cf);
+        reinterpret_cast<T*>(p.Lt)[p.t * n + k] = lv;
+      }
+      lval[threadIdx.x] = lv;
+    }
+    __syncthreads();
+  }
+  T lv[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) lv[r] = UPDATE ? lval[r] : S::zero();
+  const T* prow = UPDATE ? reinterpret_cast<const T*>(p.U) + p.t * p.ldu : nullptr;
+
+  double acc[RB];
+  double mx[RB];
+  long long mi[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) { acc[r] = 0.0; mx[r] = -1.0; mi[r] = m; }
+
+  const long long mv = (m / VEC) * VEC;  // vectorised part
+  for (long long l = (long long)threadIdx.x * VEC; l < mv; l += (long long)NT * VEC) {
+    VecT<T, VEC> pv;
+    if (UPDATE) pv = *reinterpret_cast<const VecT<T, VEC>*>(prow + l);
+    VecT<T, VEC> rv[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (row0 + r < n) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (row0 + r) * ld + l);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (row0 + r < n) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          T x = rv[r].v[e];
+          if (UPDATE) x = S::sub_outer(x, lv[r], pv.v[e]);
+          rv[r].v[e] = x;
+          acc[r] += S::mass(x);
+          if (TRACK_MAX) argmax_merge(mx[r], mi[r], S::absval(x), l + e);
+        }
+        if (UPDATE) *reinterpret_cast<VecT<T, VEC>*>(R + (row0 + r) * ld + l) = rv[r];
+      }
+    }
+  }
+  // scalar tail (m % VEC columns)
+  for (long long l = mv + threadIdx.x; l < m; l += NT) {
+    T pvs = UPDATE ? prow[l] : S::zero();
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (row0 + r < n) {
+        T x = R[(row0 + r) * ld + l];
+        if (UPDATE) {
+          x = S::sub_outer(x, lv[r], pvs);
+          R[(row0 + r) * ld + l] = x;
+        }
+        acc[r] += S::mass(x);
+        if (TRACK_MAX) argmax_merge(mx[r], mi[r], S::absval(x), l);
+      }
+    }
+  }
+  // block reduction of the RB row masses (and maxima)
+  __shared__ double red[NT / 32][RB];
+  __shared__ double redm[TRACK_MAX ? NT / 32 : 1][RB];
+  __shared__ long long redi[TRACK_MAX ? NT / 32 : 1][RB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    double s = warp_sum(acc[r]);
+    if (lane == 0) red[w][r] = s;
+    if (TRACK_MAX) {
+      double v = mx[r];
+      long long i = mi[r];
+      warp_argmax(v, i);
+      if (lane == 0) { redm[w][r] = v; redi[w][r] = i; }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < RB) {
+    const int r = threadIdx.x;
+    const long long k = row0 + r;
+    if (k < n) {
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NT / 32; ++ww) s += red[ww][r];
+      p.masses[k] = s;
+      if (TRACK_MAX) {
+        double v = -1.0;
+        long long i = m;
+        for (int ww = 0; ww < NT / 32; ++ww) argmax_merge(v, i, redm[ww][r], redi[ww][r]);
+        p.rowmax[k] = v;
+        p.rowarg[k] = i;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: pivot selection for step t (t == steps: final residual norm only).
+template <typename T>
+__global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  constexpr int B = 1024;
+  DevState* st = p.st;
+  if (!st->active) return;
+  __shared__ CdfSmem<B> sm;
+  __shared__ long long s_i, s_j;
+  __shared__ int s_stop;
+  const long long n = p.n, m = p.m, ld = p.ld, t = p.t;
+  const T* R = reinterpret_cast<const T*>(p.R);
+  const double* masses = p.masses;
+  auto wrow = [&](long long k) { return masses[k]; };
+
+  Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+  const double total = cr.total;
+  const double resid = sqrt(total);
+  if (threadIdx.x == 0) {
+    p.resid[t] = resid;
+    if (t == 0) st->fro0 = resid;
+    double fro0 = (t == 0) ? resid : st->fro0;
+    int stop = 0;
+    if (t > 0 && p.stop_tol > 0.0 && resid <= p.stop_tol * fro0) {
+      st->status = kTolStop;
+      stop = 1;
+    } else if (t >= p.steps) {
+      stop = 1;
+    } else if (resid == 0.0) {
+      st->status = kCleanStop;
+      stop = 1;
+    }
+    if (stop) st->active = 0;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) return;
+
+  long long uc = st->ucount;
+  long long near = 0;
+  long long i = 0, j = 0;
+  T a = S::zero();
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (p.rule == RPLU_RULE_RPLU) {
+      if (uc + 2 > p.n_uniforms) {
+        if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
+        return;
+      }
+      const double u1 = p.uniforms[uc];
+      const double u2 = p.uniforms[uc + 1];
+      uc += 2;
+      i = cdf_find<B>(wrow, n, cr, u1, sm);
+      // near-boundary accounting for the row draw
+      if (threadIdx.x == 0) {
+        double tol = kNearBoundaryRel * total, tg = u1 * total;
+        if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+      }
+      const T* row = R + i * ld;
+      auto wcol = [&](long long k) { return S::weight(row[k]); };
+      __syncthreads();
+      Cdf<B> cc = cdf_build<B>(wcol, m, sm);
+      j = cdf_find<B>(wcol, m, cc, u2, sm);
+      if (threadIdx.x == 0) {
+        double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+        if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+      }
+    } else if (p.rule == RPLU_RULE_C2PLU) {
+      i = block_argmax<B>(wrow, n, nullptr);
+      const T* row = R + i * ld;
+      auto wabs = [&](long long k) { return S::absval(row[k]); };
+      j = block_argmax<B>(wabs, m, nullptr);
+    } else {  // CPLU: flat argmax of |R| from the per-row maxima
+      const double* rm = p.rowmax;
+      auto wmax = [&](long long k) { return rm[k]; };
+      i = block_argmax<B>(wmax, n, nullptr);
+      j = p.rowarg[i];
+    }
+    a = R[i * ld + j];
+    if (!S::is_zero(a)) break;
+    if (attempt == 1 || p.rule != RPLU_RULE_RPLU) {
+      if (threadIdx.x == 0) {
+        st->status = kZeroPivot;
+        st->active = 0;
+        st->err_i = i;
+        st->err_j = j;
+        st->ucount = uc;
+        st->near_boundary += near;
+      }
+      return;
+    }
+    __syncthreads();
+  }
+  // U[t,:] = R[i,:] (the pre-update pivot row; K3 reads it from here)
+  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+  const T* row = R + i * ld;
+  for (long long k = threadIdx.x; k < m; k += B) urow[k] = row[k];
+  if (threadIdx.x == 0) {
+    st->ucount = uc;
+    st->near_boundary += near;
+    st->pi = i;
+    st->pj = j;
+    store_coef<T>(st, a);
+    p.pivots[2 * t] = i;
+    p.pivots[2 * t + 1] = j;
+    st->done = t + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+
+__global__ void init_state_kernel(DevState* st) {
+  st->ucount = 0;
+  st->near_boundary = 0;
+  st->pi = st->pj = -1;
+  st->err_i = st->err_j = -1;
+  st->active = 1;
+  st->status = kRunning;
+  st->fro0 = 0.0;
+  st->done = 0;
+}
+
+template <typename T, int VEC, int RB>
+static void launch_sweep(const DenseParams& p, bool update, bool track, cudaStream_t s) {
+  dim3 grid((unsigned)((p.n + RB - 1) / RB));
+  if (update) {
+    if (track) dense_sweep_kernel<T, VEC, RB, true, true><<<grid, 256, 0, s>>>(p);
+    else dense_sweep_kernel<T, VEC, RB, true, false><<<grid, 256, 0, s>>>(p);
+  } else {
+    if (track) dense_sweep_kernel<T, VEC, RB, false, true><<<grid, 256, 0, s>>>(p);
+    else dense_sweep_kernel<T, VEC, RB, false, false><<<grid, 256, 0, s>>>(p);
+  }
+}
+
+template <typename T>
+static void sweep(const DenseParams& p, bool update, bool track, cudaStream_t s) {
+  constexpr int VEC = Scalar<T>::kVec;
+  bool vec_ok = (p.ld % VEC == 0) && ((uintptr_t)p.R % 16 == 0) &&
+                (!update || ((p.ldu % VEC == 0) && ((uintptr_t)p.U % 16 == 0)));
+  if (vec_ok) launch_sweep<T, VEC, 4>(p, update, track, s);
+  else launch_sweep<T, 1, 4>(p, update, track, s);
+}
+
+struct LoopTiming {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs (start, end) per timed launch
+  std::vector<int> kind;        // 0 = select, 1 = sweep
+  ~LoopTiming() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  void mark(int k, cudaStream_t s, bool start) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    if (start) kind.push_back(k);
+  }
+};
+
+template <typename T>
+static int dense_loop(const DenseParams& base, cudaStream_t s, LoopTiming& tm, long long* launches) {
+  DenseParams p = base;
+  const bool track = (p.rule == RPLU_RULE_CPLU);
+  sweep<T>(p, false, track, s);  // K1: masses of A
+  RPLU_CUDA(cudaGetLastError());
+  long long nl = 1;
+  for (long long t = 0; t <= p.steps; ++t) {
+    p.t = t;
+    tm.mark(0, s, true);
+    dense_select_kernel<T><<<1, 1024, 0, s>>>(p);
+    tm.mark(0, s, false);
+    ++nl;
+    if (t < p.steps) {
+      tm.mark(1, s, true);
+      sweep<T>(p, true, track, s);
+      tm.mark(1, s, false);
+      ++nl;
+    }
+  }
+  RPLU_CUDA(cudaGetLastError());
+  *launches = nl;
+  return RPLU_OK;
+}
+
+int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  const long long n = a->n, m = a->m, steps = a->steps;
+  int rc;
+  if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
+  if ((rc = ctx->masses.ensure(sizeof(double) * (size_t)(n > 0 ? n : 1)))) return rc;
+  if ((rc = ctx->pivots.ensure(sizeof(long long) * (size_t)(2 * steps + 2)))) return rc;
+  if ((rc = ctx->resid.ensure(sizeof(double) * (size_t)(steps + 1)))) return rc;
+  if (a->rule == RPLU_RULE_CPLU) {
+    if ((rc = ctx->rowmax.ensure(sizeof(double) * (size_t)n))) return rc;
+    if ((rc = ctx->rowarg.ensure(sizeof(long long) * (size_t)n))) return rc;
+  }
+  long long nu = (a->rule == RPLU_RULE_RPLU) ? a->n_uniforms : 0;
+  if ((rc = ctx->uniforms.ensure(sizeof(double) * (size_t)(nu > 0 ? nu : 1)))) return rc;
+  if (nu > 0)
+    RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * nu,
+                              cudaMemcpyHostToDevice, s));
+  DevState* st = reinterpret_cast<DevState*>(ctx->state.ptr);
+  init_state_kernel<<<1, 1, 0, s>>>(st);
+
+  DenseParams p{};
+  p.R = a->R;
+  p.ld = a->ld;
+  p.n = n;
+  p.m = m;
+  p.Lt = a->Lt;
+  p.U = a->U;
+  p.ldu = a->ldu;
+  p.masses = reinterpret_cast<double*>(ctx->masses.ptr);
+  p.rowmax = reinterpret_cast<double*>(ctx->rowmax.ptr);
+  p.rowarg = reinterpret_cast<long long*>(ctx->rowarg.ptr);
+  p.st = st;
+  p.steps = steps;
+  p.uniforms = reinterpret_cast<const double*>(ctx->uniforms.ptr);
+  p.n_uniforms = nu;
+  p.resid = reinterpret_cast<double*>(ctx->resid.ptr);
+  p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
+  p.stop_tol = a->stop_tol;
+  p.rule = a->rule;
+
+  LoopTiming tm;
+  tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
+  long long launches = 0;
+  switch (a->dtype) {
+    case RPLU_F64: rc = dense_loop<double>(p, s, tm, &launches); break;
+    case RPLU_F32: rc = dense_loop<float>(p, s, tm, &launches); break;
+    case RPLU_C128: rc = dense_loop<double2>(p, s, tm, &launches); break;
+    default: set_error("unknown dtype"); return RPLU_ERR_ARG;
+  }
+  if (rc) return rc;
+
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  const long long done = hs.done;
+  if (done > 0)
+    RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,
+                         cudaMemcpyDeviceToHost));
+  RPLU_CUDA(cudaMemcpy(out->resid_fro, p.resid, sizeof(double) * (done + 1),
+                       cudaMemcpyDeviceToHost));
+  out->steps_done = done;
+  out->kernel_launches = launches + 1;  // + init_state
+  out->sweep_ms = out->select_ms = 0.0;
+  out->sweep_launches = 0;
+  if (tm.on) {
+    // only launches that did work count (early-exit launches after a stop are
+    // a few microseconds and are excluded from the per-launch average)
+    for (size_t q = 0; q < tm.kind.size(); ++q) {
+      float ms = 0.f;
+      RPLU_CUDA(cudaEventElapsedTime(&ms, tm.ev[2 * q], tm.ev[2 * q + 1]));
+      if (tm.kind[q] == 1) {
+        if ((long long)out->sweep_launches < done) { out->sweep_ms += ms; out->sweep_launches++; }
+      } else {
+        out->select_ms += ms;
+      }
+    }
+  }
+  out->uniforms_consumed = hs.ucount;
+  out->near_boundary_draws = hs.near_boundary;
+  out->clean_early_stop = (hs.status == kCleanStop);
+  out->tol_stop = (hs.status == kTolStop);
+  out->zero_pivot_i = hs.err_i;
+  out->zero_pivot_j = hs.err_j;
+  return hs.status;
+}
+
+}  // namespace rplu
+
+namespace rplu {
+
+int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long long m,
+                    long long ld, double* masses, cudaStream_t s) {
+  (void)ctx;
+  if (n == 0) return RPLU_OK;
+  DenseParams p{};
+  p.R = const_cast<void*>(R);
+  p.ld = ld;
+  p.n = n;
+  p.m = m;
+  p.masses = masses;
+  p.ldu = m;
+  switch (dtype) {
+    case RPLU_F64: sweep<double>(p, false, false, s); break;
+    case RPLU_F32: sweep<float>(p, false, false, s); break;
+    case RPLU_C128: sweep<double2>(p, false, false, s); break;
+    default: set_error("unknown dtype"); return RPLU_ERR_ARG;
+  }
+  RPLU_CUDA(cudaGetLastError());
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  return RPLU_OK;
+}
+
+}  // namespace rplu
+
+// ---------------------------------------------------------------------------
+// sample_index (rng.py:50-74) as a standalone device call: the same K2 CDF
+// code the pivot loops use, exposed so its tie / zero / clamp semantics are
+// testable against the reference on arbitrary weight vectors.
+namespace rplu {
+
+struct SampleOut {
+  long long idx;
+  int status;  // 0 ok, 1 negative weight, 2 all zero
+  int near;
+};
+
+__global__ void __launch_bounds__(1024) sample_index_kernel(const double* w, long long n, double u,
+                                                            SampleOut* out) {
+  constexpr int B = 1024;
+  __shared__ CdfSmem<B> sm;
+  __shared__ int neg;
+  if (threadIdx.x == 0) neg = 0;
+  __syncthreads();
+  for (long long k = threadIdx.x; k < n; k += B)
+    if (w[k] < 0.0) neg = 1;
+  __syncthreads();
+  if (neg) {
+    if (threadIdx.x == 0) { out->status = 1; out->idx = -1; out->near = 0; }
+    return;
+  }
+  auto wf = [&](long long k) { return w[k]; };
+  Cdf<B> c = cdf_build<B>(wf, n, sm);
+  if (!(c.total > 0.0)) {
+    if (threadIdx.x == 0) { out->status = 2; out->idx = -1; out->near = 0; }
+    return;
+  }
+  long long i = cdf_find<B>(wf, n, c, u, sm);
+  if (threadIdx.x == 0) {
+    double tol = kNearBoundaryRel * c.total, tg = u * c.total;
+    out->near = (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) ? 1 : 0;
+    out->idx = i;
+    out->status = 0;
+  }
+}
+
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
+                      int* near, cudaStream_t s) {
+  int rc;
+  if ((rc = ctx->scratch[7].ensure(sizeof(SampleOut)))) return rc;
+  SampleOut* d = reinterpret_cast<SampleOut*>(ctx->scratch[7].ptr);
+  sample_index_kernel<<<1, 1024, 0, s>>>(w, n, u, d);
+  RPLU_CUDA(cudaGetLastError());
+  SampleOut h;
+  RPLU_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  if (h.status == 1) { set_error("weights must be nonnegative"); return RPLU_ERR_ARG; }
+  if (h.status == 2) { set_error("all weights are zero; nothing to sample"); return RPLU_ERR_ARG; }
+  *idx = h.idx;
+  if (near) *near = h.near;
+  return RPLU_OK;
+}
+
+}  // namespace rplu

@@ -1,0 +1,324 @@
+// Shared device helpers for the RPLU pivot loop (sm_100a).
+//
+// * Scalar traits for the three residual element types the reference path
+//   supports (fp32, fp64, complex128).  The reference computes everything in
+//   complex128 (dense_pivots.py:196-199, accessors.py:416); a real input has a
+//   zero imaginary part, so the real instantiations reproduce its arithmetic
+//   exactly (see numpy_cdiv / cmul_np below and DESIGN.md §"numerics").
+// * numpy-exact complex kernels: division (Smith, numpy loops.c divide),
+//   multiplication (npyv SIMD: fma(ar,br,-ai*bi), fma(ar,bi,ai*br)) and the
+//   AVX-512 cabs (L*sqrt(fma(r,r,1))).  All "_rn" intrinsics: no contraction.
+// * Block-wide chunked inverse-CDF search with the exact tie/zero semantics of
+//   rplu.rng.sample_index (rng.py:50-74): first index whose running sum is
+//   strictly greater than u*total (searchsorted side='right'), top clamp,
+//   walk-back over zero weights, first-positive fallback.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rplu {
+
+constexpr double kNearBoundaryRel = 1e-12;  // BASELINE north star: draws within
+                                            // 1e-12 relative of a CDF boundary
+
+// ---------------------------------------------------------------------------
+// complex helpers (double2 = {re, im})
+
+__device__ __forceinline__ double2 cmul_np(double2 a, double2 b) {
+  // numpy complex multiply as dispatched on x86-64 (AVX2/AVX-512 npyv path).
+  double re = __fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y));
+  double im = __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x));
+  return make_double2(re, im);
+}
+
+// Smith-division coefficients of a pivot value a, hoisted out of the column
+// loop.  branch 0: |ar| >= |ai|; branch 1 otherwise.
+struct CDivCoef {
+  double rat, scl;
+  int branch;
+};
+
+__device__ __forceinline__ CDivCoef cdiv_coef(double2 b) {
+  CDivCoef c;
+  if (fabs(b.x) >= fabs(b.y)) {
+    c.branch = 0;
+    c.rat = __ddiv_rn(b.y, b.x);
+    c.scl = __ddiv_rn(1.0, __dadd_rn(b.x, __dmul_rn(b.y, c.rat)));
+  } else {
+    c.branch = 1;
+    c.rat = __ddiv_rn(b.x, b.y);
+    c.scl = __ddiv_rn(1.0, __dadd_rn(b.y, __dmul_rn(b.x, c.rat)));
+  }
+  return c;
+}
+
+__device__ __forceinline__ double2 cdiv_apply(double2 a, const CDivCoef& c) {
+  double re, im;
+  if (c.branch == 0) {
+    re = __dmul_rn(__dadd_rn(a.x, __dmul_rn(a.y, c.rat)), c.scl);
+    im = __dmul_rn(__dsub_rn(a.y, __dmul_rn(a.x, c.rat)), c.scl);
+  } else {
+    re = __dmul_rn(__dadd_rn(__dmul_rn(a.x, c.rat), a.y), c.scl);
+    im = __dmul_rn(__dsub_rn(__dmul_rn(a.y, c.rat), a.x), c.scl);
+  }
+  return make_double2(re, im);
+}
+
+__device__ __forceinline__ double2 cdiv_np(double2 a, double2 b) {
+  return cdiv_apply(a, cdiv_coef(b));
+}
+
+__device__ __forceinline__ double cabs_np(double2 a) {
+  double x = fabs(a.x), y = fabs(a.y);
+  double L = fmax(x, y), S = fmin(x, y);
+  if (L == 0.0) return 0.0;
+  double r = __ddiv_rn(S, L);
+  return __dmul_rn(L, __dsqrt_rn(__fma_rn(r, r, 1.0)));
+}
+
+// ---------------------------------------------------------------------------
+// scalar traits
+
+template <typename T> struct Scalar;
+
+template <> struct Scalar<double> {
+  using coef_t = double;  // reciprocal of the pivot, x*(1/a) (numpy Smith, ai=0)
+  static constexpr int kVec = 2;
+  __device__ static __forceinline__ double mass(double v) { return v * v; }
+  // column weight |r|^2 with |.| = np.abs (exact for real values)
+  __device__ static __forceinline__ double weight(double v) { return __dmul_rn(v, v); }
+  __device__ static __forceinline__ double absval(double v) { return fabs(v); }
+  __device__ static __forceinline__ bool is_zero(double v) { return v == 0.0; }
+  __device__ static __forceinline__ coef_t make_coef(double a) { return __ddiv_rn(1.0, a); }
+  __device__ static __forceinline__ double scale(double c, coef_t k) { return __dmul_rn(c, k); }
+  __device__ static __forceinline__ double sub_outer(double r, double l, double p) {
+    return __dsub_rn(r, __dmul_rn(l, p));
+  }
+  __device__ static __forceinline__ double zero() { return 0.0; }
+};
+
+template <> struct Scalar<float> {
+  using coef_t = float;
+  static constexpr int kVec = 4;
+  __device__ static __forceinline__ double mass(float v) { double d = v; return d * d; }
+  __device__ static __forceinline__ double weight(float v) { double d = v; return d * d; }
+  __device__ static __forceinline__ double absval(float v) { return fabs((double)v); }
+  __device__ static __forceinline__ bool is_zero(float v) { return v == 0.0f; }
+  __device__ static __forceinline__ coef_t make_coef(float a) { return __fdiv_rn(1.0f, a); }
+  __device__ static __forceinline__ float scale(float c, coef_t k) { return __fmul_rn(c, k); }
+  __device__ static __forceinline__ float sub_outer(float r, float l, float p) {
+    return __fsub_rn(r, __fmul_rn(l, p));
+  }
+  __device__ static __forceinline__ float zero() { return 0.0f; }
+};
+
+template <> struct Scalar<double2> {
+  using coef_t = CDivCoef;
+  static constexpr int kVec = 1;
+  __device__ static __forceinline__ double mass(double2 v) { return v.x * v.x + v.y * v.y; }
+  __device__ static __forceinline__ double weight(double2 v) {
+    double a = cabs_np(v);
+    return __dmul_rn(a, a);
+  }
+  __device__ static __forceinline__ double absval(double2 v) { return cabs_np(v); }
+  __device__ static __forceinline__ bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+  __device__ static __forceinline__ coef_t make_coef(double2 a) { return cdiv_coef(a); }
+  __device__ static __forceinline__ double2 scale(double2 c, const coef_t& k) { return cdiv_apply(c, k); }
+  __device__ static __forceinline__ double2 sub_outer(double2 r, double2 l, double2 p) {
+    double2 q = cmul_np(l, p);
+    return make_double2(__dsub_rn(r.x, q.x), __dsub_rn(r.y, q.y));
+  }
+  __device__ static __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
+};
+
+// ---------------------------------------------------------------------------
+// warp / block primitives
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// argmax with lowest-index tie break (np.argmax semantics)
+__device__ __forceinline__ void argmax_merge(double& v, long long& i, double v2, long long i2) {
+  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, long long& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    argmax_merge(v, i, v2, i2);
+  }
+}
+
+// Shared scratch for the single-CTA select kernels.
+template <int BLOCK>
+struct CdfSmem {
+  double incl[BLOCK];  // inclusive chunk-boundary sums, incl[t] == excl[t+1]
+  double wsum[BLOCK / 32];
+  long long idx;
+  double val;
+  double lo_c, hi_c;
+  int flag;
+};
+
+// Block-wide inclusive scan of one double per thread.  Result: s.incl[tid].
+template <int BLOCK>
+__device__ __forceinline__ double block_incl_scan(double v, CdfSmem<BLOCK>& s) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s.wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    double t = (lane < BLOCK / 32) ? s.wsum[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < BLOCK / 32) s.wsum[lane] = t;  // inclusive warp totals
+  }
+  __syncthreads();
+  if (w > 0) x += s.wsum[w - 1];
+  s.incl[threadIdx.x] = x;
+  __syncthreads();
+  return x;
+}
+
+// Chunked CDF over n weights given by wf(k) (k in [0,n)), one CTA of BLOCK
+// threads.  Thread t owns rows [t*C, min((t+1)*C, n)) and sums them in index
+// order (the reference's np.cumsum is sequential; within a chunk we keep that
+// order).  Chunk boundaries come from the block scan.
+template <int BLOCK>
+struct Cdf {
+  long long lo, hi;
+  double excl, incl, total;
+};
+
+template <int BLOCK, typename WF>
+__device__ __forceinline__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
+  Cdf<BLOCK> c;
+  long long C = (n + BLOCK - 1) / BLOCK;
+  c.lo = min((long long)threadIdx.x * C, n);
+  c.hi = min(c.lo + C, n);
+  double acc = 0.0;
+  for (long long k = c.lo; k < c.hi; ++k) acc += wf(k);
+  c.incl = block_incl_scan<BLOCK>(acc, s);
+  c.excl = threadIdx.x ? s.incl[threadIdx.x - 1] : 0.0;
+  c.total = s.incl[BLOCK - 1];
+  return c;
+}
+
+// sample_index(w, u) on a built CDF.  Returns the index (block-uniform); the
+// CDF values bracketing the draw are left in s.lo_c / s.hi_c for the caller's
+// near-boundary accounting.
+template <int BLOCK, typename WF>
+__device__ long long cdf_find(const WF& wf, long long n, const Cdf<BLOCK>& c, double u,
+                              CdfSmem<BLOCK>& s) {
+  const double target = u * c.total;
+  if (threadIdx.x == 0) { s.idx = n; s.flag = 0; }
+  __syncthreads();
+  // lowest thread whose chunk upper boundary exceeds the target
+  int mine = (c.hi > c.lo && c.incl > target) ? (int)threadIdx.x : BLOCK;
+  // block min
+  int wm = mine;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+  __shared__ int warp_min[BLOCK / 32];
+  if ((threadIdx.x & 31) == 0) warp_min[threadIdx.x >> 5] = wm;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = (threadIdx.x < BLOCK / 32) ? warp_min[threadIdx.x] : BLOCK;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) warp_min[0] = v;
+  }
+  __syncthreads();
+  const int owner = warp_min[0];
+  if (owner < BLOCK && (int)threadIdx.x == owner) {
+    double acc = 0.0, prev = c.excl;
+    long long found = c.hi - 1;
+    double hi_c = c.incl;
+    for (long long k = c.lo; k < c.hi; ++k) {
+      acc += wf(k);
+      double ck = (k == c.hi - 1) ? c.incl : c.excl + acc;
+      if (ck > target) { found = k; hi_c = ck; break; }
+      prev = ck;
+    }
+    s.idx = found;
+    s.lo_c = prev;
+    s.hi_c = hi_c;
+  }
+  if (owner >= BLOCK && threadIdx.x == 0) {
+    // u*total >= every partial sum: searchsorted returns n, clamp to n-1
+    s.idx = n - 1;
+    s.lo_c = c.total;  // boundary at the top
+    s.hi_c = c.total;
+  }
+  __syncthreads();
+  long long i = s.idx;
+  // walk back over zero weights (rng.py:70-73)
+  double wi = wf(i);
+  __syncthreads();
+  if (!(wi > 0.0)) {
+    // largest k <= i with w(k) > 0, else smallest k with w(k) > 0
+    long long best_lo = -1, best_any = n;
+    for (long long k = threadIdx.x; k < n; k += BLOCK) {
+      if (wf(k) > 0.0) {
+        if (k <= i && k > best_lo) best_lo = k;
+        if (k < best_any) best_any = k;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      best_lo = max(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
+      best_any = min(best_any, __shfl_xor_sync(0xffffffffu, best_any, o));
+    }
+    __shared__ long long wlo[BLOCK / 32], wany[BLOCK / 32];
+    if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = best_lo; wany[threadIdx.x >> 5] = best_any; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long a = -1, b = n;
+      for (int w = 0; w < BLOCK / 32; ++w) { a = max(a, wlo[w]); b = min(b, wany[w]); }
+      s.idx = (a >= 0) ? a : b;
+    }
+    __syncthreads();
+    i = s.idx;
+    __syncthreads();
+  }
+  return i;
+}
+
+// Block argmax of wf(k) over [0,n) with lowest-index ties.
+template <int BLOCK, typename WF>
+__device__ long long block_argmax(const WF& wf, long long n, double* out_val) {
+  double v = -1.0;
+  long long idx = n;
+  for (long long k = threadIdx.x; k < n; k += BLOCK) argmax_merge(v, idx, wf(k), k);
+  warp_argmax(v, idx);
+  __shared__ double sv[BLOCK / 32];
+  __shared__ long long si[BLOCK / 32];
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = v; si[threadIdx.x >> 5] = idx; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = (threadIdx.x < BLOCK / 32) ? sv[threadIdx.x] : -1.0;
+    idx = (threadIdx.x < BLOCK / 32) ? si[threadIdx.x] : n;
+    warp_argmax(v, idx);
+    if (threadIdx.x == 0) { sv[0] = v; si[0] = idx; }
+  }
+  __syncthreads();
+  long long r = si[0];
+  if (out_val) *out_val = sv[0];
+  __syncthreads();
+  return r;
+}
+
+}  // namespace rplu

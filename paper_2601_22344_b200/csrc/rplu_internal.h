@@ -1,0 +1,71 @@
+// Internal (non-exported) declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/rplu_b200.h"
+
+namespace rplu {
+
+// Per-run device-resident control block.  One instance lives in device memory
+// for the whole pivot loop so no step needs a host round trip.
+struct DevState {
+  long long ucount;         // uniforms consumed so far
+  long long near_boundary;  // draws within 1e-12*total of a CDF boundary
+  long long pi, pj;         // pivot of the current step
+  long long err_i, err_j;   // zero pivot location
+  long long done;           // pivots committed
+  int active;               // 1 while the loop runs
+  int status;               // 0 running/ok, 1 clean stop, 2 tol stop, 3 degenerate,
+                            // -2 zero pivot, -1 uniform stream exhausted
+  double fro0;              // residual Frobenius norm at step 0 (or u0_max / total0)
+  // pivot coefficients of the current step
+  double inv_d;             // 1/a (real fp64)
+  float inv_f;              // 1/a (fp32)
+  int branch;               // complex Smith branch
+  double rat, scl;          // complex Smith coefficients
+  double a_re, a_im;        // pivot value
+  double aux[8];            // path-specific scratch (Cauchy / CUR)
+};
+
+enum Status {
+  kRunning = 0,
+  kCleanStop = 1,
+  kTolStop = 2,
+  kDegenerate = 3,
+  kUniformsExhausted = -1,
+  kZeroPivot = -2,
+};
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define RPLU_CUDA(call)                                        \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::rplu::cuda_fail(_e, #call); \
+  } while (0)
+
+// Grow-only device workspace owned by a context.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+};
+
+}  // namespace rplu
+
+struct rplu_ctx {
+  int device = 0;
+  int sm_count = 148;
+  rplu::DevBuf state;       // DevState
+  rplu::DevBuf masses;      // n doubles
+  rplu::DevBuf rowmax;      // n doubles (CPLU)
+  rplu::DevBuf rowarg;      // n int64 (CPLU)
+  rplu::DevBuf uniforms;    // device copy of the uniform stream
+  rplu::DevBuf pivots;      // 2*steps int64
+  rplu::DevBuf resid;       // steps+1 doubles
+  rplu::DevBuf scratch[8];  // path-specific
+};

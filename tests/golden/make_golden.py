@@ -1,0 +1,210 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (the reference is importable only here):
+
+    python tests/golden/make_golden.py [--c1]
+
+It imports ``rplu`` from /root/reference/pkg/src, runs its public entry
+points (eliminate, structured_eliminate, cur_build, sample_index) on seeded
+desk-size inputs and writes the inputs and outputs as small fixtures next to
+this script.  The fixtures pin the oracle (tests/test_oracle_golden.py) and
+the GPU path (tests/test_*_gpu.py).  ``--c1`` also records the reference's
+C1 run (2000 x 2000, r = 100, seeds 0..29): pivots, residual norms and
+||A - LU||_F / ||A||_F, plus a hash of the input bytes (the 32 MB inputs are
+regenerated from the seed, not committed).
+"""
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import rplu  # noqa: E402  (the reference)
+import scipy  # noqa: E402
+
+from paper_2601_22344_b200 import gen  # noqa: E402  (input constructors only)
+
+
+def meta():
+    return {"numpy": np.__version__, "scipy": scipy.__version__, "rplu": rplu.__version__}
+
+
+def _compact(a):
+    a = np.asarray(a)
+    if np.iscomplexobj(a) and not np.any(a.imag):
+        return np.ascontiguousarray(a.real)  # reference complex128 with zero imaginary part
+    return a
+
+
+def save(name, arrays, info):
+    arrays = {k: _compact(v) for k, v in arrays.items()}
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **arrays)
+    with open(os.path.join(HERE, name + ".json"), "w") as f:
+        json.dump({"meta": meta(), "cases": info}, f, indent=1)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def sample_index_cases():
+    arrays, info = {}, []
+    rs = np.random.default_rng(5)
+    vecs = [
+        np.array([1.0]),
+        np.array([0.0, 1.0, 0.0, 2.0, 0.0]),
+        np.array([3.0, 0.0, 0.0]),
+        np.array([0.0, 0.0, 5.0]),
+        np.array([1.0, 1.0, 1.0, 1.0]),
+        rs.random(1000) * (rs.random(1000) > 0.3),
+        rs.random(5000) ** 8,
+        np.concatenate([np.zeros(700), rs.random(3000), np.zeros(300)]),
+    ]
+    us = [0.0, 0.25, 0.5, 0.75, 1.0 - 2.0 ** -53, 0.123456789, 0.999999]
+    for k, w in enumerate(vecs):
+        out = []
+        for u in us:
+            out.append(rplu.sample_index(w, u))
+        # exact boundary draws: u*total == c_k for a few k
+        c = np.cumsum(w)
+        arrays[f"w{k}"] = w
+        arrays[f"idx{k}"] = np.array(out)
+        info.append({"key": f"w{k}", "us": us, "n": int(w.size), "total": float(c[-1])})
+    arrays["us"] = np.array(us)
+    save("sample_index", arrays, info)
+
+
+def dense_cases():
+    arrays, info = {}, []
+    cases = []
+    rs = np.random.default_rng(11)
+    cases.append(("diag2", np.eye(2), "rplu", 2, 3, 0.0))
+    cases.append(("cplu2", np.array([[1.0, 3.0], [2.0, 0.0]]), "cplu", 1, None, 0.0))
+    cases.append(("c8x6", rs.standard_normal((8, 6)) + 1j * rs.standard_normal((8, 6)), "rplu", 6, 1, 0.0))
+    cases.append(("real40x30", rs.standard_normal((40, 30)), "rplu", 30, 2, 0.0))
+    cases.append(("planted60", gen.planted_spectrum(60, 60, 0.3, 100), "rplu", 10, 7, 0.0))
+    cases.append(("planted60c2", gen.planted_spectrum(60, 60, 0.3, 101), "c2plu", 12, None, 0.0))
+    cases.append(("planted60cplu", gen.planted_spectrum(60, 60, 0.3, 102), "cplu", 12, None, 0.0))
+    cases.append(("rank3_clean", rs.standard_normal((20, 3)) @ rs.standard_normal((3, 25)),
+                  "rplu", 10, 4, 0.0))
+    cases.append(("diag5_clean", np.diag([5.0, 4.0, 3.0, 2.0, 1.0]), "rplu", 5, 9, 0.0))
+    cases.append(("tol_stop", gen.c1_dense(3, n=200), "rplu", 150, 3, 1e-2))
+    cases.append(("c1_small_real", gen.c1_dense(0, n=300, m=257), "rplu", 60, 0, 0.0))
+    cases.append(("c3_small_real", gen.c3_dense_host(0, n=512, m=384, reflectors=8), "rplu", 96, 0, 0.0))
+    cases.append(("c3_small_f32src", gen.c3_dense_host(1, n=256, reflectors=8).astype(np.float32),
+                  "rplu", 64, 1, 0.0))
+    for name, A, tag, steps, seed, tol in cases:
+        rule = rplu.PivotRule(tag, rplu.RngState(seed) if seed is not None else None)
+        tr = rplu.eliminate(A, rule, steps, stop_tol=tol)
+        after = rule.rng.uniform() if rule.rng is not None else None
+        arrays[name + "_A"] = A
+        arrays[name + "_L"] = tr.L
+        arrays[name + "_U"] = tr.U
+        arrays[name + "_resid_fro"] = tr.resid_fro
+        if tr.residual.size <= 4096:
+            arrays[name + "_residual"] = tr.residual
+        info.append({"name": name, "rule": tag, "steps": steps, "seed": seed, "stop_tol": tol,
+                     "pivots": [list(map(int, p)) for p in tr.pivots], "steps_done": tr.steps,
+                     "clean_early_stop": bool(tr.clean_early_stop), "tol_stop": bool(tr.tol_stop),
+                     "next_uniform": after})
+    save("dense", arrays, info)
+
+
+def cauchy_cases():
+    arrays, info = {}, []
+    rs = np.random.default_rng(21)
+    cases = []
+    x, y, G, B = gen.c2_cauchy(0, n=300)
+    cases.append(("c2_300", x, y, G, B, "rplu", 40, 9, 0.0))
+    x, y, G, B = gen.c4_cauchy_like(0, n=256, p=4)
+    cases.append(("c4_256", x, y, G, B, "rplu", 32, 3, 0.0))
+    x, y, G, B = gen.c4_cauchy_like(1, n=200, m=150, p=2)
+    cases.append(("c4_200x150_p2", x, y, G, B, "rplu", 30, 5, 0.0))
+    x, y, G, B = gen.c4_cauchy_like(2, n=128, p=3)
+    cases.append(("c4_128_c2plu", x, y, G, B, "c2plu", 20, None, 0.0))
+    x, y, G, B = gen.c2_cauchy(4, n=64)
+    cases.append(("c2_64_full", x, y, G, B, "rplu", 64, 4, 1e-9))
+    for name, x, y, G, B, rule, rank, seed, tol in cases:
+        M = rplu.CauchyLikeMatrix(x, y, G, B)
+        rng = rplu.RngState(seed) if seed is not None else None
+        tr = rplu.structured_eliminate(M, rule, rank, stop_tol=tol, rng=rng, keep_steps=True)
+        after = rng.uniform() if rng is not None else None
+        arrays[name + "_x"], arrays[name + "_y"] = x, y
+        arrays[name + "_G"], arrays[name + "_B"] = G, B
+        k = len(tr.row_indices)
+        if k:
+            arrays[name + "_c"] = np.stack([s[0] for s in tr.steps])
+            arrays[name + "_r"] = np.stack([s[1] for s in tr.steps])
+            arrays[name + "_a"] = np.array([s[2] for s in tr.steps])
+        arrays[name + "_norms0"] = rplu.exact_row_norms(M)
+        info.append({"name": name, "rule": rule, "rank": rank, "seed": seed, "stop_tol": tol,
+                     "rows": tr.row_indices, "cols": tr.col_indices,
+                     "bound_sums": tr.bound_sums, "bound_maxes": tr.bound_maxes,
+                     "tol_stop": tr.tol_stop, "degenerate_stop": tr.degenerate_stop,
+                     "next_uniform": after})
+    save("cauchy", arrays, info)
+
+
+class _Gauss(rplu.CallableOperator):
+    def __init__(self, P, Q, h=0.1):
+        d2 = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(-1)
+        K = np.exp(-d2 / (2 * h * h))
+        self.K = K
+        super().__init__(K.shape, lambda v: K @ v, lambda v: K.conj().T @ v,
+                         row_norms_fn=lambda: np.einsum("ij,ij->i", K, K))
+
+
+def cur_cases():
+    arrays, info = {}, []
+    cases = []
+    A = gen.planted_spectrum(60, 60, 0.3, 100)
+    cases.append(("planted60", rplu.DenseMatrix(A), A, "rplu-cur", 10, 7))
+    P, Q = gen.c5_points(0, n=400, m=300)
+    op = _Gauss(P, Q)
+    cases.append(("gauss400x300", op, op.K, "rplu-cur", 24, 3))
+    arrays["gauss400x300_P"], arrays["gauss400x300_Q"] = P, Q
+    A2 = gen.c1_dense(5, n=120, m=90)
+    cases.append(("c1_120x90", rplu.DenseMatrix(A2), A2, "rplu-cur", 30, 5))
+    cases.append(("c1_120x90_c2", rplu.DenseMatrix(A2), A2, "c2plu-cur", 20, None))
+    for name, acc, dense, rule, k, seed in cases:
+        rng = rplu.RngState(seed) if seed is not None else None
+        fact, inf = rplu.cur_build(acc, rule, k, rng=rng)
+        after = rng.uniform() if rng is not None else None
+        arrays[name + "_dense"] = dense
+        arrays[name + "_W"] = fact.core_matrix()
+        arrays[name + "_row_norms"] = inf.row_norms
+        info.append({"name": name, "rule": rule, "rank": k, "seed": seed,
+                     "I": fact.row_indices, "J": fact.col_indices,
+                     "total_sq_norms": inf.total_sq_norms, "clamped": inf.clamped,
+                     "rebuilds": inf.rebuilds, "degenerate_stop": inf.degenerate_stop,
+                     "tol_stop": inf.tol_stop, "next_uniform": after})
+    save("cur", arrays, info)
+
+
+def c1_runs(seeds=range(30), steps=100):
+    out = []
+    for s in seeds:
+        A = gen.c1_dense(s)
+        tr = rplu.eliminate(A, rplu.PivotRule("rplu", rplu.RngState(s)), steps)
+        err = float(np.linalg.norm(A - tr.L @ tr.U) / np.linalg.norm(A))
+        out.append({"seed": s, "sha256": sha(A), "pivots": [list(map(int, p)) for p in tr.pivots],
+                    "resid_fro": [float(v) for v in tr.resid_fro], "rel_err": err})
+        print("c1 seed", s, err, tr.pivots[:2], flush=True)
+    with open(os.path.join(HERE, "c1_reference.json"), "w") as f:
+        json.dump({"meta": meta(), "n": 2000, "steps": steps, "runs": out}, f)
+
+
+if __name__ == "__main__":
+    sample_index_cases()
+    dense_cases()
+    cauchy_cases()
+    cur_cases()
+    if "--c1" in sys.argv:
+        c1_runs()
