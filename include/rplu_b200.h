@@ -115,6 +115,56 @@ int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* o
 int rplu_row_masses(rplu_ctx* ctx, int32_t dtype, const void* R, int64_t n, int64_t m,
                     int64_t ld, double* masses, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Cauchy-like structured elimination, exact row norms (structured_eliminate,
+ * plan=None).  Entries A_ij = (G_i . B_:,j) / (x_i - y_j), complex128.      */
+
+typedef struct rplu_cauchy_args {
+  int32_t rule;           /* RPLU_RULE_RPLU | RPLU_RULE_C2PLU */
+  int32_t p;              /* displacement rank, 1..8 */
+  int64_t n, m;           /* shape */
+  int64_t rank;           /* pivots requested, 0 <= rank <= min(n, m) */
+  double stop_tol;        /* stop when max_i u_i <= stop_tol^2 * max_i u_i^(0) */
+  const void* x;          /* device complex128[n] */
+  const void* y;          /* device complex128[m] */
+  void* G;                /* device complex128 n x p row-major; updated in place */
+  void* Bt;               /* device complex128 m x p row-major (column j of B
+                             contiguous = the reference's F-order B); updated */
+  void* C;                /* device complex128 rank x n: column c of each step, or NULL */
+  void* Rrow;             /* device complex128 rank x m: row r of each step, or NULL */
+  void* a;                /* device complex128[rank]: pivot values, or NULL */
+  const double* uniforms; /* host uniform stream (rule rplu; 3*rank suffices) */
+  int64_t n_uniforms;
+  void* stream;
+  int32_t flags;          /* RPLU_FLAG_* */
+  int32_t reserved;
+} rplu_cauchy_args;
+
+typedef struct rplu_cauchy_out {
+  int64_t* rows;          /* host, caller-owned, >= rank: pivot rows */
+  int64_t* cols;          /* host, caller-owned, >= rank: pivot columns */
+  double* bound_maxes;    /* host, >= rank: max_i u_i at the start of each step */
+  double* bound_sums;     /* host, >= rank: sum_i u_i at the start of each step */
+  int64_t steps_done;
+  int64_t bounds_recorded;
+  int64_t uniforms_consumed;
+  int64_t near_boundary_draws;
+  int32_t tol_stop;
+  int32_t degenerate_stop;
+  int64_t zero_pivot_i, zero_pivot_j;
+  double masses_ms;       /* RPLU_FLAG_TIME_KERNELS: CUDA-event time of K5 */
+  int64_t masses_launches;
+  int64_t kernel_launches;
+} rplu_cauchy_out;
+
+int rplu_cauchy_run(rplu_ctx* ctx, const rplu_cauchy_args* args, rplu_cauchy_out* out);
+
+/* exact_row_norms (cauchy.py:129-137): u_i = sum_j |G_i.B_:,j / (x_i-y_j)|^2
+ * into the device array `out` (n doubles). */
+int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                          const void* y, const void* G, const void* Bt, double* out,
+                          void* stream);
+
 /* sample_index(weights, u) on a device weight vector (rng.py:50-74):
  * first index whose running sum exceeds u*total, top clamp, walk-back over
  * zero weights.  RPLU_ERR_ARG for empty / negative / all-zero weights.

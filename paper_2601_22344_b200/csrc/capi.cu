@@ -42,6 +42,9 @@ int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long l
                     long long ld, double* masses, cudaStream_t s);
 int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
                       int* near, cudaStream_t s);
+int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out);
+int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
+                      const void* G, const void* Bt, double* out, cudaStream_t s);
 
 // Bind the calling thread to the context's device for the duration of a call.
 struct DeviceGuard {
@@ -167,6 +170,73 @@ int rplu_row_masses(rplu_ctx* ctx, int32_t dtype, const void* R, int64_t n, int6
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
   return row_masses_impl(ctx, dtype, R, n, m, ld, masses, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Validation mirrors structured_eliminate (cauchy.py:193-199) and
+// CauchyLikeMatrix (:59-66).
+int rplu_cauchy_run(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out) {
+  if (!ctx || !a || !out) { set_error("rplu_cauchy_run: NULL argument"); return RPLU_ERR_ARG; }
+  if (a->rule != RPLU_RULE_RPLU && a->rule != RPLU_RULE_C2PLU) {
+    set_error("unknown structured rule id " + std::to_string(a->rule));
+    return RPLU_ERR_ARG;
+  }
+  if (a->p < 1 || a->p > 8) {
+    set_error("displacement rank " + std::to_string(a->p) + " exceeds 8");
+    return RPLU_ERR_ARG;
+  }
+  if (a->n < 1 || a->m < 1) { set_error("rplu_cauchy_run: empty shape"); return RPLU_ERR_ARG; }
+  const int64_t kmax = a->n < a->m ? a->n : a->m;
+  if (a->rank < 0 || a->rank > kmax) {
+    set_error("rank " + std::to_string(a->rank) + " out of range [0, " + std::to_string(kmax) +
+              "]");
+    return RPLU_ERR_ARG;
+  }
+  if (!a->x || !a->y || !a->G || !a->Bt) {
+    set_error("rplu_cauchy_run: NULL generator buffer");
+    return RPLU_ERR_ARG;
+  }
+  if (a->rule == RPLU_RULE_RPLU && a->rank > 0 && (!a->uniforms || a->n_uniforms < 2)) {
+    set_error("structured rplu needs an RngState");
+    return RPLU_ERR_ARG;
+  }
+  if (a->rank > 0 && (!out->rows || !out->cols || !out->bound_maxes || !out->bound_sums)) {
+    set_error("rplu_cauchy_run: NULL output array");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  if (a->rank == 0) {
+    out->steps_done = out->bounds_recorded = 0;
+    out->uniforms_consumed = out->near_boundary_draws = 0;
+    out->tol_stop = out->degenerate_stop = 0;
+    out->kernel_launches = 0;
+    return RPLU_OK;
+  }
+  int st = cauchy_run_impl(ctx, a, out);
+  if (st == RPLU_ERR_CUDA || st == RPLU_ERR_ARG) return st;
+  if (st == kZeroPivot) {
+    set_error("pivot (" + std::to_string(out->zero_pivot_i) + ", " +
+              std::to_string(out->zero_pivot_j) + ") is numerically zero" +
+              (a->rule == RPLU_RULE_RPLU ? " after resampling" : ""));
+    return RPLU_ERR_ZERO_PIVOT;
+  }
+  if (st == kUniformsExhausted) {
+    set_error("uniform stream exhausted (pass at least 3*rank uniforms)");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                          const void* y, const void* G, const void* Bt, double* out,
+                          void* stream) {
+  if (!ctx || !x || !y || !G || !Bt || !out || n < 1 || m < 1 || p < 1 || p > 8) {
+    set_error("rplu_cauchy_row_norms: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_norms_impl(ctx, p, n, m, x, y, G, Bt, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,

@@ -1,0 +1,579 @@
+// Cauchy-like structured RPLU (Alg 3, exact row norms) — K5 generated-entry
+// row masses, K6 pivot row / column generation and generator update.
+//
+// Reference: rplu.cauchy.structured_eliminate, plan=None branch
+// (pkg/src/rplu/cauchy.py:177-256):
+//   u = exact_row_norms(cur) (:209-210, :129-137), bound_maxes/sums (:211-214),
+//   degenerate / tol stops (:217-222), i = sample_index(u, u1) (:228),
+//   r = row(i) (:82-83), j = sample_index(|r|^2, u2) (:236), relative zero-pivot
+//   guard with one resample (:237-245), c = column(j) (:85-86),
+//   G -= outer(c/a, G_i), B -= outer(B_:,j, r/a) (:247-250).
+//
+// Device layout (complex128 = double2): x[n], y[m]; G row-major n x P (the
+// reference's C-order G); Bt row-major m x P, i.e. column j of B contiguous
+// (the reference's F-order B).  No matrix is ever stored: K5 regenerates
+// every entry (G_i . B_j) / (x_i - y_j) from registers (row side) and a shared
+// memory tile of (y_j, B_j) (column side), so a step is FP64-pipe bound.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "rplu_common.cuh"
+#include "rplu_internal.h"
+
+namespace rplu {
+
+constexpr double kPivotRelTol = 1e-14;  // cauchy.py:33
+
+struct CauchyParams {
+  long long n, m, rank;
+  int p;
+  const double2* x;
+  const double2* y;
+  double2* G;
+  double2* Bt;
+  double* partial;   // [splits][n] partial row masses
+  int splits;
+  double2* rbuf;     // row r of the current step (m)
+  double* wbuf;      // |r|^2 (m)
+  double2* Cout;     // keep_steps: rank x n (or null)
+  double2* Rout;     // keep_steps: rank x m (or null)
+  double2* Aout;     // keep_steps: rank (or null)
+  DevState* st;
+  long long t;
+  const double* uniforms;
+  long long n_uniforms;
+  long long* rows;
+  long long* cols;
+  double* bmax;
+  double* bsum;
+  double stop_tol;
+  int rule;
+};
+
+// ---------------------------------------------------------------------------
+// fast FP64 reciprocal: MUFU.RCP64H seed + two Newton steps (DFMA)
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// K5: partial[s][i] = sum_{j in split s} |G_i . B_j|^2 / |x_i - y_j|^2
+template <int P, int RPT, int TJ>
+__global__ void __launch_bounds__(256) cauchy_mass_kernel(CauchyParams q) {
+  constexpr int NT = 256;
+  if (q.st && !q.st->active) return;
+  __shared__ double2 sy[TJ];
+  __shared__ double2 sb[TJ * P];
+  const long long row_base = (long long)blockIdx.x * NT * RPT;
+  // this CTA's column range
+  const long long cols_per = (q.m + q.splits - 1) / q.splits;
+  const long long j0 = (long long)blockIdx.y * cols_per;
+  const long long j1 = min(q.m, j0 + cols_per);
+
+  double2 g[RPT][P];
+  double2 xr[RPT];
+  double acc[RPT];
+  bool valid[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    valid[r] = i < q.n;
+    long long ii = valid[r] ? i : 0;
+    xr[r] = q.x[ii];
+#pragma unroll
+    for (int l = 0; l < P; ++l) g[r][l] = q.G[ii * P + l];
+    acc[r] = 0.0;
+  }
+  for (long long jt = j0; jt < j1; jt += TJ) {
+    const int cnt = (int)min((long long)TJ, j1 - jt);
+    __syncthreads();
+    for (int c = threadIdx.x; c < TJ; c += NT) {
+      if (c < cnt) {
+        sy[c] = q.y[jt + c];
+#pragma unroll
+        for (int l = 0; l < P; ++l) sb[c * P + l] = q.Bt[(jt + c) * P + l];
+      }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int c = 0; c < cnt; ++c) {
+      const double2 yj = sy[c];
+      double2 b[P];
+#pragma unroll
+      for (int l = 0; l < P; ++l) b[l] = sb[c * P + l];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          re = fma(g[r][l].x, b[l].x, re);
+          re = fma(-g[r][l].y, b[l].y, re);
+          im = fma(g[r][l].x, b[l].y, im);
+          im = fma(g[r][l].y, b[l].x, im);
+        }
+        const double dr = xr[r].x - yj.x, di = xr[r].y - yj.y;
+        const double num = fma(re, re, im * im);
+        const double den = fma(dr, dr, di * di);
+        acc[r] = fma(num, rcp_nr(den), acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    if (valid[r]) q.partial[(long long)blockIdx.y * q.n + i] = acc[r];
+  }
+}
+
+// Sum the split partials into masses (used by exact_row_norms).
+__global__ void sum_partials_kernel(const double* partial, int splits, long long n, double* out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += partial[(long long)k * n + i];
+  out[i] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K2a: row selection + stop rules.
+__global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q) {
+  constexpr int B = 1024;
+  DevState* st = q.st;
+  if (!st->active) return;
+  __shared__ CdfSmem<B> sm;
+  __shared__ int s_stop;
+  __shared__ double s_max[B / 32];
+  const long long n = q.n, t = q.t;
+  const double* part = q.partial;
+  const int S = q.splits;
+  auto wrow = [&](long long k) {
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += part[(long long)z * n + k];
+    return s;
+  };
+  Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+  // umax over rows
+  double mx = 0.0;
+  for (long long k = cr.lo; k < cr.hi; ++k) mx = fmax(mx, wrow(k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double umax = 0.0;
+    for (int w = 0; w < B / 32; ++w) umax = fmax(umax, s_max[w]);
+    q.bmax[t] = umax;
+    q.bsum[t] = cr.total;
+    if (t == 0) st->fro0 = umax;
+    const double u0 = (t == 0) ? umax : st->fro0;
+    int stop = 0;
+    if (umax <= 0.0) {
+      st->status = kDegenerate;
+      stop = 1;
+    } else if (q.stop_tol > 0.0 && umax <= q.stop_tol * q.stop_tol * u0) {
+      st->status = kTolStop;
+      stop = 1;
+    }
+    if (stop) st->active = 0;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) return;
+  long long i;
+  long long uc = st->ucount;
+  if (q.rule == RPLU_RULE_RPLU) {
+    if (uc + 1 > q.n_uniforms) {
+      if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
+      return;
+    }
+    const double u1 = q.uniforms[uc];
+    i = cdf_find<B>(wrow, n, cr, u1, sm);
+    if (threadIdx.x == 0) {
+      const double tol = kNearBoundaryRel * cr.total, tg = u1 * cr.total;
+      if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) st->near_boundary++;
+      st->ucount = uc + 1;
+    }
+  } else {
+    i = block_argmax<B>(wrow, n, nullptr);
+  }
+  if (threadIdx.x == 0) st->pi = i;
+}
+
+// ---------------------------------------------------------------------------
+// K6a: pivot row r_j = (G_i . B_j) / (x_i - y_j) for all j, weights |r_j|^2.
+// numpy order: matmul then complex division (Smith).
+template <int P>
+__global__ void cauchy_row_kernel(CauchyParams q) {
+  if (!q.st->active) return;
+  const long long i = q.st->pi;
+  double2 gi[P];
+#pragma unroll
+  for (int l = 0; l < P; ++l) gi[l] = q.G[i * P + l];
+  const double2 xi = q.x[i];
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < q.m;
+       j += (long long)gridDim.x * blockDim.x) {
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+      const double2 b = q.Bt[j * P + l];
+      re = fma(gi[l].x, b.x, fma(-gi[l].y, b.y, re));
+      im = fma(gi[l].x, b.y, fma(gi[l].y, b.x, im));
+    }
+    const double2 yj = q.y[j];
+    const double2 d = make_double2(xi.x - yj.x, xi.y - yj.y);
+    const double2 r = cdiv_np(make_double2(re, im), d);
+    q.rbuf[j] = r;
+    const double a = cabs_np(r);
+    q.wbuf[j] = a * a;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: column selection with the relative zero-pivot guard; captures G_i and
+// B_j (pre-update) and 1/a coefficients into the state for the update.
+__global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q) {
+  constexpr int B = 1024;
+  DevState* st = q.st;
+  if (!st->active) return;
+  __shared__ CdfSmem<B> sm;
+  __shared__ double s_max[B / 32];
+  const long long m = q.m, t = q.t;
+  const double* w = q.wbuf;
+  auto wcol = [&](long long k) { return w[k]; };
+  auto wabs = [&](long long k) { return cabs_np(q.rbuf[k]); };
+  // max |r| for the relative threshold
+  double mx = 0.0;
+  for (long long k = threadIdx.x; k < m; k += B) mx = fmax(mx, wabs(k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  double rmax = 0.0;
+  for (int k = 0; k < B / 32; ++k) rmax = fmax(rmax, s_max[k]);
+  const double thr = kPivotRelTol * rmax;
+  long long j;
+  long long uc = st->ucount;
+  long long near = 0;
+  if (q.rule == RPLU_RULE_RPLU) {
+    Cdf<B> cc = cdf_build<B>(wcol, m, sm);
+    int attempt = 0;
+    for (;;) {
+      if (uc + 1 > q.n_uniforms) {
+        if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
+        return;
+      }
+      const double u2 = q.uniforms[uc];
+      uc += 1;
+      j = cdf_find<B>(wcol, m, cc, u2, sm);
+      if (threadIdx.x == 0) {
+        const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+        if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+      }
+      __syncthreads();
+      if (wabs(j) > thr) break;
+      if (attempt++ == 1) {
+        if (threadIdx.x == 0) {
+          st->status = kZeroPivot;
+          st->active = 0;
+          st->err_i = st->pi;
+          st->err_j = j;
+          st->ucount = uc;
+          st->near_boundary += near;
+        }
+        return;
+      }
+    }
+  } else {
+    j = block_argmax<B>(wabs, m, nullptr);
+    if (!(wabs(j) > thr)) {
+      if (threadIdx.x == 0) {
+        st->status = kZeroPivot;
+        st->active = 0;
+        st->err_i = st->pi;
+        st->err_j = j;
+      }
+      return;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const long long i = st->pi;
+    const double2 a = q.rbuf[j];
+    st->pj = j;
+    st->ucount = uc;
+    st->near_boundary += near;
+    st->a_re = a.x;
+    st->a_im = a.y;
+    const CDivCoef cf = cdiv_coef(a);
+    st->rat = cf.rat;
+    st->scl = cf.scl;
+    st->branch = cf.branch;
+    // pre-update generator row G_i and column B_j (P <= 8 -> 16 doubles in aux)
+    // are captured by the update kernel itself from its own registers; record
+    // the step here.
+    q.rows[t] = i;
+    q.cols[t] = j;
+    if (q.Aout) q.Aout[t] = a;
+    st->done = t + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6b: c_k = (G_k . B_j)/(x_k - y_j); G_k -= (c_k/a) G_i  (k < n)
+//      B_l -= B_j (r_l/a)                                 (l < m)
+// G_i and B_j are read from a snapshot taken before any CTA writes (gsnap).
+template <int P>
+__global__ void cauchy_update_kernel(CauchyParams q, const double2* __restrict__ gsnap) {
+  if (!q.st->active) return;
+  const long long j = q.st->pj;
+  CDivCoef cf;
+  cf.rat = q.st->rat;
+  cf.scl = q.st->scl;
+  cf.branch = q.st->branch;
+  double2 gi[P], bj[P];
+#pragma unroll
+  for (int l = 0; l < P; ++l) {
+    gi[l] = gsnap[l];
+    bj[l] = gsnap[P + l];
+  }
+  const double2 yj = q.y[j];
+  const long long total = q.n + q.m;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (long long)gridDim.x * blockDim.x) {
+    if (k < q.n) {
+      double2 g[P];
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        g[l] = q.G[k * P + l];
+        re = fma(g[l].x, bj[l].x, fma(-g[l].y, bj[l].y, re));
+        im = fma(g[l].x, bj[l].y, fma(g[l].y, bj[l].x, im));
+      }
+      const double2 xk = q.x[k];
+      const double2 c = cdiv_np(make_double2(re, im), make_double2(xk.x - yj.x, xk.y - yj.y));
+      if (q.Cout) q.Cout[q.t * q.n + k] = c;
+      const double2 ca = cdiv_apply(c, cf);
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double2 pr = cmul_np(ca, gi[l]);
+        q.G[k * P + l] = make_double2(__dsub_rn(g[l].x, pr.x), __dsub_rn(g[l].y, pr.y));
+      }
+    } else {
+      const long long l2 = k - q.n;
+      const double2 r = q.rbuf[l2];
+      if (q.Rout) q.Rout[q.t * q.m + l2] = r;
+      const double2 ra = cdiv_apply(r, cf);
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double2 b = q.Bt[l2 * P + l];
+        const double2 pr = cmul_np(bj[l], ra);
+        q.Bt[l2 * P + l] = make_double2(__dsub_rn(b.x, pr.x), __dsub_rn(b.y, pr.y));
+      }
+    }
+  }
+}
+
+// snapshot G_i and B_j (2P complex) before the update kernel overwrites them
+__global__ void cauchy_snapshot_kernel(CauchyParams q, double2* gsnap) {
+  if (!q.st->active) return;
+  const int l = threadIdx.x;
+  if (l < q.p) {
+    gsnap[l] = q.G[q.st->pi * q.p + l];
+    gsnap[q.p + l] = q.Bt[q.st->pj * q.p + l];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+static int choose_splits(long long n, long long m, int rows_per_cta, int sm_count) {
+  long long row_blocks = (n + rows_per_cta - 1) / rows_per_cta;
+  long long want = 4LL * sm_count;  // CTAs for latency-bound sizes
+  long long s = (want + row_blocks - 1) / row_blocks;
+  long long max_s = (m + 255) / 256;  // at least 256 columns per split
+  if (s > max_s) s = max_s;
+  if (s < 1) s = 1;
+  if (s > 1024) s = 1024;
+  return (int)s;
+}
+
+template <int P>
+static void launch_mass(CauchyParams& q, cudaStream_t s) {
+  constexpr int RPT = (P <= 4) ? 2 : 1;
+  constexpr int TJ = 128;
+  dim3 grid((unsigned)((q.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)q.splits);
+  cauchy_mass_kernel<P, RPT, TJ><<<grid, 256, 0, s>>>(q);
+}
+
+#define RPLU_P_SWITCH(p, CALL)      \
+  switch (p) {                      \
+    case 1: { constexpr int PP = 1; CALL; } break; \
+    case 2: { constexpr int PP = 2; CALL; } break; \
+    case 3: { constexpr int PP = 3; CALL; } break; \
+    case 4: { constexpr int PP = 4; CALL; } break; \
+    case 5: { constexpr int PP = 5; CALL; } break; \
+    case 6: { constexpr int PP = 6; CALL; } break; \
+    case 7: { constexpr int PP = 7; CALL; } break; \
+    case 8: { constexpr int PP = 8; CALL; } break; \
+    default: break;                 \
+  }
+
+static int rows_per_cta(int p) { return 256 * ((p <= 4) ? 2 : 1); }
+
+int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
+                      const void* G, const void* Bt, double* out, cudaStream_t s) {
+  CauchyParams q{};
+  q.n = n;
+  q.m = m;
+  q.p = p;
+  q.x = reinterpret_cast<const double2*>(x);
+  q.y = reinterpret_cast<const double2*>(y);
+  q.G = reinterpret_cast<double2*>(const_cast<void*>(G));
+  q.Bt = reinterpret_cast<double2*>(const_cast<void*>(Bt));
+  q.splits = choose_splits(n, m, rows_per_cta(p), ctx->sm_count);
+  int rc;
+  if ((rc = ctx->scratch[0].ensure(sizeof(double) * (size_t)q.splits * n))) return rc;
+  q.partial = reinterpret_cast<double*>(ctx->scratch[0].ptr);
+  q.st = nullptr;
+  RPLU_P_SWITCH(p, launch_mass<PP>(q, s));
+  sum_partials_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(q.partial, q.splits, n, out);
+  RPLU_CUDA(cudaGetLastError());
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  return RPLU_OK;
+}
+
+__global__ void cauchy_init_state(DevState* st) {
+  st->ucount = 0;
+  st->near_boundary = 0;
+  st->pi = st->pj = -1;
+  st->err_i = st->err_j = -1;
+  st->active = 1;
+  st->status = kRunning;
+  st->fro0 = 0.0;
+  st->done = 0;
+}
+
+int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  const long long n = a->n, m = a->m, K = a->rank;
+  const int p = a->p;
+  int rc;
+  CauchyParams q{};
+  q.n = n;
+  q.m = m;
+  q.rank = K;
+  q.p = p;
+  q.x = reinterpret_cast<const double2*>(a->x);
+  q.y = reinterpret_cast<const double2*>(a->y);
+  q.G = reinterpret_cast<double2*>(a->G);
+  q.Bt = reinterpret_cast<double2*>(a->Bt);
+  q.splits = choose_splits(n, m, rows_per_cta(p), ctx->sm_count);
+  q.stop_tol = a->stop_tol;
+  q.rule = a->rule;
+  if ((rc = ctx->scratch[0].ensure(sizeof(double) * (size_t)q.splits * n))) return rc;
+  if ((rc = ctx->scratch[1].ensure(sizeof(double2) * (size_t)m))) return rc;
+  if ((rc = ctx->scratch[2].ensure(sizeof(double) * (size_t)m))) return rc;
+  if ((rc = ctx->scratch[3].ensure(sizeof(double2) * 16))) return rc;
+  if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
+  if ((rc = ctx->pivots.ensure(sizeof(long long) * (size_t)(2 * K + 2)))) return rc;
+  if ((rc = ctx->resid.ensure(sizeof(double) * (size_t)(2 * K + 2)))) return rc;
+  long long nu = (a->rule == RPLU_RULE_RPLU) ? a->n_uniforms : 0;
+  if ((rc = ctx->uniforms.ensure(sizeof(double) * (size_t)(nu > 0 ? nu : 1)))) return rc;
+  if (nu > 0)
+    RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * nu,
+                              cudaMemcpyHostToDevice, s));
+  q.partial = reinterpret_cast<double*>(ctx->scratch[0].ptr);
+  q.rbuf = reinterpret_cast<double2*>(ctx->scratch[1].ptr);
+  q.wbuf = reinterpret_cast<double*>(ctx->scratch[2].ptr);
+  double2* gsnap = reinterpret_cast<double2*>(ctx->scratch[3].ptr);
+  q.Cout = reinterpret_cast<double2*>(a->C);
+  q.Rout = reinterpret_cast<double2*>(a->Rrow);
+  q.Aout = reinterpret_cast<double2*>(a->a);
+  q.st = reinterpret_cast<DevState*>(ctx->state.ptr);
+  q.uniforms = reinterpret_cast<const double*>(ctx->uniforms.ptr);
+  q.n_uniforms = nu;
+  long long* piv = reinterpret_cast<long long*>(ctx->pivots.ptr);
+  q.rows = piv;
+  q.cols = piv + K + 1;
+  double* bb = reinterpret_cast<double*>(ctx->resid.ptr);
+  q.bmax = bb;
+  q.bsum = bb + K + 1;
+  cauchy_init_state<<<1, 1, 0, s>>>(q.st);
+
+  const bool timing = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
+  std::vector<cudaEvent_t> ev;
+  long long launches = 1;
+  const int upd_blocks = (int)std::min<long long>((n + m + 255) / 256, 8LL * ctx->sm_count);
+  const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
+  for (long long t = 0; t < K; ++t) {
+    q.t = t;
+    if (timing) {
+      cudaEvent_t e0;
+      cudaEventCreate(&e0);
+      cudaEventRecord(e0, s);
+      ev.push_back(e0);
+    }
+    RPLU_P_SWITCH(p, launch_mass<PP>(q, s));
+    if (timing) {
+      cudaEvent_t e1;
+      cudaEventCreate(&e1);
+      cudaEventRecord(e1, s);
+      ev.push_back(e1);
+    }
+    cauchy_select_row_kernel<<<1, 1024, 0, s>>>(q);
+    RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, s>>>(q)));
+    cauchy_select_col_kernel<<<1, 1024, 0, s>>>(q);
+    cauchy_snapshot_kernel<<<1, 32, 0, s>>>(q, gsnap);
+    RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, s>>>(q, gsnap)));
+    launches += 6;
+  }
+  RPLU_CUDA(cudaGetLastError());
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, q.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  const long long done = hs.done;
+  // bounds are recorded for every step that started (done, plus the stopping one)
+  long long nb = done + ((hs.status == kTolStop || hs.status == kDegenerate ||
+                          hs.status == kZeroPivot) ? 1 : 0);
+  if (nb > K) nb = K;
+  if (done > 0) {
+    RPLU_CUDA(cudaMemcpy(out->rows, q.rows, sizeof(long long) * done, cudaMemcpyDeviceToHost));
+    RPLU_CUDA(cudaMemcpy(out->cols, q.cols, sizeof(long long) * done, cudaMemcpyDeviceToHost));
+  }
+  if (nb > 0) {
+    RPLU_CUDA(cudaMemcpy(out->bound_maxes, q.bmax, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    RPLU_CUDA(cudaMemcpy(out->bound_sums, q.bsum, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+  }
+  out->steps_done = done;
+  out->bounds_recorded = nb;
+  out->uniforms_consumed = hs.ucount;
+  out->near_boundary_draws = hs.near_boundary;
+  out->tol_stop = hs.status == kTolStop;
+  out->degenerate_stop = hs.status == kDegenerate;
+  out->zero_pivot_i = hs.err_i;
+  out->zero_pivot_j = hs.err_j;
+  out->kernel_launches = launches;
+  out->masses_ms = 0.0;
+  out->masses_launches = 0;
+  if (timing) {
+    for (size_t k = 0; k + 1 < ev.size(); k += 2) {
+      if ((long long)(k / 2) >= nb) break;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      out->masses_ms += ms;
+      out->masses_launches++;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  return hs.status;
+}
+
+}  // namespace rplu
