@@ -38,6 +38,11 @@ CONFIGS = {
                   n=32768, rank=512, dtype="f32", seed=0),
     "c1": dict(desc="C1 dense fp64 2000x2000 rank 100 (BASELINE configs[0])",
                n=2000, rank=100, dtype="f64", seed=0, kind="c1"),
+    "c2": dict(desc="C2 Cauchy c128 4096x4096 p=1 rank 200, exact norms (BASELINE configs[1])",
+               n=4096, rank=200, dtype="c128", seed=0, kind="cauchy", p=1),
+    "c4": dict(desc="C4 Cauchy-like c128 2^20 x 2^20 p=4 (BASELINE configs[3]); bench step = "
+                    "`rank` pivot steps of the rank-256 run",
+               n=1 << 20, rank=4, dtype="c128", seed=0, kind="cauchy", p=4),
 }
 METRIC = "RPLU pivot steps/sec at rank k; dense Schur step HBM GB/s vs B200 peak"
 UNIT = "pivot steps/s"
@@ -177,8 +182,111 @@ def run_reference_arm(args, cfg, rank_id):
     print(json.dumps(line), flush=True)
 
 
+def _cauchy_input(cfg):
+    from paper_2601_22344_b200 import gen
+    if cfg["p"] == 1:
+        return gen.c2_cauchy(cfg["seed"], n=cfg["n"])
+    return gen.c4_cauchy_like(cfg["seed"], n=cfg["n"], p=cfg["p"])
+
+
+def run_cauchy_arm(args, cfg):
+    """Cauchy-like exact-norm path (structured_eliminate, plan=None)."""
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _ffi
+    torch.cuda.set_device(0)
+    n, rank, seed, p = cfg["n"], cfg["rank"], cfg["seed"], cfg["p"]
+    x, y, G, B = _cauchy_input(cfg)
+    M = rp.CauchyLikeMatrix(x, y, G, B, check_points=False)
+
+    def one_run(tk=False, mat=M):
+        return rp.structured_eliminate(mat, "rplu", rank, rng=rp.RngState(seed),
+                                       time_kernels=tk)
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    ev0.record()
+    for _ in range(args.steps):
+        tr = one_run(True)
+        stats.append(tr.kernel_stats)
+    ev1.record()
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    k = tr.rank
+    value = args.steps * k / (total_ms / 1e3)
+    mass_ms = sum(s["masses_ms"] for s in stats)
+    mass_n = sum(s["masses_launches"] for s in stats)
+    flops = float(n) * n * (8 * p + 8)
+    avg_s = mass_ms / mass_n / 1e3
+    achieved = flops / avg_s / 1e12
+    peak = _ffi.fp64_peak_tflops(0)
+    # e2e: host generators in, host trace out (the reference-facing call)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    Mh = rp.CauchyLikeMatrix(x, y, G, B, check_points=False)
+    trh = rp.structured_eliminate(Mh, "rplu", rank, rng=rp.RngState(seed), keep_steps=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = 16 * (n + n + n * p + n * p)
+    d2h = 16 * trh.rank * (2 * n + 1) + 16 * trh.rank + 16 * trh.rank
+    # CPU baseline: oracle port, bounded sample of pivot steps on the same bytes
+    model, cores = _cpu_info()
+    cpu_k = 3 if n > 8192 else 10
+    if n > 65536:
+        # a full-size oracle step is ~2e4 s: time exact_row_norms on a row
+        # sample and extrapolate per step (labelled)
+        rows = 64
+        t0 = time.perf_counter()
+        oracle.exact_row_norms(x[:rows], y, G[:rows], B)
+        dt = time.perf_counter() - t0
+        cb_v = 1.0 / (dt * n / rows)
+        sample = (f"exact_row_norms on {rows} of {n} rows ({dt:.1f}s), extrapolated to one "
+                  f"full step (the step is 99.8% row norms); 1 thread (numpy)")
+    else:
+        t0 = time.perf_counter()
+        oracle.structured_eliminate(x, y, G, B, "rplu", cpu_k, seed=seed)
+        dt = time.perf_counter() - t0
+        cb_v = cpu_k / dt
+        sample = f"{cpu_k} pivot steps of the oracle port on the same bytes ({dt:.1f}s)"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded BASELINE construction)",
+        "config": {"workload": cfg["desc"], "n": n, "m": n, "p": p, "rank": rank, "seed": seed,
+                   "step": f"one structured_eliminate run of {rank} pivot steps",
+                   "l2": "generated entries; no matrix in HBM"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "cauchy_mass_kernel (K5 generated-entry row masses)",
+                     "algorithmic_flops_per_launch": flops, "avg_launch_ms": avg_s * 1e3,
+                     "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)"},
+        "step_breakdown_ms": {"masses_per_pivot": mass_ms / mass_n,
+                              "total_per_pivot": total_ms / (args.steps * k)},
+        "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample + f"; CPU: {model}"},
+        "e2e": {"value": trh.rank / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": sum(s["kernel_launches"] for s in stats),
+        "near_boundary_draws": tr.near_boundary_draws,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200_arm(args, cfg, dist, rank_id, world):
     import torch
+    if cfg.get("kind") == "cauchy":
+        return run_cauchy_arm(args, cfg)
 
     import paper_2601_22344_b200 as rp
     from paper_2601_22344_b200 import gen

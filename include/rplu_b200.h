@@ -165,6 +165,11 @@ int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const 
                           const void* y, const void* G, const void* Bt, double* out,
                           void* stream);
 
+/* Diagnostic: measured FP64 FMA-pipe throughput of the context's GPU
+ * (TFLOP/s, best of 5), the roofline denominator of the generated-entry
+ * (Cauchy-like, Gaussian-kernel) kernels. */
+int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms);
+
 /* sample_index(weights, u) on a device weight vector (rng.py:50-74):
  * first index whose running sum exceeds u*total, top clamp, walk-back over
  * zero weights.  RPLU_ERR_ARG for empty / negative / all-zero weights.

@@ -12,11 +12,15 @@ entry points raise.
 __version__ = "0.1.0"
 
 from .accessors import CallableOperator, CapabilityError, DenseMatrix, MatrixAccessor, materialize
+from .cauchy import (CauchyLikeMatrix, StructuredPivotTrace, exact_row_norms,
+                     generator_schur_update, structured_eliminate)
 from .dense_pivots import EliminationTrace, PivotRule, eliminate
 from .rng import RngState, sample_index
 
 __all__ = [
     "CallableOperator", "CapabilityError", "DenseMatrix", "MatrixAccessor", "materialize",
+    "CauchyLikeMatrix", "StructuredPivotTrace", "exact_row_norms", "generator_schur_update",
+    "structured_eliminate",
     "EliminationTrace", "PivotRule", "eliminate",
     "RngState", "sample_index",
 ]

@@ -61,6 +61,28 @@ class DenseOut(ctypes.Structure):
     ]
 
 
+class CauchyArgs(ctypes.Structure):
+    _fields_ = [
+        ("rule", c_i32), ("p", c_i32), ("n", c_i64), ("m", c_i64), ("rank", c_i64),
+        ("stop_tol", c_dbl),
+        ("x", c_vp), ("y", c_vp), ("G", c_vp), ("Bt", c_vp),
+        ("C", c_vp), ("Rrow", c_vp), ("a", c_vp),
+        ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
+        ("stream", c_vp), ("flags", c_i32), ("reserved", c_i32),
+    ]
+
+
+class CauchyOut(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.POINTER(c_i64)), ("cols", ctypes.POINTER(c_i64)),
+        ("bound_maxes", ctypes.POINTER(c_dbl)), ("bound_sums", ctypes.POINTER(c_dbl)),
+        ("steps_done", c_i64), ("bounds_recorded", c_i64), ("uniforms_consumed", c_i64),
+        ("near_boundary_draws", c_i64), ("tol_stop", c_i32), ("degenerate_stop", c_i32),
+        ("zero_pivot_i", c_i64), ("zero_pivot_j", c_i64),
+        ("masses_ms", c_dbl), ("masses_launches", c_i64), ("kernel_launches", c_i64),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/rplu_b200.h
 SIGNATURES = {
     "rplu_abi_version": (ctypes.c_int, []),
@@ -71,7 +93,20 @@ SIGNATURES = {
     "rplu_row_masses": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "rplu_sample_index": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_i64),
                                          ctypes.POINTER(c_i32), c_vp]),
+    "rplu_cauchy_run": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyArgs),
+                                       ctypes.POINTER(CauchyOut)]),
+    "rplu_cauchy_row_norms": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                             c_vp, c_vp]),
+    "rplu_diag_fp64_peak": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
 }
+
+
+def fp64_peak_tflops(device=0):
+    """Measured FP64 FMA throughput of `device` (TFLOP/s) via the library probe."""
+    c = context(device)
+    tf, ms = c_dbl(0.0), c_dbl(0.0)
+    check(c._lib.rplu_diag_fp64_peak(c.handle, ctypes.byref(tf), ctypes.byref(ms)))
+    return tf.value
 
 _lib = None
 _lib_lock = threading.Lock()

@@ -43,6 +43,7 @@ int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long l
 int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
                       int* near, cudaStream_t s);
 int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out);
+int fp64_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
 int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
                       const void* G, const void* Bt, double* out, cudaStream_t s);
 
@@ -237,6 +238,13 @@ int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const 
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
   return cauchy_norms_impl(ctx, p, n, m, x, y, G, Bt, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {
+  if (!ctx || !tflops) { set_error("rplu_diag_fp64_peak: NULL argument"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return fp64_peak_impl(ctx, tflops, best_ms);
 }
 
 int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
