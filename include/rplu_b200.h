@@ -109,6 +109,49 @@ typedef struct rplu_dense_out {
 
 int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* out);
 
+/* ------------------------------------------------------------------------ */
+/* Row-block sharded dense RPLU (one rank per GPU).  The host
+ * driver (paper_2601_22344_b200.distributed) interleaves these calls with two
+ * collectives per step on the same stream:
+ *   begin -> allgather(local_total) ->
+ *   for t: select(t) -> allreduce_sum(header[4], U[t,:]) -> update(t)
+ *          -> allgather(local_total)
+ *   select(steps) (final residual norm) -> finish.
+ * Non-owning ranks contribute -0.0, so the sums reproduce the owner's bits. */
+
+typedef struct rplu_shard_args {
+  int32_t dtype;          /* RPLU_F32 | RPLU_F64 | RPLU_C128 */
+  int32_t world, rank;    /* shard count and this shard's index */
+  int32_t reserved;
+  int64_t n_local, m;     /* local row block shape */
+  int64_t ld;             /* row stride of R (elements) */
+  int64_t row_offset;     /* global index of local row 0 */
+  int64_t steps;
+  double stop_tol;
+  void* R;                /* device: n_local x ld residual rows, updated in place */
+  void* Lt;               /* device: steps x n_local (local rows of L, transposed) */
+  void* U;                /* device: steps x ldu (replicated on every rank) */
+  int64_t ldu;
+  const double* uniforms; /* host uniform stream (uploaded by begin) */
+  int64_t n_uniforms;
+  void* stream;
+} rplu_shard_args;
+
+/* K1 masses of the local rows, state reset, uniforms upload; writes the local
+ * mass total to local_total (device double). */
+int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_total);
+/* Global owner selection from totals[world] (device), owner's row/column draw;
+ * writes header[4] (device doubles) and U[t,:] (owner bits or -0.0). */
+int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* totals,
+                      double* header);
+/* Post the reduced header, K3 fused update of the local rows, local total. */
+int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* header,
+                      double* local_total);
+/* 1 if the loop is still running (synchronizes the stream). */
+int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active);
+/* Copy pivots / residual norms / flags to the host (out as for rplu_dense_run). */
+int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* out);
+
 /* Squared row masses sum_j |R_ij|^2 of a device matrix (K1), written to the
  * device array `masses` (n doubles).  Used by the sharded driver for step 0
  * and by accessors' row_norms(). */
@@ -164,6 +207,40 @@ int rplu_cauchy_run(rplu_ctx* ctx, const rplu_cauchy_args* args, rplu_cauchy_out
 int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
                           const void* y, const void* G, const void* Bt, double* out,
                           void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Matrix-free CUR-form Alg 2 (cur_build) for the Gaussian-kernel operator
+ * A_ij = exp(-|p_i - q_j|^2 / (2 h^2)).  The Python driver
+ * (paper_2601_22344_b200.lowmem_cur.cur_build, mirroring lowmem_cur.py:212-300)
+ * sequences these device primitives; every vector is a device fp64 array. */
+
+typedef struct rplu_gauss_op {
+  int64_t n, m;
+  const double* P;  /* device n x 3 row-major: points p_i */
+  const double* Q;  /* device m x 3 row-major: points q_j */
+  double h;         /* bandwidth (> 0) */
+} rplu_gauss_op;
+
+/* K7 full generated GEMV: adjoint=0: out[n] = A v[m]; adjoint=1: out[m] = A^T v[n]
+ * (accessor apply / adjoint_apply, accessors.py:36-90).  *kernel_ms (optional)
+ * receives the CUDA-event time of the generated-entry kernel. */
+int rplu_gauss_apply(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t adjoint, const double* v,
+                     double* out, double* kernel_ms, void* stream);
+/* squared row norms sum_j A_ij^2 into out[n] (row_norms()) */
+int rplu_gauss_row_norms(rplu_ctx* ctx, const rplu_gauss_op* op, double* out, void* stream);
+/* axis=0: out[m] = A[index, :];  axis=1: out[n] = A[:, index] */
+int rplu_gauss_line(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis, int64_t index,
+                    double* out, void* stream);
+/* K8 k-restricted products: axis=0: out[m] = A[sel, :]^T w;  axis=1: out[n] = A[:, sel] w
+ * (sel: device int64[k], w: device fp64[k]); replaces lowmem_cur.py:174-187. */
+int rplu_gauss_restricted(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis,
+                          const int64_t* sel, const double* w, int64_t k, double* out,
+                          void* stream);
+/* K9 row-norm downdate (lowmem_cur.py:277-285): nrow -= 2 (g - v) chat;
+ * nrow += l2 chat^2; count entries < -floor; clip at 0; *total = sum(nrow). */
+int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, const double* v,
+                      const double* chat, double l2, double floor, int64_t* clamped,
+                      double* total, void* stream);
 
 /* Diagnostic: measured FP64 FMA-pipe throughput of the context's GPU
  * (TFLOP/s, best of 5), the roofline denominator of the generated-entry

@@ -15,6 +15,9 @@ from .accessors import CallableOperator, CapabilityError, DenseMatrix, MatrixAcc
 from .cauchy import (CauchyLikeMatrix, StructuredPivotTrace, exact_row_norms,
                      generator_schur_update, structured_eliminate)
 from .dense_pivots import EliminationTrace, PivotRule, eliminate
+from .lowmem_cur import (CurBuildInfo, CurFactorization, core_extend, cur_build, residual_column,
+                         residual_row)
+from .operators import GaussianKernelOperator
 from .rng import RngState, sample_index
 
 __all__ = [
@@ -22,5 +25,7 @@ __all__ = [
     "CauchyLikeMatrix", "StructuredPivotTrace", "exact_row_norms", "generator_schur_update",
     "structured_eliminate",
     "EliminationTrace", "PivotRule", "eliminate",
+    "CurBuildInfo", "CurFactorization", "core_extend", "cur_build", "residual_column",
+    "residual_row", "GaussianKernelOperator",
     "RngState", "sample_index",
 ]

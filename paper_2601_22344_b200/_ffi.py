@@ -98,6 +98,14 @@ SIGNATURES = {
     "rplu_cauchy_row_norms": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                              c_vp, c_vp]),
     "rplu_diag_fp64_peak": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
+    # Gaussian-kernel operator struct is passed by pointer (operators._GaussOpStruct)
+    "rplu_gauss_apply": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(c_dbl),
+                                        c_vp]),
+    "rplu_gauss_row_norms": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "rplu_gauss_line": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "rplu_gauss_restricted": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
+                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
 }
 
 

@@ -44,6 +44,34 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, lon
                       int* near, cudaStream_t s);
 int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out);
 int fp64_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
+int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
+                    cudaStream_t s, float* ms);
+int gauss_line_impl(const double* pts, long long count, const double* base, double c, double* out,
+                    cudaStream_t s);
+int gauss_restricted_impl(rplu_ctx* ctx, const double* targets, long long count,
+                          const double* selpts, const long long* sel, const double* w,
+                          long long k, double c, double* out, cudaStream_t s);
+int cur_downdate_impl(rplu_ctx* ctx, long long n, double* nrow, const double* g, const double* v,
+                      const double* chat, double l2, double floor, long long* clamped,
+                      double* total, cudaStream_t s);
+
+static int gauss_check(const rplu_gauss_op* op) {
+  if (!op || op->n < 1 || op->m < 1 || !op->P || !op->Q || !(op->h > 0.0)) {
+    set_error("invalid Gaussian-kernel operator");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+static GaussOp gauss_of(const rplu_gauss_op* op, bool adjoint) {
+  GaussOp g;
+  g.n = adjoint ? op->m : op->n;
+  g.m = adjoint ? op->n : op->m;
+  g.P = adjoint ? op->Q : op->P;
+  g.Q = adjoint ? op->P : op->Q;
+  g.c = 1.0 / (2.0 * op->h * op->h);
+  return g;
+}
 int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
                       const void* G, const void* Bt, double* out, cudaStream_t s);
 
@@ -238,6 +266,253 @@ int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const 
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
   return cauchy_norms_impl(ctx, p, n, m, x, y, G, Bt, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static int shard_check(rplu_ctx* ctx, const rplu_shard_args* a) {
+  if (!ctx || !a || a->world < 1 || a->rank < 0 || a->rank >= a->world || a->n_local < 0 ||
+      a->m < 1 || a->ld < a->m || a->ldu < a->m || a->steps < 0 || !a->U ||
+      (a->n_local > 0 && !a->R)) {
+    set_error("rplu_shard: bad arguments");
+    return RPLU_ERR_ARG;
+  }
+  if (a->dtype != RPLU_F32 && a->dtype != RPLU_F64 && a->dtype != RPLU_C128) {
+    set_error("rplu_shard: unknown dtype");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
+  ShardParams p{};
+  p.dtype = a->dtype;
+  p.R = a->R;
+  p.ld = a->ld;
+  p.n_local = a->n_local;
+  p.m = a->m;
+  p.row_offset = a->row_offset;
+  p.steps = a->steps;
+  p.U = a->U;
+  p.ldu = a->ldu;
+  p.masses = reinterpret_cast<double*>(ctx->masses.ptr);
+  p.st = reinterpret_cast<DevState*>(ctx->state.ptr);
+  p.world = a->world;
+  p.rank = a->rank;
+  p.uniforms = reinterpret_cast<const double*>(ctx->uniforms.ptr);
+  p.n_uniforms = a->n_uniforms;
+  p.resid = reinterpret_cast<double*>(ctx->resid.ptr);
+  p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
+  p.stop_tol = a->stop_tol;
+  return p;
+}
+
+__global__ void shard_init_state(DevState* st) {
+  st->ucount = 0;
+  st->near_boundary = 0;
+  st->pi = st->pj = -1;
+  st->err_i = st->err_j = -1;
+  st->active = 1;
+  st->status = 0;
+  st->fro0 = 0.0;
+  st->done = 0;
+}
+
+int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_total) {
+  int rc;
+  if ((rc = shard_check(ctx, a))) return rc;
+  if (!local_total || !a->uniforms || a->n_uniforms < 2) {
+    set_error("rplu_shard_begin: needs local_total and a uniform stream");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
+  if ((rc = ctx->masses.ensure(sizeof(double) * (size_t)(a->n_local > 0 ? a->n_local : 1)))) return rc;
+  if ((rc = ctx->pivots.ensure(sizeof(long long) * (size_t)(2 * a->steps + 2)))) return rc;
+  if ((rc = ctx->resid.ensure(sizeof(double) * (size_t)(a->steps + 1)))) return rc;
+  if ((rc = ctx->uniforms.ensure(sizeof(double) * (size_t)a->n_uniforms))) return rc;
+  RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * a->n_uniforms,
+                            cudaMemcpyHostToDevice, s));
+  shard_init_state<<<1, 1, 0, s>>>(reinterpret_cast<DevState*>(ctx->state.ptr));
+  double* masses = reinterpret_cast<double*>(ctx->masses.ptr);
+  if (a->n_local > 0) {
+    if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
+                                 masses, nullptr, 0, false, s)))
+      return rc;
+    return shard_total_impl(masses, a->n_local, local_total, s);
+  }
+  RPLU_CUDA(cudaMemsetAsync(local_total, 0, sizeof(double), s));
+  return RPLU_OK;
+}
+
+int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* totals,
+                      double* header) {
+  int rc;
+  if ((rc = shard_check(ctx, a))) return rc;
+  if (!totals || !header || t < 0 || t > a->steps) {
+    set_error("rplu_shard_select: bad arguments");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  ShardParams p = shard_params(ctx, a);
+  p.t = t;
+  p.totals = totals;
+  p.header = header;
+  return shard_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
+}
+
+int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* header,
+                      double* local_total) {
+  int rc;
+  if ((rc = shard_check(ctx, a))) return rc;
+  if (!header || !local_total || t < 0 || t >= a->steps) {
+    set_error("rplu_shard_update: bad arguments");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  ShardParams p = shard_params(ctx, a);
+  p.t = t;
+  p.header = const_cast<double*>(header);
+  if ((rc = shard_post_impl(p, s))) return rc;
+  if (a->n_local > 0) {
+    if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
+                                 p.masses, p.st, t, true, s)))
+      return rc;
+    return shard_total_impl(p.masses, a->n_local, local_total, s);
+  }
+  RPLU_CUDA(cudaMemsetAsync(local_total, 0, sizeof(double), s));
+  return RPLU_OK;
+}
+
+int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active) {
+  int rc;
+  if ((rc = shard_check(ctx, a))) return rc;
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, ctx->state.ptr, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  *active = hs.active;
+  return RPLU_OK;
+}
+
+int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* out) {
+  int rc;
+  if ((rc = shard_check(ctx, a))) return rc;
+  if (!out || !out->resid_fro || (a->steps > 0 && !out->pivots)) {
+    set_error("rplu_shard_finish: bad output");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, ctx->state.ptr, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  const long long done = hs.done;
+  if (done > 0)
+    RPLU_CUDA(cudaMemcpy(out->pivots, ctx->pivots.ptr, sizeof(long long) * 2 * done,
+                         cudaMemcpyDeviceToHost));
+  RPLU_CUDA(cudaMemcpy(out->resid_fro, ctx->resid.ptr, sizeof(double) * (done + 1),
+                       cudaMemcpyDeviceToHost));
+  out->steps_done = done;
+  out->uniforms_consumed = hs.ucount;
+  out->near_boundary_draws = hs.near_boundary;
+  out->clean_early_stop = hs.status == kCleanStop;
+  out->tol_stop = hs.status == kTolStop;
+  out->zero_pivot_i = hs.err_i;
+  out->zero_pivot_j = hs.err_j;
+  if (hs.status == kZeroPivot) {
+    set_error("pivot (" + std::to_string(hs.err_i) + ", " + std::to_string(hs.err_j) +
+              ") has exactly zero value (no resample on the sharded path)");
+    return RPLU_ERR_ZERO_PIVOT;
+  }
+  if (hs.status == kUniformsExhausted) {
+    set_error("uniform stream exhausted");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+int rplu_gauss_apply(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t adjoint, const double* v,
+                     double* out, double* kernel_ms, void* stream) {
+  int rc;
+  if (!ctx || !v || !out) { set_error("rplu_gauss_apply: NULL argument"); return RPLU_ERR_ARG; }
+  if ((rc = gauss_check(op))) return rc;
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  float ms = 0.f;
+  rc = gauss_gemv_impl(ctx, gauss_of(op, adjoint != 0), v, out, false,
+                       reinterpret_cast<cudaStream_t>(stream), kernel_ms ? &ms : nullptr);
+  if (kernel_ms) *kernel_ms = ms;
+  return rc;
+}
+
+int rplu_gauss_row_norms(rplu_ctx* ctx, const rplu_gauss_op* op, double* out, void* stream) {
+  int rc;
+  if (!ctx || !out) { set_error("rplu_gauss_row_norms: NULL argument"); return RPLU_ERR_ARG; }
+  if ((rc = gauss_check(op))) return rc;
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return gauss_gemv_impl(ctx, gauss_of(op, false), nullptr, out, true,
+                         reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+int rplu_gauss_line(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis, int64_t index,
+                    double* out, void* stream) {
+  int rc;
+  if (!ctx || !out) { set_error("rplu_gauss_line: NULL argument"); return RPLU_ERR_ARG; }
+  if ((rc = gauss_check(op))) return rc;
+  const int64_t lim = axis == 0 ? op->n : op->m;
+  if (index < 0 || index >= lim) { set_error("index out of range"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  const double c = 1.0 / (2.0 * op->h * op->h);
+  if (axis == 0) return gauss_line_impl(op->Q, op->m, op->P + 3 * index, c, out,
+                                        reinterpret_cast<cudaStream_t>(stream));
+  return gauss_line_impl(op->P, op->n, op->Q + 3 * index, c, out,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_gauss_restricted(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis,
+                          const int64_t* sel, const double* w, int64_t k, double* out,
+                          void* stream) {
+  int rc;
+  if (!ctx || !out || (k > 0 && (!sel || !w)) || k < 0) {
+    set_error("rplu_gauss_restricted: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  if ((rc = gauss_check(op))) return rc;
+  if (k > 12000) { set_error("restricted product supports k <= 12000"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  const double c = 1.0 / (2.0 * op->h * op->h);
+  const long long* s = reinterpret_cast<const long long*>(sel);
+  if (axis == 0)  // out[m] = A[sel,:]^T w : targets Q, selected P[sel]
+    return gauss_restricted_impl(ctx, op->Q, op->m, op->P, s, w, k, c, out,
+                                 reinterpret_cast<cudaStream_t>(stream));
+  return gauss_restricted_impl(ctx, op->P, op->n, op->Q, s, w, k, c, out,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, const double* v,
+                      const double* chat, double l2, double floor, int64_t* clamped,
+                      double* total, void* stream) {
+  if (!ctx || !nrow || !g || !v || !chat || !clamped || !total || n < 1) {
+    set_error("rplu_cur_downdate: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard gd(ctx->device);
+  if (gd.rc) return gd.rc;
+  long long c = 0;
+  int rc = cur_downdate_impl(ctx, n, nrow, g, v, chat, l2, floor, &c, total,
+                             reinterpret_cast<cudaStream_t>(stream));
+  *clamped = c;
+  return rc;
 }
 
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {

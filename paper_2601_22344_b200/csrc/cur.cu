@@ -1,0 +1,285 @@
+// Matrix-free CUR-form RPLU (Alg 2) device kernels for the Gaussian-kernel
+// operator A_ij = exp(-|p_i - q_j|^2 / (2 h^2)) (BASELINE configs[4]).
+//
+// Reference: rplu.lowmem_cur.cur_build (pkg/src/rplu/lowmem_cur.py:212-300).
+// The reference touches A only through full applies (4 of A + 2 of A^T per
+// step, :161-187, :266-275, :303-312).  Here:
+//   K7  gauss_apply      full generated GEMV g = A l (the one O(nm) pass per
+//                        step, :273), FP64-pipe bound: no matrix in HBM
+//   K8  gauss_rows/cols  k-restricted products A[I,:]^T w and A[:,J] w
+//                        (:174-187; the reference spends a full apply on a
+//                        k-sparse vector), single rows/columns A[i,:], A[:,j]
+//   K9  cur_downdate     n_row -= 2 Re((g-v) conj(chat)); += |l|^2 |chat|^2;
+//                        clamp count against eps*prev/n; total (:277-285)
+// All vectors are real fp64: the operator is real, so the reference's
+// complex128 vectors carry zero imaginary parts throughout.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "rplu_common.cuh"
+#include "rplu_internal.h"
+
+namespace rplu {
+
+// exp(x) for x <= 0 (the kernel's exponent).  Cody-Waite reduction
+// x = k ln2 + r, |r| <= ln2/2, degree-13 Taylor polynomial (truncation
+// < 4e-18 relative), scale by 2^k through the exponent field.  Accuracy
+// ~1 ulp; underflow below -708 returns 0 (entries < 1e-307).
+__device__ __forceinline__ double exp_nonpos(double x) {
+  if (x < -708.0) return 0.0;
+  const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest
+  const double kd = fma(x, 1.4426950408889634074, shifter) - shifter;
+  double r = fma(kd, -6.93147180369123816490e-01, x);
+  r = fma(kd, -1.90821492927058770002e-10, r);
+  double p = 1.6059043836821614599e-10;           // 1/13!
+  p = fma(p, r, 2.0876756987868098979e-09);       // 1/12!
+  p = fma(p, r, 2.5052108385441718775e-08);       // 1/11!
+  p = fma(p, r, 2.7557319223985890653e-07);       // 1/10!
+  p = fma(p, r, 2.7557319223985890653e-06);       // 1/9!
+  p = fma(p, r, 2.4801587301587301566e-05);       // 1/8!
+  p = fma(p, r, 1.9841269841269841253e-04);       // 1/7!
+  p = fma(p, r, 1.3888888888888889419e-03);       // 1/6!
+  p = fma(p, r, 8.3333333333333332177e-03);       // 1/5!
+  p = fma(p, r, 4.1666666666666664354e-02);       // 1/4!
+  p = fma(p, r, 1.6666666666666665741e-01);       // 1/3!
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const long long k = (long long)kd;
+  return p * __longlong_as_double((k + 1023) << 52);
+}
+
+__device__ __forceinline__ double gauss_entry(double px, double py, double pz, double qx,
+                                              double qy, double qz, double c) {
+  const double dx = px - qx, dy = py - qy, dz = pz - qz;
+  const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  return exp_nonpos(-c * d2);
+}
+
+// ---------------------------------------------------------------------------
+// K7: out[i] (+split partial) = sum_j A_ij v_j, or sum_j A_ij^2 (SQUARE, v
+// ignored) for row norms.  Row side in registers, column side (q_j, v_j) in
+// shared-memory tiles; columns split across gridDim.y for small n.
+template <int RPT, int TJ, bool SQUARE>
+__global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const double* __restrict__ v,
+                                                         double* __restrict__ partial, int splits) {
+  constexpr int NT = 256;
+  __shared__ double sq[TJ * 4];
+  const long long row_base = (long long)blockIdx.x * NT * RPT;
+  const long long cols_per = (op.m + splits - 1) / splits;
+  const long long j0 = (long long)blockIdx.y * cols_per;
+  const long long j1 = min(op.m, j0 + cols_per);
+  double px[RPT], py[RPT], pz[RPT], acc[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    long long ii = i < op.n ? i : 0;
+    px[r] = op.P[ii * 3 + 0];
+    py[r] = op.P[ii * 3 + 1];
+    pz[r] = op.P[ii * 3 + 2];
+    acc[r] = 0.0;
+  }
+  for (long long jt = j0; jt < j1; jt += TJ) {
+    const int cnt = (int)min((long long)TJ, j1 - jt);
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < cnt; cc += NT) {
+      const long long j = jt + cc;
+      sq[cc * 4 + 0] = op.Q[j * 3 + 0];
+      sq[cc * 4 + 1] = op.Q[j * 3 + 1];
+      sq[cc * 4 + 2] = op.Q[j * 3 + 2];
+      sq[cc * 4 + 3] = SQUARE ? 1.0 : v[j];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int cc = 0; cc < cnt; ++cc) {
+      const double qx = sq[cc * 4 + 0], qy = sq[cc * 4 + 1], qz = sq[cc * 4 + 2];
+      const double vj = sq[cc * 4 + 3];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const double e = gauss_entry(px[r], py[r], pz[r], qx, qy, qz, op.c);
+        acc[r] = SQUARE ? fma(e, e, acc[r]) : fma(e, vj, acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    if (i < op.n) partial[(long long)blockIdx.y * op.n + i] = acc[r];
+  }
+}
+
+__global__ void reduce_splits_kernel(const double* partial, int splits, long long n, double* out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += partial[(long long)k * n + i];
+  out[i] = s;
+}
+
+// K8: single row A[i,:] (m) or column A[:,j] (n) — out[k] = entry(base, pts[k])
+__global__ void gauss_line_kernel(const double* __restrict__ pts, long long count,
+                                  const double* __restrict__ base, double c, double* out) {
+  const double bx = base[0], by = base[1], bz = base[2];
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+       k += (long long)gridDim.x * blockDim.x)
+    out[k] = gauss_entry(bx, by, bz, pts[k * 3], pts[k * 3 + 1], pts[k * 3 + 2], c);
+}
+
+// K8: out[t] = sum_s w_s A(sel_s, t) over `count` targets t, where the k
+// selected points (rows I or columns J) and their weights are staged in smem.
+// A[I,:]^T w: targets = Q (m), selected = P[I];  A[:,J] w: targets = P (n),
+// selected = Q[J].  The kernel is symmetric in its point arguments.
+__global__ void __launch_bounds__(256) gauss_restricted_kernel(
+    const double* __restrict__ targets, long long count, const double* __restrict__ selpts,
+    const long long* __restrict__ sel, const double* __restrict__ w, long long k, double c,
+    double* out) {
+  extern __shared__ double ss[];  // k * 4
+  for (long long s = threadIdx.x; s < k; s += blockDim.x) {
+    const long long ix = sel[s];
+    ss[s * 4 + 0] = selpts[ix * 3 + 0];
+    ss[s * 4 + 1] = selpts[ix * 3 + 1];
+    ss[s * 4 + 2] = selpts[ix * 3 + 2];
+    ss[s * 4 + 3] = w[s];
+  }
+  __syncthreads();
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (long long)gridDim.x * blockDim.x) {
+    const double tx = targets[t * 3], ty = targets[t * 3 + 1], tz = targets[t * 3 + 2];
+    double acc = 0.0;
+    for (long long s = 0; s < k; ++s)
+      acc = fma(gauss_entry(ss[s * 4], ss[s * 4 + 1], ss[s * 4 + 2], tx, ty, tz, c), ss[s * 4 + 3],
+                acc);
+    out[t] = acc;
+  }
+}
+
+// K9: row-norm downdate with clamp (lowmem_cur.py:277-285), per-CTA partial
+// (sum, clamp count) written for a deterministic second-stage reduction.
+__global__ void __launch_bounds__(256) cur_downdate_kernel(long long n, double* nrow,
+                                                           const double* g, const double* v,
+                                                           const double* chat, double l2,
+                                                           double floor, double* psum,
+                                                           long long* pcnt) {
+  double s = 0.0;
+  long long cnt = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double ch = chat[i];
+    double x = nrow[i];
+    // one rounding per numpy ufunc, as in the reference (no contraction)
+    x = __dsub_rn(x, __dmul_rn(2.0, __dmul_rn(__dsub_rn(g[i], v[i]), ch)));
+    x = __dadd_rn(x, __dmul_rn(l2, __dmul_rn(ch, ch)));
+    if (x < -floor) ++cnt;
+    x = x > 0.0 ? x : 0.0;
+    nrow[i] = x;
+    s += x;
+  }
+  s = warp_sum(s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  __shared__ double ws[8];
+  __shared__ long long wc[8];
+  if ((threadIdx.x & 31) == 0) { ws[threadIdx.x >> 5] = s; wc[threadIdx.x >> 5] = cnt; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    long long c = 0;
+    for (int w = 0; w < 8; ++w) { t += ws[w]; c += wc[w]; }
+    psum[blockIdx.x] = t;
+    pcnt[blockIdx.x] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+static int gemv_splits(long long n, long long m, int rows_per_cta, int sms) {
+  long long rb = (n + rows_per_cta - 1) / rows_per_cta;
+  long long s = (4LL * sms + rb - 1) / rb;
+  long long max_s = (m + 511) / 512;
+  s = std::max(1LL, std::min(s, max_s));
+  return (int)std::min(s, 1024LL);
+}
+
+int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
+                    cudaStream_t s, float* ms) {
+  constexpr int RPT = 2, TJ = 256;
+  const int splits = gemv_splits(op.n, op.m, 256 * RPT, ctx->sm_count);
+  int rc;
+  if ((rc = ctx->scratch[4].ensure(sizeof(double) * (size_t)splits * op.n))) return rc;
+  double* part = reinterpret_cast<double*>(ctx->scratch[4].ptr);
+  dim3 grid((unsigned)((op.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)splits);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ms) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  if (square) gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits);
+  else gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits);
+  if (ms) cudaEventRecord(e1, s);
+  reduce_splits_kernel<<<(unsigned)((op.n + 255) / 256), 256, 0, s>>>(part, splits, op.n, out);
+  RPLU_CUDA(cudaGetLastError());
+  if (ms) {
+    RPLU_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return RPLU_OK;
+}
+
+int gauss_line_impl(const double* pts, long long count, const double* base, double c, double* out,
+                    cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((count + 255) / 256, 4096);
+  gauss_line_kernel<<<blocks, 256, 0, s>>>(pts, count, base, c, out);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int gauss_restricted_impl(rplu_ctx* ctx, const double* targets, long long count,
+                          const double* selpts, const long long* sel, const double* w,
+                          long long k, double c, double* out, cudaStream_t s) {
+  if (k == 0) {
+    RPLU_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * count, s));
+    return RPLU_OK;
+  }
+  const size_t smem = sizeof(double) * 4 * (size_t)k;
+  if (smem > 48 * 1024) {
+    RPLU_CUDA(cudaFuncSetAttribute(gauss_restricted_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  const int blocks = (int)std::min<long long>((count + 255) / 256, 16LL * ctx->sm_count);
+  gauss_restricted_kernel<<<blocks, 256, smem, s>>>(targets, count, selpts, sel, w, k, c, out);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int cur_downdate_impl(rplu_ctx* ctx, long long n, double* nrow, const double* g, const double* v,
+                      const double* chat, double l2, double floor, long long* clamped,
+                      double* total, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4LL * ctx->sm_count);
+  int rc;
+  if ((rc = ctx->scratch[5].ensure((sizeof(double) + sizeof(long long)) * (size_t)blocks)))
+    return rc;
+  double* ps = reinterpret_cast<double*>(ctx->scratch[5].ptr);
+  long long* pc = reinterpret_cast<long long*>(ps + blocks);
+  cur_downdate_kernel<<<blocks, 256, 0, s>>>(n, nrow, g, v, chat, l2, floor, ps, pc);
+  RPLU_CUDA(cudaGetLastError());
+  std::vector<double> hs(blocks);
+  std::vector<long long> hc(blocks);
+  RPLU_CUDA(cudaMemcpyAsync(hs.data(), ps, sizeof(double) * blocks, cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaMemcpyAsync(hc.data(), pc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  double t = 0.0;
+  long long c = 0;
+  for (int b = 0; b < blocks; ++b) { t += hs[b]; c += hc[b]; }
+  *total = t;
+  *clamped = c;
+  return RPLU_OK;
+}
+
+}  // namespace rplu

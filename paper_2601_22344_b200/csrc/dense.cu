@@ -554,3 +554,31 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, lon
 }
 
 }  // namespace rplu
+
+namespace rplu {
+
+int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
+                       void* U, long long ldu, double* masses, DevState* st, long long t,
+                       bool update, cudaStream_t s) {
+  DenseParams p{};
+  p.R = R;
+  p.ld = ld;
+  p.n = n;
+  p.m = m;
+  p.Lt = Lt;
+  p.U = U;
+  p.ldu = ldu;
+  p.masses = masses;
+  p.st = st;
+  p.t = t;
+  switch (dtype) {
+    case RPLU_F64: sweep<double>(p, update, false, s); break;
+    case RPLU_F32: sweep<float>(p, update, false, s); break;
+    case RPLU_C128: sweep<double2>(p, update, false, s); break;
+    default: set_error("unknown dtype"); return RPLU_ERR_ARG;
+  }
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+}  // namespace rplu

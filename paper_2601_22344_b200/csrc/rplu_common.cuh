@@ -221,9 +221,19 @@ __device__ __forceinline__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSm
 // CDF values bracketing the draw are left in s.lo_c / s.hi_c for the caller's
 // near-boundary accounting.
 template <int BLOCK, typename WF>
-__device__ long long cdf_find(const WF& wf, long long n, const Cdf<BLOCK>& c, double u,
-                              CdfSmem<BLOCK>& s) {
-  const double target = u * c.total;
+__device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>& c,
+                                     double target, CdfSmem<BLOCK>& s);
+
+template <int BLOCK, typename WF>
+__device__ __forceinline__ long long cdf_find(const WF& wf, long long n, const Cdf<BLOCK>& c,
+                                              double u, CdfSmem<BLOCK>& s) {
+  return cdf_find_target<BLOCK>(wf, n, c, u * c.total, s);
+}
+
+// Same search against an absolute target in [0, total] (sharded draws).
+template <int BLOCK, typename WF>
+__device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>& c,
+                                     double target, CdfSmem<BLOCK>& s) {
   if (threadIdx.x == 0) { s.idx = n; s.flag = 0; }
   __syncthreads();
   // lowest thread whose chunk upper boundary exceeds the target

@@ -38,6 +38,44 @@ enum Status {
   kZeroPivot = -2,
 };
 
+// Gaussian-kernel operator as the kernels see it (rows P, columns Q,
+// c = 1/(2h^2)); the adjoint swaps P and Q.
+struct GaussOp {
+  long long n, m;
+  const double* P;  // n x 3
+  const double* Q;  // m x 3
+  double c;
+};
+
+// Sharded dense step (shard.cu).
+struct ShardParams {
+  int dtype;
+  void* R;
+  long long ld, n_local, m, row_offset, steps;
+  void* U;
+  long long ldu;
+  double* masses;
+  DevState* st;
+  long long t;
+  const double* totals;  // [world] allgathered shard totals
+  int world, rank;
+  const double* uniforms;
+  long long n_uniforms;
+  double* header;  // 4 doubles: i_global, j, a_re, a_im
+  double* resid;
+  long long* pivots;
+  double stop_tol;
+};
+int shard_select_impl(const ShardParams& p, cudaStream_t s);
+int shard_post_impl(const ShardParams& p, cudaStream_t s);
+int shard_total_impl(const double* masses, long long n, double* out, cudaStream_t s);
+
+// K1 (update=false) / K3 (update=true) on a row block, from dense.cu; the
+// pivot (pj, coefficients) is read from *st and the pivot row from U[t,:].
+int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
+                       void* U, long long ldu, double* masses, DevState* st, long long t,
+                       bool update, cudaStream_t s);
+
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 
