@@ -43,6 +43,9 @@ CONFIGS = {
     "c4": dict(desc="C4 Cauchy-like c128 2^20 x 2^20 p=4 (BASELINE configs[3]); bench step = "
                     "`rank` pivot steps of the rank-256 run",
                n=1 << 20, rank=4, dtype="c128", seed=0, kind="cauchy", p=4),
+    "c5": dict(desc="C5 matrix-free Gaussian kernel fp64 2e6 x 2e6 (BASELINE configs[4]); bench "
+                    "step = `rank` pivot steps of the rank-1024 cur_build",
+               n=2_000_000, rank=2, dtype="f64", seed=0, kind="cur"),
 }
 METRIC = "RPLU pivot steps/sec at rank k; dense Schur step HBM GB/s vs B200 peak"
 UNIT = "pivot steps/s"
@@ -283,10 +286,93 @@ def run_cauchy_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_cur_arm(args, cfg):
+    """Matrix-free CUR path (cur_build on the Gaussian-kernel operator)."""
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _ffi, gen
+    torch.cuda.set_device(0)
+    n, rank, seed = cfg["n"], cfg["rank"], cfg["seed"]
+    P, Q = gen.c5_points(seed, n=n)
+    op = rp.GaussianKernelOperator(P, Q, h=0.1)
+    for _ in range(args.warmup):
+        rp.cur_build(op, "rplu-cur", rank, rng=rp.RngState(seed))
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gemv = []
+    ev0.record()
+    for _ in range(args.steps):
+        fact, info = rp.cur_build(op, "rplu-cur", rank, rng=rp.RngState(seed), time_gemv=True)
+        gemv += info.gemv_ms
+    ev1.record()
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    k = fact.rank
+    value = args.steps * k / (total_ms / 1e3)
+    evals = float(n) * n
+    avg_s = sum(gemv) / len(gemv) / 1e3
+    flops_per_eval = 13.0   # 3 sub, 3 mul/fma (d^2), 1 scale, 1 exp, 2 (accumulate)... see DESIGN.md
+    achieved = evals * flops_per_eval / avg_s / 1e12
+    peak = _ffi.fp64_peak_tflops(0)
+    # e2e: host points in, host factorization out
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    oph = rp.GaussianKernelOperator(P, Q, h=0.1)
+    facth, infoh = rp.cur_build(oph, "rplu-cur", rank, rng=rp.RngState(seed))
+    Wh = facth.core_matrix()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    model, cores = _cpu_info()
+    # CPU baseline: one full apply on a row sample, extrapolated to the
+    # reference's 6 applies per step (labelled)
+    rows = 200
+    host = oracle.GaussianKernelHost(P[:rows], Q)
+    t0 = time.perf_counter()
+    host.apply(np.ones(n))
+    dt = time.perf_counter() - t0
+    per_apply = dt * n / rows
+    cb_v = 1.0 / (6 * per_apply)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE construction)",
+        "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": rank, "seed": seed,
+                   "step": f"one cur_build run of {rank} pivot steps",
+                   "l2": "generated entries; points only in HBM (48 MB per side)"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "gauss_gemv_kernel (K7 full generated GEMV g = A l)",
+                     "algorithmic_flops_per_launch": evals * flops_per_eval,
+                     "avg_launch_ms": avg_s * 1e3, "evals_per_s": evals / avg_s,
+                     "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)",
+                     "note": "13 flop/eval counts exp as one op; the exp costs ~17 DFMA"},
+        "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"one Gaussian-kernel apply on {rows} of {n} rows "
+                                   f"({dt:.2f}s), extrapolated to the reference's 6 full "
+                                   f"applies per step; CPU: {model}"},
+        "e2e": {"value": k / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 48 * n,
+                "d2h_bytes_per_step": Wh.nbytes + 8 * n},
+        "gpu_launches": None,
+        "near_boundary_draws": info.near_boundary_draws,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200_arm(args, cfg, dist, rank_id, world):
     import torch
     if cfg.get("kind") == "cauchy":
         return run_cauchy_arm(args, cfg)
+    if cfg.get("kind") == "cur":
+        return run_cur_arm(args, cfg)
 
     import paper_2601_22344_b200 as rp
     from paper_2601_22344_b200 import gen

@@ -83,6 +83,17 @@ class CauchyOut(ctypes.Structure):
     ]
 
 
+class ShardArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", c_i32), ("world", c_i32), ("rank", c_i32), ("reserved", c_i32),
+        ("n_local", c_i64), ("m", c_i64), ("ld", c_i64), ("row_offset", c_i64),
+        ("steps", c_i64), ("stop_tol", c_dbl),
+        ("R", c_vp), ("Lt", c_vp), ("U", c_vp), ("ldu", c_i64),
+        ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
+        ("stream", c_vp),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/rplu_b200.h
 SIGNATURES = {
     "rplu_abi_version": (ctypes.c_int, []),
@@ -106,6 +117,12 @@ SIGNATURES = {
     "rplu_gauss_restricted": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
+    "rplu_shard_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_vp]),
+    "rplu_shard_select": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),
+    "rplu_shard_update": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),
+    "rplu_shard_active": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), ctypes.POINTER(c_i32)]),
+    "rplu_shard_finish": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs),
+                                         ctypes.POINTER(DenseOut)]),
 }
 
 

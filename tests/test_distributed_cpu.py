@@ -1,0 +1,113 @@
+"""World-size-2 gloo tests of the sharded driver on CPU.
+
+The choreography (allgather of shard totals, root-free allreduce of the pivot
+header and row with -0.0 contributions, global stop decisions) is the code
+the GPU ranks run (paper_2601_22344_b200.distributed.run_sharded); here it
+drives a numpy backend.  The sharded run must reproduce the single-process
+oracle's pivots and factors.
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, A, seed, steps, stop_tol, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_cpu_backend import NumpyShardBackend
+
+        from paper_2601_22344_b200.distributed import run_sharded, shard_rows
+        lo, hi = shard_rows(A.shape[0], world, rank)
+        be = NumpyShardBackend(A[lo:hi], lo, world, rank, seed, steps, stop_tol)
+        res = run_sharded(be, steps, poll_every=4)
+        out_q.put((rank, lo, hi, res["pivots"], res["resid_fro"], res["L_local"], res["U"],
+                   res["status"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(A, seed, steps, world=2, stop_tol=0.0):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, A, seed, steps, stop_tol, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(outs)
+
+
+def test_shard_rows_partition():
+    from paper_2601_22344_b200.distributed import shard_rows
+    for n in (1, 7, 32768, 1000003):
+        for w in (1, 2, 3, 8):
+            blocks = [shard_rows(n, w, r) for r in range(w)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(blocks[r][1] == blocks[r + 1][0] for r in range(w - 1))
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_matches_single_process(world):
+    import oracle
+    from paper_2601_22344_b200 import gen
+    A = gen.c1_dense(4, n=90, m=70)
+    steps = 40
+    outs = _run(A, seed=4, steps=steps, world=world)
+    ref = oracle.eliminate_real(A, "rplu", steps, seed=4, margins=True)
+    pivots = outs[0][3]
+    for o in outs:
+        assert o[3] == pivots, "ranks disagree on the pivot sequence"
+    mism = [t for t, (a, b) in enumerate(zip(pivots, ref["pivots"])) if a != b]
+    if mism:
+        assert ref["margins"][mism[0]] <= oracle.NEAR_REL
+        return
+    assert pivots == ref["pivots"]
+    L = np.concatenate([o[5] for o in outs], axis=0)
+    np.testing.assert_array_equal(L, ref["L"])
+    for o in outs:
+        np.testing.assert_array_equal(o[6], ref["U"])
+    np.testing.assert_allclose(outs[0][4], ref["resid_fro"], rtol=1e-12)
+
+
+def test_sharded_tol_stop_is_global():
+    import oracle
+    from paper_2601_22344_b200 import gen
+    A = gen.c1_dense(3, n=64)
+    outs = _run(A, seed=3, steps=60, stop_tol=0.3)
+    ref = oracle.eliminate_real(A, "rplu", 60, seed=3, stop_tol=0.3)
+    assert ref["tol_stop"]
+    for o in outs:
+        assert o[7] == "tol"
+        assert len(o[3]) == ref["steps"]
+
+
+def test_negative_zero_allreduce_is_exact():
+    """x + (-0.0) == x bit for bit, including x = -0.0 and tiny subnormals."""
+    x = np.array([-0.0, 0.0, 5e-324, -5e-324, 1.0, -3.5, np.finfo(float).max])
+    y = x + (-0.0)
+    assert np.array_equal(x.view(np.int64), y.view(np.int64))
