@@ -60,6 +60,20 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _traffic(cfg, n):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), when it matches."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        key = "c3" + cfg["dtype"]
+        if key in t and t[key]["n"] == n:
+            return t[key]["traffic_bytes"]
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -464,7 +478,7 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                    "step": f"one full elimination of {rank} pivot steps",
                    "l2": f"inputs larger than L2 ({n * n * esize / 1e9:.1f} GB residual)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": _traffic(cfg, n),
                      "kernel": "dense_sweep_kernel (K3 fused Schur update + row masses)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src},

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
   Cdf<B> cr = cdf_build<B>(wrow, n, sm);
   // umax over rows
   double mx = 0.0;
-  for (long long k = cr.lo; k < cr.hi; ++k) mx = fmax(mx, wrow(k));
+  for (long long k = threadIdx.x; k < n; k += B) mx = fmax(mx, wrow(k));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;

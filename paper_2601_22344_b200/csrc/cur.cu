@@ -24,39 +24,52 @@
 
 namespace rplu {
 
-// exp(x) for x <= 0 (the kernel's exponent).  Cody-Waite reduction
-// x = k ln2 + r, |r| <= ln2/2, degree-13 Taylor polynomial (truncation
-// < 4e-18 relative), scale by 2^k through the exponent field.  Accuracy
-// ~1 ulp; underflow below -708 returns 0 (entries < 1e-307).
-__device__ __forceinline__ double exp_nonpos(double x) {
-  if (x < -708.0) return 0.0;
+// exp(x) for x <= 0 (the kernel's exponent), table-driven: x = (32n + j)
+// ln2/32 + r with |r| <= ln2/64, exp(x) = 2^n * 2^(j/32) * p(r), p the
+// degree-6 Taylor polynomial (truncation < 4e-18 relative).  2^(j/32) comes
+// from a 32-entry table held one entry per lane (fetched with a warp
+// shuffle: no shared-memory bank conflicts), 2^n is added to the table
+// value's exponent field with integer ops, and k = 32n + j is read from the
+// low word of the round-to-nearest shifter sum — so an entry costs 19 FP64
+// pipe operations including the distance and the accumulate.  Accuracy
+// ~1 ulp.  Below -708 the result is 0 (entries < 1e-307).
+// Every lane of the warp must call it (warp-synchronous shuffle).
+__constant__ double kExp2Tab[32] = {
+    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
+    1.0905077326652577, 1.1143867425958924, 1.1387886347566916, 1.1637248587775775,
+    1.189207115002721, 1.215247359980469, 1.241857812073484, 1.2690509571917332,
+    1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
+    1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,
+    1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965,
+    1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,
+    1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002};
+
+__device__ __forceinline__ double exp2tab_lane() { return kExp2Tab[threadIdx.x & 31]; }
+
+__device__ __forceinline__ double exp_nonpos(double x, double tlane) {
   const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest
-  const double kd = fma(x, 1.4426950408889634074, shifter) - shifter;
-  double r = fma(kd, -6.93147180369123816490e-01, x);
-  r = fma(kd, -1.90821492927058770002e-10, r);
-  double p = 1.6059043836821614599e-10;           // 1/13!
-  p = fma(p, r, 2.0876756987868098979e-09);       // 1/12!
-  p = fma(p, r, 2.5052108385441718775e-08);       // 1/11!
-  p = fma(p, r, 2.7557319223985890653e-07);       // 1/10!
-  p = fma(p, r, 2.7557319223985890653e-06);       // 1/9!
-  p = fma(p, r, 2.4801587301587301566e-05);       // 1/8!
-  p = fma(p, r, 1.9841269841269841253e-04);       // 1/7!
-  p = fma(p, r, 1.3888888888888889419e-03);       // 1/6!
-  p = fma(p, r, 8.3333333333333332177e-03);       // 1/5!
-  p = fma(p, r, 4.1666666666666664354e-02);       // 1/4!
-  p = fma(p, r, 1.6666666666666665741e-01);       // 1/3!
+  const double sft = fma(x, 46.16624130844683, shifter);   // x * 32/ln2
+  const double kd = sft - shifter;
+  const int k = __double2loint(sft);
+  double r = fma(kd, -0.02166084938653512, x);             // ln2/32 (hi)
+  r = fma(kd, -5.9631716539705866e-12, r);                 // ln2/32 (lo)
+  double p = 1.3888888888888889e-03;                       // 1/720
+  p = fma(p, r, 8.3333333333333333e-03);                   // 1/120
+  p = fma(p, r, 4.1666666666666667e-02);                   // 1/24
+  p = fma(p, r, 1.6666666666666667e-01);                   // 1/6
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const long long k = (long long)kd;
-  return p * __longlong_as_double((k + 1023) << 52);
+  const double t = __shfl_sync(0xffffffffu, tlane, k & 31);
+  const double ts = __hiloint2double(__double2hiint(t) + ((k >> 5) << 20), __double2loint(t));
+  return x < -708.0 ? 0.0 : p * ts;
 }
 
 __device__ __forceinline__ double gauss_entry(double px, double py, double pz, double qx,
-                                              double qy, double qz, double c) {
+                                              double qy, double qz, double c, double tlane) {
   const double dx = px - qx, dy = py - qy, dz = pz - qz;
   const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  return exp_nonpos(-c * d2);
+  return exp_nonpos(-c * d2, tlane);
 }
 
 // ---------------------------------------------------------------------------
@@ -72,6 +85,7 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
   const long long cols_per = (op.m + splits - 1) / splits;
   const long long j0 = (long long)blockIdx.y * cols_per;
   const long long j1 = min(op.m, j0 + cols_per);
+  const double tl = exp2tab_lane();
   double px[RPT], py[RPT], pz[RPT], acc[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -99,7 +113,7 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
       const double vj = sq[cc * 4 + 3];
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const double e = gauss_entry(px[r], py[r], pz[r], qx, qy, qz, op.c);
+        const double e = gauss_entry(px[r], py[r], pz[r], qx, qy, qz, op.c, tl);
         acc[r] = SQUARE ? fma(e, e, acc[r]) : fma(e, vj, acc[r]);
       }
     }
@@ -123,9 +137,15 @@ __global__ void reduce_splits_kernel(const double* partial, int splits, long lon
 __global__ void gauss_line_kernel(const double* __restrict__ pts, long long count,
                                   const double* __restrict__ base, double c, double* out) {
   const double bx = base[0], by = base[1], bz = base[2];
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < count;
-       k += (long long)gridDim.x * blockDim.x)
-    out[k] = gauss_entry(bx, by, bz, pts[k * 3], pts[k * 3 + 1], pts[k * 3 + 2], c);
+  const double tl = exp2tab_lane();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the exp's table shuffle needs every lane)
+  for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < count; k0 += stride) {
+    const long long k = k0 + threadIdx.x;
+    const long long kk = k < count ? k : count - 1;
+    const double e = gauss_entry(bx, by, bz, pts[kk * 3], pts[kk * 3 + 1], pts[kk * 3 + 2], c, tl);
+    if (k < count) out[k] = e;
+  }
 }
 
 // K8: out[t] = sum_s w_s A(sel_s, t) over `count` targets t, where the k
@@ -145,14 +165,17 @@ __global__ void __launch_bounds__(256) gauss_restricted_kernel(
     ss[s * 4 + 3] = w[s];
   }
   __syncthreads();
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
-       t += (long long)gridDim.x * blockDim.x) {
-    const double tx = targets[t * 3], ty = targets[t * 3 + 1], tz = targets[t * 3 + 2];
+  const double tl = exp2tab_lane();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < count; t0 += stride) {
+    const long long t = t0 + threadIdx.x;
+    const long long tt = t < count ? t : count - 1;
+    const double tx = targets[tt * 3], ty = targets[tt * 3 + 1], tz = targets[tt * 3 + 2];
     double acc = 0.0;
     for (long long s = 0; s < k; ++s)
-      acc = fma(gauss_entry(ss[s * 4], ss[s * 4 + 1], ss[s * 4 + 2], tx, ty, tz, c), ss[s * 4 + 3],
-                acc);
-    out[t] = acc;
+      acc = fma(gauss_entry(ss[s * 4], ss[s * 4 + 1], ss[s * 4 + 2], tx, ty, tz, c, tl),
+                ss[s * 4 + 3], acc);
+    if (t < count) out[t] = acc;
   }
 }
 

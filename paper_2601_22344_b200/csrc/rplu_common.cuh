@@ -157,63 +157,79 @@ __device__ __forceinline__ void warp_argmax(double& v, long long& i) {
 // Shared scratch for the single-CTA select kernels.
 template <int BLOCK>
 struct CdfSmem {
-  double incl[BLOCK];  // inclusive chunk-boundary sums, incl[t] == excl[t+1]
-  double wsum[BLOCK / 32];
+  double wexcl[BLOCK / 32];  // CDF value before warp segment w
+  double wincl[BLOCK / 32];  // CDF value at the end of warp segment w
   long long idx;
-  double val;
   double lo_c, hi_c;
-  int flag;
+  int owner;
 };
 
-// Block-wide inclusive scan of one double per thread.  Result: s.incl[tid].
+// CDF layout (one CTA of BLOCK threads).  The n weights are split into
+// BLOCK/32 contiguous warp segments of S elements (S a multiple of 32), each
+// walked in slabs of 32 consecutive elements (one coalesced load per lane).
+// Inside a slab the running sum is a warp inclusive scan p_l; slabs
+// accumulate sequentially into r_s; segments accumulate sequentially into
+// excl_w.  The CDF value of element k (warp w, slab s, lane l) is
+//     c_k = excl_w + (r_s + p_l),
+// and the last element of segment w has c = excl_w + r_end = incl_w exactly,
+// so the segment boundaries the owner search uses are the same numbers the
+// in-segment walk reproduces.  (The reference's np.cumsum is one sequential
+// sum; the association differs, so GPU and reference draws agree except
+// within rounding of a boundary — counted as near-boundary draws.)
 template <int BLOCK>
-__device__ __forceinline__ double block_incl_scan(double v, CdfSmem<BLOCK>& s) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double x = v;
+struct Cdf {
+  long long seg;  // segment length S
+  double total;
+};
+
+constexpr int kCdfUnroll = 4;  // slabs in flight per warp
+
+__device__ __forceinline__ double warp_incl_scan(double x) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    double y = __shfl_up_sync(0xffffffffu, x, o);
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) s.wsum[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    double t = (lane < BLOCK / 32) ? s.wsum[lane] : 0.0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      double y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < BLOCK / 32) s.wsum[lane] = t;  // inclusive warp totals
-  }
-  __syncthreads();
-  if (w > 0) x += s.wsum[w - 1];
-  s.incl[threadIdx.x] = x;
-  __syncthreads();
   return x;
 }
 
-// Chunked CDF over n weights given by wf(k) (k in [0,n)), one CTA of BLOCK
-// threads.  Thread t owns rows [t*C, min((t+1)*C, n)) and sums them in index
-// order (the reference's np.cumsum is sequential; within a chunk we keep that
-// order).  Chunk boundaries come from the block scan.
-template <int BLOCK>
-struct Cdf {
-  long long lo, hi;
-  double excl, incl, total;
-};
-
 template <int BLOCK, typename WF>
-__device__ __forceinline__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
+__device__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
+  constexpr int W = BLOCK / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Cdf<BLOCK> c;
-  long long C = (n + BLOCK - 1) / BLOCK;
-  c.lo = min((long long)threadIdx.x * C, n);
-  c.hi = min(c.lo + C, n);
-  double acc = 0.0;
-  for (long long k = c.lo; k < c.hi; ++k) acc += wf(k);
-  c.incl = block_incl_scan<BLOCK>(acc, s);
-  c.excl = threadIdx.x ? s.incl[threadIdx.x - 1] : 0.0;
-  c.total = s.incl[BLOCK - 1];
+  c.seg = (((n + W - 1) / W) + 31) / 32 * 32;
+  if (c.seg < 32) c.seg = 32;
+  const long long lo = min((long long)w * c.seg, n), hi = min(lo + c.seg, n);
+  double run = 0.0;
+  for (long long base = lo; base < hi; base += 32 * kCdfUnroll) {
+    double xs[kCdfUnroll];
+#pragma unroll
+    for (int u = 0; u < kCdfUnroll; ++u) {
+      const long long k = base + 32 * u + lane;
+      xs[u] = (k < hi) ? wf(k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kCdfUnroll; ++u) {
+      if (base + 32 * u >= hi) break;
+      const double p = warp_incl_scan(xs[u]);
+      run += __shfl_sync(0xffffffffu, p, 31);
+    }
+  }
+  if (lane == 0) s.wincl[w] = run;  // segment total (temporarily)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0;
+    for (int q = 0; q < W; ++q) {
+      const double st = s.wincl[q];
+      s.wexcl[q] = e;
+      e = e + st;
+      s.wincl[q] = e;
+    }
+  }
+  __syncthreads();
+  c.total = s.wincl[W - 1];
   return c;
 }
 
@@ -234,44 +250,61 @@ __device__ __forceinline__ long long cdf_find(const WF& wf, long long n, const C
 template <int BLOCK, typename WF>
 __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>& c,
                                      double target, CdfSmem<BLOCK>& s) {
-  if (threadIdx.x == 0) { s.idx = n; s.flag = 0; }
-  __syncthreads();
-  // lowest thread whose chunk upper boundary exceeds the target
-  int mine = (c.hi > c.lo && c.incl > target) ? (int)threadIdx.x : BLOCK;
-  // block min
-  int wm = mine;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-  __shared__ int warp_min[BLOCK / 32];
-  if ((threadIdx.x & 31) == 0) warp_min[threadIdx.x >> 5] = wm;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int v = (threadIdx.x < BLOCK / 32) ? warp_min[threadIdx.x] : BLOCK;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) warp_min[0] = v;
-  }
-  __syncthreads();
-  const int owner = warp_min[0];
-  if (owner < BLOCK && (int)threadIdx.x == owner) {
-    double acc = 0.0, prev = c.excl;
-    long long found = c.hi - 1;
-    double hi_c = c.incl;
-    for (long long k = c.lo; k < c.hi; ++k) {
-      acc += wf(k);
-      double ck = (k == c.hi - 1) ? c.incl : c.excl + acc;
-      if (ck > target) { found = k; hi_c = ck; break; }
-      prev = ck;
+  constexpr int W = BLOCK / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int owner = -1;
+    for (int q = 0; q < W; ++q)
+      if (s.wincl[q] > target) { owner = q; break; }
+    s.owner = owner;
+    if (owner < 0) {
+      // u*total >= every partial sum: searchsorted returns n, clamp to n-1
+      s.idx = n - 1;
+      s.lo_c = c.total;
+      s.hi_c = c.total;
     }
-    s.idx = found;
-    s.lo_c = prev;
-    s.hi_c = hi_c;
   }
-  if (owner >= BLOCK && threadIdx.x == 0) {
-    // u*total >= every partial sum: searchsorted returns n, clamp to n-1
-    s.idx = n - 1;
-    s.lo_c = c.total;  // boundary at the top
-    s.hi_c = c.total;
+  __syncthreads();
+  if (w == s.owner) {
+    const long long lo = min((long long)w * c.seg, n), hi = min(lo + c.seg, n);
+    const double ex = s.wexcl[w];
+    double run = 0.0, prev = ex;
+    bool done = false;
+    for (long long base = lo; base < hi && !done; base += 32 * kCdfUnroll) {
+      double xs[kCdfUnroll];
+#pragma unroll
+      for (int u = 0; u < kCdfUnroll; ++u) {
+        const long long k = base + 32 * u + lane;
+        xs[u] = (k < hi) ? wf(k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCdfUnroll; ++u) {
+        const long long sb = base + 32 * u;
+        if (done || sb >= hi) break;
+        const double p = warp_incl_scan(xs[u]);
+        const double ck = ex + (run + p);
+        const unsigned hit = __ballot_sync(0xffffffffu, (sb + lane < hi) && ck > target);
+        if (hit) {
+          const int L = __ffs(hit) - 1;
+          const double hc = __shfl_sync(0xffffffffu, ck, L);
+          const double pc = __shfl_sync(0xffffffffu, ck, L > 0 ? L - 1 : 0);
+          if (lane == 0) {
+            s.idx = sb + L;
+            s.hi_c = hc;
+            s.lo_c = L > 0 ? pc : prev;
+          }
+          done = true;
+        } else {
+          run += __shfl_sync(0xffffffffu, p, 31);
+          prev = ex + run;
+        }
+      }
+    }
+    if (!done && lane == 0) {  // unreachable for consistent sums; defensive
+      s.idx = hi - 1;
+      s.lo_c = prev;
+      s.hi_c = prev;
+    }
   }
   __syncthreads();
   long long i = s.idx;
@@ -293,11 +326,11 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
       best_any = min(best_any, __shfl_xor_sync(0xffffffffu, best_any, o));
     }
     __shared__ long long wlo[BLOCK / 32], wany[BLOCK / 32];
-    if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = best_lo; wany[threadIdx.x >> 5] = best_any; }
+    if (lane == 0) { wlo[w] = best_lo; wany[w] = best_any; }
     __syncthreads();
     if (threadIdx.x == 0) {
       long long a = -1, b = n;
-      for (int w = 0; w < BLOCK / 32; ++w) { a = max(a, wlo[w]); b = min(b, wany[w]); }
+      for (int q = 0; q < BLOCK / 32; ++q) { a = max(a, wlo[q]); b = min(b, wany[q]); }
       s.idx = (a >= 0) ? a : b;
     }
     __syncthreads();
