@@ -45,7 +45,8 @@ def test_cur_golden(case, cuda_device):
     # -eps*total/n: a rounding-noise event, compared with slack
     assert len(info.clamped) == len(case["clamped"])
     assert all(abs(a - b) <= 2 for a, b in zip(info.clamped, case["clamped"]))
-    assert info.rebuilds == case["rebuilds"]
+    # with n = 60 a single noise-level clamp (> 1% of n) triggers a rebuild
+    assert abs(info.rebuilds - case["rebuilds"]) <= 1
     np.testing.assert_allclose(info.row_norms, arr[name + "_row_norms"], rtol=1e-6,
                                atol=1e-12 * case["total_sq_norms"][0])
     if rng is not None:
@@ -63,8 +64,11 @@ def test_gauss_operator_matches_host(cuda_device):
     np.testing.assert_allclose(op.adjoint_apply(u), K.T @ u, rtol=1e-12,
                                atol=1e-12 * np.abs(K.T @ u).max())
     np.testing.assert_allclose(op.row_norms(), np.einsum("ij,ij->i", K, K), rtol=1e-13)
-    np.testing.assert_allclose(op.row(5), K[5], rtol=2e-15, atol=0)
-    np.testing.assert_allclose(op.column(7), K[:, 7], rtol=2e-15, atol=0)
+    # entries agree to |x| ulp (x = -d^2/(2h^2) up to ~220 for these points:
+    # exp amplifies the exponent's rounding; the host divides by 2h^2, the
+    # device multiplies by 1/(2h^2)) -> 1e-13 relative
+    np.testing.assert_allclose(op.row(5), K[5], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(op.column(7), K[:, 7], rtol=1e-13, atol=0)
     # k-restricted products
     I = torch.tensor([3, 9, 400], device="cuda")
     w = torch.tensor([0.5, -1.0, 2.0], dtype=torch.float64, device="cuda")
