@@ -124,7 +124,7 @@ class ClockSampler:
 
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws > 1:
+    if ws > 1 or os.environ.get("RPLU_FORCE_SHARDED") == "1":
         import torch.distributed as dist
         backend = os.environ.get("RPLU_DIST_BACKEND", "nccl")
         dist.init_process_group(backend)
@@ -398,7 +398,7 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     tdtype = torch.float32 if cfg["dtype"] == "f32" else torch.float64
     esize = 4 if cfg["dtype"] == "f32" else 8
 
-    if world > 1:
+    if dist is not None:
         from paper_2601_22344_b200 import distributed as rdist
         return rdist.bench_sharded(args, cfg, dist, rank_id, world, dev, METRIC, UNIT)
 

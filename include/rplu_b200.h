@@ -52,6 +52,7 @@ extern "C" {
 
 /* flags */
 #define RPLU_FLAG_TIME_KERNELS 1 /* bracket K2/K3 launches with CUDA events */
+#define RPLU_FLAG_NO_GRAPH 2     /* never capture the step loop into a CUDA graph */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0

@@ -31,6 +31,7 @@ RPLU_C128 = 3
 RULE_IDS = {"rplu": 0, "c2plu": 1, "cplu": 2}
 
 FLAG_TIME_KERNELS = 1
+FLAG_NO_GRAPH = 2
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -37,6 +37,49 @@ void DevBuf::release() {
   bytes = 0;
 }
 
+int run_maybe_graph(rplu_ctx* ctx, cudaStream_t user, bool use_graph, int slot,
+                    const std::function<int(cudaStream_t)>& enqueue) {
+  if (!use_graph) return enqueue(user);
+  if (!ctx->priv) {
+    RPLU_CUDA(cudaStreamCreateWithFlags(&ctx->priv, cudaStreamNonBlocking));
+    RPLU_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+    RPLU_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  }
+  RPLU_CUDA(cudaEventRecord(ctx->ev_in, user));
+  RPLU_CUDA(cudaStreamWaitEvent(ctx->priv, ctx->ev_in, 0));
+  RPLU_CUDA(cudaStreamBeginCapture(ctx->priv, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue(ctx->priv);
+  cudaGraph_t g = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(ctx->priv, &g);
+  if (rc != RPLU_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
+  cudaGraphExec_t& ex = ctx->graph_exec[slot];
+  if (ex) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ex, g, &info) != cudaSuccess) {
+      cudaGetLastError();  // clear the sticky-free update error
+      cudaGraphExecDestroy(ex);
+      ex = nullptr;
+    }
+  }
+  if (!ex) {
+    ec = cudaGraphInstantiate(&ex, g, 0);
+    if (ec != cudaSuccess) {
+      cudaGraphDestroy(g);
+      ex = nullptr;
+      return cuda_fail(ec, "cudaGraphInstantiate");
+    }
+  }
+  cudaGraphDestroy(g);
+  RPLU_CUDA(cudaGraphLaunch(ex, ctx->priv));
+  RPLU_CUDA(cudaEventRecord(ctx->ev_out, ctx->priv));
+  RPLU_CUDA(cudaStreamWaitEvent(user, ctx->ev_out, 0));
+  return RPLU_OK;
+}
+
 int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out);
 int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long long m,
                     long long ld, double* masses, cudaStream_t s);
@@ -135,6 +178,11 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->pivots.release();
     ctx->resid.release();
     for (auto& b : ctx->scratch) b.release();
+    for (auto& e : ctx->graph_exec)
+      if (e) cudaGraphExecDestroy(e);
+    if (ctx->priv) cudaStreamDestroy(ctx->priv);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   }
   delete ctx;
   return RPLU_OK;

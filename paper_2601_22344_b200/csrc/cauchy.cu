@@ -35,6 +35,7 @@ struct CauchyParams {
   double2* G;
   double2* Bt;
   double* partial;   // [splits][n] partial row masses
+  double* masses;    // n row masses (== partial when splits == 1)
   int splits;
   double2* rbuf;     // row r of the current step (m)
   double* wbuf;      // |r|^2 (m)
@@ -153,13 +154,8 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
   __shared__ int s_stop;
   __shared__ double s_max[B / 32];
   const long long n = q.n, t = q.t;
-  const double* part = q.partial;
-  const int S = q.splits;
-  auto wrow = [&](long long k) {
-    double s = 0.0;
-    for (int z = 0; z < S; ++z) s += part[(long long)z * n + k];
-    return s;
-  };
+  const double* masses = q.masses;
+  auto wrow = [&](long long k) { return masses[k]; };
   Cdf<B> cr = cdf_build<B>(wrow, n, sm);
   // umax over rows
   double mx = 0.0;
@@ -491,6 +487,8 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
     RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * nu,
                               cudaMemcpyHostToDevice, s));
   q.partial = reinterpret_cast<double*>(ctx->scratch[0].ptr);
+  if ((rc = ctx->masses.ensure(sizeof(double) * (size_t)n))) return rc;
+  q.masses = q.splits > 1 ? reinterpret_cast<double*>(ctx->masses.ptr) : q.partial;
   q.rbuf = reinterpret_cast<double2*>(ctx->scratch[1].ptr);
   q.wbuf = reinterpret_cast<double*>(ctx->scratch[2].ptr);
   double2* gsnap = reinterpret_cast<double2*>(ctx->scratch[3].ptr);
@@ -506,35 +504,47 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   double* bb = reinterpret_cast<double*>(ctx->resid.ptr);
   q.bmax = bb;
   q.bsum = bb + K + 1;
-  cauchy_init_state<<<1, 1, 0, s>>>(q.st);
-
   const bool timing = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
   std::vector<cudaEvent_t> ev;
   long long launches = 1;
   const int upd_blocks = (int)std::min<long long>((n + m + 255) / 256, 8LL * ctx->sm_count);
   const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
-  for (long long t = 0; t < K; ++t) {
-    q.t = t;
-    if (timing) {
-      cudaEvent_t e0;
-      cudaEventCreate(&e0);
-      cudaEventRecord(e0, s);
-      ev.push_back(e0);
+  // per-step GPU time of tens of microseconds: capture the loop as one graph
+  const bool graph = (a->flags & RPLU_FLAG_NO_GRAPH) == 0 &&
+                     (double)n * (double)m * p <= 256.0 * 1024 * 1024 && K >= 4;
+  rc = run_maybe_graph(ctx, s, graph, 1, [&](cudaStream_t qs) -> int {
+    cauchy_init_state<<<1, 1, 0, qs>>>(q.st);
+    for (long long t = 0; t < K; ++t) {
+      q.t = t;
+      if (timing) {
+        cudaEvent_t e0;
+        cudaEventCreate(&e0);
+        cudaEventRecord(e0, qs);
+        ev.push_back(e0);
+      }
+      RPLU_P_SWITCH(p, launch_mass<PP>(q, qs));
+      if (timing) {
+        cudaEvent_t e1;
+        cudaEventCreate(&e1);
+        cudaEventRecord(e1, qs);
+        ev.push_back(e1);
+      }
+      if (q.splits > 1) {
+        sum_partials_kernel<<<(unsigned)((n + 255) / 256), 256, 0, qs>>>(q.partial, q.splits, n,
+                                                                          q.masses);
+        ++launches;
+      }
+      cauchy_select_row_kernel<<<1, 1024, 0, qs>>>(q);
+      RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, qs>>>(q)));
+      cauchy_select_col_kernel<<<1, 1024, 0, qs>>>(q);
+      cauchy_snapshot_kernel<<<1, 32, 0, qs>>>(q, gsnap);
+      RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, qs>>>(q, gsnap)));
+      launches += 6;
     }
-    RPLU_P_SWITCH(p, launch_mass<PP>(q, s));
-    if (timing) {
-      cudaEvent_t e1;
-      cudaEventCreate(&e1);
-      cudaEventRecord(e1, s);
-      ev.push_back(e1);
-    }
-    cauchy_select_row_kernel<<<1, 1024, 0, s>>>(q);
-    RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, s>>>(q)));
-    cauchy_select_col_kernel<<<1, 1024, 0, s>>>(q);
-    cauchy_snapshot_kernel<<<1, 32, 0, s>>>(q, gsnap);
-    RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, s>>>(q, gsnap)));
-    launches += 6;
-  }
+    RPLU_CUDA(cudaGetLastError());
+    return RPLU_OK;
+  });
+  if (rc) return rc;
   RPLU_CUDA(cudaGetLastError());
   DevState hs;
   RPLU_CUDA(cudaMemcpyAsync(&hs, q.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));

@@ -399,7 +399,6 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * nu,
                               cudaMemcpyHostToDevice, s));
   DevState* st = reinterpret_cast<DevState*>(ctx->state.ptr);
-  init_state_kernel<<<1, 1, 0, s>>>(st);
 
   DenseParams p{};
   p.R = a->R;
@@ -424,12 +423,20 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   LoopTiming tm;
   tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
   long long launches = 0;
-  switch (a->dtype) {
-    case RPLU_F64: rc = dense_loop<double>(p, s, tm, &launches); break;
-    case RPLU_F32: rc = dense_loop<float>(p, s, tm, &launches); break;
-    case RPLU_C128: rc = dense_loop<double2>(p, s, tm, &launches); break;
-    default: set_error("unknown dtype"); return RPLU_ERR_ARG;
-  }
+  // Small residuals (per-step GPU time of a few microseconds) are host-launch
+  // bound: enqueue the whole loop as one CUDA graph.
+  const bool graph = (a->flags & RPLU_FLAG_NO_GRAPH) == 0 &&
+                     (double)n * (double)m <= 64.0 * 1024 * 1024 && steps >= 4;
+  rc = run_maybe_graph(ctx, s, graph, 0, [&](cudaStream_t q) -> int {
+    init_state_kernel<<<1, 1, 0, q>>>(st);
+    switch (a->dtype) {
+      case RPLU_F64: return dense_loop<double>(p, q, tm, &launches);
+      case RPLU_F32: return dense_loop<float>(p, q, tm, &launches);
+      case RPLU_C128: return dense_loop<double2>(p, q, tm, &launches);
+    }
+    set_error("unknown dtype");
+    return RPLU_ERR_ARG;
+  });
   if (rc) return rc;
 
   DevState hs;

@@ -182,7 +182,7 @@ struct Cdf {
   double total;
 };
 
-constexpr int kCdfUnroll = 4;  // slabs in flight per warp
+constexpr int kCdfUnroll = 8;  // slabs in flight per warp
 
 __device__ __forceinline__ double warp_incl_scan(double x) {
   const int lane = threadIdx.x & 31;

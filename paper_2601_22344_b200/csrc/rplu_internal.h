@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <functional>
 #include <string>
 
 #include "../../include/rplu_b200.h"
@@ -95,9 +96,22 @@ struct DevBuf {
 
 }  // namespace rplu
 
+namespace rplu {
+// Enqueue work either directly on `user` or captured into a CUDA graph on the
+// context's private stream (one graph launch instead of one launch per
+// kernel: the latency-bound configs are otherwise host-launch bound).  The
+// graph is ordered after earlier work on `user` and before later work on it;
+// the instantiated graph of each slot is cached and updated in place.
+int run_maybe_graph(rplu_ctx* ctx, cudaStream_t user, bool use_graph, int slot,
+                    const std::function<int(cudaStream_t)>& enqueue);
+}  // namespace rplu
+
 struct rplu_ctx {
   int device = 0;
   int sm_count = 148;
+  cudaStream_t priv = nullptr;       // capture stream
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t graph_exec[4] = {nullptr, nullptr, nullptr, nullptr};
   rplu::DevBuf state;       // DevState
   rplu::DevBuf masses;      // n doubles
   rplu::DevBuf rowmax;      // n doubles (CPLU)

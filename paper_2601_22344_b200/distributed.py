@@ -46,7 +46,7 @@ def shard_rows(n, world, rank):
 
 
 def _all_gather_scalar(x, group, world):
-    if world == 1:
+    if not dist.is_initialized():
         return x.reshape(1)
     parts = [torch.empty_like(x.reshape(1)) for _ in range(world)]
     dist.all_gather(parts, x.reshape(1), group=group)
@@ -62,7 +62,7 @@ def run_sharded(backend, steps, group=None, poll_every=32, step_hook=None):
         header = backend.select(t, totals)
         if t == steps:
             break
-        if world > 1:
+        if dist.is_initialized():   # (also at world 1: exercises the NCCL path)
             dist.all_reduce(header, op=dist.ReduceOp.SUM, group=group)
             dist.all_reduce(backend.u_row(t), op=dist.ReduceOp.SUM, group=group)
         if step_hook is not None:
