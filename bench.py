@@ -229,13 +229,18 @@ def run_cauchy_arm(args, cfg):
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
+    # graph-captured loop for small sizes; K5 durations then from a second,
+    # per-launch-evented pass (as in the dense leg)
+    graphable = float(n) * n * p <= 256.0 * 1024 * 1024
     ev0.record()
     for _ in range(args.steps):
-        tr = one_run(True)
+        tr = one_run(not graphable)
         stats.append(tr.kernel_stats)
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
+    if graphable:
+        stats = [one_run(True).kernel_stats for _ in range(args.steps)]
     clk = clocks.stop()
     k = tr.rank
     value = args.steps * k / (total_ms / 1e3)
@@ -420,15 +425,22 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     clocks.start()
     time.sleep(0.3)
     stats = []
+    # Small residuals run as one CUDA graph per elimination (host-launch
+    # bound otherwise); graph-recorded events cannot be timed, so for them the
+    # K3 launch durations come from a second pass of the same K runs with
+    # per-launch events (plain stream launches).  Large residuals: one pass.
+    graphable = n * n <= 64 * 1024 * 1024
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record()
     for _ in range(args.steps):
-        tr = one_run(time_kernels=True)
+        tr = one_run(time_kernels=not graphable)
         stats.append(tr.kernel_stats)
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
+    if graphable:
+        stats = [one_run(time_kernels=True).kernel_stats for _ in range(args.steps)]
     clk = clocks.stop()
     pivots_done = tr.steps
     value = args.steps * pivots_done / (total_ms / 1e3)
@@ -506,15 +518,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3f64", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--rank", type=int, default=None)
+    # (not --n / --rank: torchrun's parser would claim those prefixes)
+    ap.add_argument("--size", type=int, default=None, help="override n (= m)")
+    ap.add_argument("--pivots", type=int, default=None, help="override the rank k")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
-    if args.n:
-        cfg["n"] = args.n
-        cfg["desc"] += f" [n overridden to {args.n}]"
-    if args.rank:
-        cfg["rank"] = args.rank
+    if args.size:
+        cfg["n"] = args.size
+        cfg["desc"] += f" [n overridden to {args.size}]"
+    if args.pivots:
+        cfg["rank"] = args.pivots
     dist, rank_id, world = _dist()
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank_id)

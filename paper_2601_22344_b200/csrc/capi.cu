@@ -106,13 +106,16 @@ static int gauss_check(const rplu_gauss_op* op) {
   return RPLU_OK;
 }
 
+// coordinate scale 1/(sqrt(2) h): |sc p - sc q|^2 = |p - q|^2 / (2 h^2)
+static double gauss_scale(double h) { return 1.0 / (1.4142135623730951 * h); }
+
 static GaussOp gauss_of(const rplu_gauss_op* op, bool adjoint) {
   GaussOp g;
   g.n = adjoint ? op->m : op->n;
   g.m = adjoint ? op->n : op->m;
   g.P = adjoint ? op->Q : op->P;
   g.Q = adjoint ? op->P : op->Q;
-  g.c = 1.0 / (2.0 * op->h * op->h);
+  g.c = gauss_scale(op->h);
   return g;
 }
 int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
@@ -519,7 +522,7 @@ int rplu_gauss_line(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis, int64_
   if (index < 0 || index >= lim) { set_error("index out of range"); return RPLU_ERR_ARG; }
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
-  const double c = 1.0 / (2.0 * op->h * op->h);
+  const double c = gauss_scale(op->h);
   if (axis == 0) return gauss_line_impl(op->Q, op->m, op->P + 3 * index, c, out,
                                         reinterpret_cast<cudaStream_t>(stream));
   return gauss_line_impl(op->P, op->n, op->Q + 3 * index, c, out,
@@ -538,7 +541,7 @@ int rplu_gauss_restricted(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis,
   if (k > 12000) { set_error("restricted product supports k <= 12000"); return RPLU_ERR_ARG; }
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
-  const double c = 1.0 / (2.0 * op->h * op->h);
+  const double c = gauss_scale(op->h);
   const long long* s = reinterpret_cast<const long long*>(sel);
   if (axis == 0)  // out[m] = A[sel,:]^T w : targets Q, selected P[sel]
     return gauss_restricted_impl(ctx, op->Q, op->m, op->P, s, w, k, c, out,

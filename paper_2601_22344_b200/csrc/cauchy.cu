@@ -510,7 +510,7 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   const int upd_blocks = (int)std::min<long long>((n + m + 255) / 256, 8LL * ctx->sm_count);
   const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
   // per-step GPU time of tens of microseconds: capture the loop as one graph
-  const bool graph = (a->flags & RPLU_FLAG_NO_GRAPH) == 0 &&
+  const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      (double)n * (double)m * p <= 256.0 * 1024 * 1024 && K >= 4;
   rc = run_maybe_graph(ctx, s, graph, 1, [&](cudaStream_t qs) -> int {
     cauchy_init_state<<<1, 1, 0, qs>>>(q.st);

@@ -65,11 +65,14 @@ __device__ __forceinline__ double exp_nonpos(double x, double tlane) {
   return x < -708.0 ? 0.0 : p * ts;
 }
 
+// Entry from coordinates prescaled by sc = 1/(sqrt(2) h) (done once per
+// point as it is loaded into registers / shared memory), so the exponent
+// -|p-q|^2/(2h^2) is just -|p'-q'|^2: 18 FP64-pipe operations per entry.
 __device__ __forceinline__ double gauss_entry(double px, double py, double pz, double qx,
-                                              double qy, double qz, double c, double tlane) {
+                                              double qy, double qz, double tlane) {
   const double dx = px - qx, dy = py - qy, dz = pz - qz;
   const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  return exp_nonpos(-c * d2, tlane);
+  return exp_nonpos(-d2, tlane);
 }
 
 // ---------------------------------------------------------------------------
@@ -91,9 +94,9 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
   for (int r = 0; r < RPT; ++r) {
     long long i = row_base + threadIdx.x + (long long)r * NT;
     long long ii = i < op.n ? i : 0;
-    px[r] = op.P[ii * 3 + 0];
-    py[r] = op.P[ii * 3 + 1];
-    pz[r] = op.P[ii * 3 + 2];
+    px[r] = op.c * op.P[ii * 3 + 0];
+    py[r] = op.c * op.P[ii * 3 + 1];
+    pz[r] = op.c * op.P[ii * 3 + 2];
     acc[r] = 0.0;
   }
   for (long long jt = j0; jt < j1; jt += TJ) {
@@ -101,9 +104,9 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
     __syncthreads();
     for (int cc = threadIdx.x; cc < cnt; cc += NT) {
       const long long j = jt + cc;
-      sq[cc * 4 + 0] = op.Q[j * 3 + 0];
-      sq[cc * 4 + 1] = op.Q[j * 3 + 1];
-      sq[cc * 4 + 2] = op.Q[j * 3 + 2];
+      sq[cc * 4 + 0] = op.c * op.Q[j * 3 + 0];
+      sq[cc * 4 + 1] = op.c * op.Q[j * 3 + 1];
+      sq[cc * 4 + 2] = op.c * op.Q[j * 3 + 2];
       sq[cc * 4 + 3] = SQUARE ? 1.0 : v[j];
     }
     __syncthreads();
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
       const double vj = sq[cc * 4 + 3];
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const double e = gauss_entry(px[r], py[r], pz[r], qx, qy, qz, op.c, tl);
+        const double e = gauss_entry(px[r], py[r], pz[r], qx, qy, qz, tl);
         acc[r] = SQUARE ? fma(e, e, acc[r]) : fma(e, vj, acc[r]);
       }
     }
@@ -136,14 +139,15 @@ __global__ void reduce_splits_kernel(const double* partial, int splits, long lon
 // K8: single row A[i,:] (m) or column A[:,j] (n) — out[k] = entry(base, pts[k])
 __global__ void gauss_line_kernel(const double* __restrict__ pts, long long count,
                                   const double* __restrict__ base, double c, double* out) {
-  const double bx = base[0], by = base[1], bz = base[2];
+  const double bx = c * base[0], by = c * base[1], bz = c * base[2];
   const double tl = exp2tab_lane();
   const long long stride = (long long)gridDim.x * blockDim.x;
   // warp-uniform trip count (the exp's table shuffle needs every lane)
   for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < count; k0 += stride) {
     const long long k = k0 + threadIdx.x;
     const long long kk = k < count ? k : count - 1;
-    const double e = gauss_entry(bx, by, bz, pts[kk * 3], pts[kk * 3 + 1], pts[kk * 3 + 2], c, tl);
+    const double e = gauss_entry(bx, by, bz, c * pts[kk * 3], c * pts[kk * 3 + 1],
+                                 c * pts[kk * 3 + 2], tl);
     if (k < count) out[k] = e;
   }
 }
@@ -159,9 +163,9 @@ __global__ void __launch_bounds__(256) gauss_restricted_kernel(
   extern __shared__ double ss[];  // k * 4
   for (long long s = threadIdx.x; s < k; s += blockDim.x) {
     const long long ix = sel[s];
-    ss[s * 4 + 0] = selpts[ix * 3 + 0];
-    ss[s * 4 + 1] = selpts[ix * 3 + 1];
-    ss[s * 4 + 2] = selpts[ix * 3 + 2];
+    ss[s * 4 + 0] = c * selpts[ix * 3 + 0];
+    ss[s * 4 + 1] = c * selpts[ix * 3 + 1];
+    ss[s * 4 + 2] = c * selpts[ix * 3 + 2];
     ss[s * 4 + 3] = w[s];
   }
   __syncthreads();
@@ -170,10 +174,11 @@ __global__ void __launch_bounds__(256) gauss_restricted_kernel(
   for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < count; t0 += stride) {
     const long long t = t0 + threadIdx.x;
     const long long tt = t < count ? t : count - 1;
-    const double tx = targets[tt * 3], ty = targets[tt * 3 + 1], tz = targets[tt * 3 + 2];
+    const double tx = c * targets[tt * 3], ty = c * targets[tt * 3 + 1],
+                 tz = c * targets[tt * 3 + 2];
     double acc = 0.0;
     for (long long s = 0; s < k; ++s)
-      acc = fma(gauss_entry(ss[s * 4], ss[s * 4 + 1], ss[s * 4 + 2], tx, ty, tz, c, tl),
+      acc = fma(gauss_entry(ss[s * 4], ss[s * 4 + 1], ss[s * 4 + 2], tx, ty, tz, tl),
                 ss[s * 4 + 3], acc);
     if (t < count) out[t] = acc;
   }

@@ -425,7 +425,9 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   long long launches = 0;
   // Small residuals (per-step GPU time of a few microseconds) are host-launch
   // bound: enqueue the whole loop as one CUDA graph.
-  const bool graph = (a->flags & RPLU_FLAG_NO_GRAPH) == 0 &&
+  // (per-kernel CUDA-event timing needs plain stream launches: events
+  // recorded by graph nodes cannot be timed)
+  const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      (double)n * (double)m <= 64.0 * 1024 * 1024 && steps >= 4;
   rc = run_maybe_graph(ctx, s, graph, 0, [&](cudaStream_t q) -> int {
     init_state_kernel<<<1, 1, 0, q>>>(st);

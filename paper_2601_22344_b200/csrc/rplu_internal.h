@@ -40,7 +40,8 @@ enum Status {
 };
 
 // Gaussian-kernel operator as the kernels see it (rows P, columns Q,
-// c = 1/(2h^2)); the adjoint swaps P and Q.
+// c = coordinate scale 1/(sqrt(2) h) applied as points are loaded); the
+// adjoint swaps P and Q.
 struct GaussOp {
   long long n, m;
   const double* P;  // n x 3

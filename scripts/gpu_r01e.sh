@@ -4,5 +4,5 @@ timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; 
 timeout 300 python bench.py --config c1 > gpurun_out/bench_c1.log 2>&1; echo c1=$?
 timeout 300 python bench.py --config c2 > gpurun_out/bench_c2.log 2>&1; echo c2=$?
 timeout 900 python bench.py > gpurun_out/bench_c3.log 2>&1; echo c3=$?
-RPLU_FORCE_SHARDED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --n 8192 --rank 64 --steps 2 --warmup 1 > gpurun_out/bench_sharded1.log 2>&1; echo sh=$?
+RPLU_FORCE_SHARDED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --size 8192 --pivots 64 --steps 2 --warmup 1 > gpurun_out/bench_sharded1.log 2>&1; echo sh=$?
 for f in gpurun_out/*.log; do echo "== $f"; tail -n 3 $f; done
