@@ -167,15 +167,17 @@ struct CdfSmem {
 // CDF layout (one CTA of BLOCK threads).  The n weights are split into
 // BLOCK/32 contiguous warp segments of S elements (S a multiple of 32), each
 // walked in slabs of 32 consecutive elements (one coalesced load per lane).
-// Inside a slab the running sum is a warp inclusive scan p_l; slabs
-// accumulate sequentially into r_s; segments accumulate sequentially into
-// excl_w.  The CDF value of element k (warp w, slab s, lane l) is
+// Segment totals T_w (lane-private sums + fixed-order warp reduction) are
+// accumulated sequentially into excl_w / incl_w = excl_w + T_w; the owner is
+// the first segment with incl_w > target.  Inside the owner segment the walk
+// uses slab scans: the CDF value of element k (slab s, lane l) is
 //     c_k = excl_w + (r_s + p_l),
-// and the last element of segment w has c = excl_w + r_end = incl_w exactly,
-// so the segment boundaries the owner search uses are the same numbers the
-// in-segment walk reproduces.  (The reference's np.cumsum is one sequential
-// sum; the association differs, so GPU and reference draws agree except
-// within rounding of a boundary — counted as near-boundary draws.)
+// p_l the warp inclusive scan of the slab, r_s the sequential sum of the
+// previous slabs; if rounding leaves every c_k <= target < incl_w, the last
+// element of the segment is chosen (its interval ends at incl_w).  (The
+// reference's np.cumsum is one sequential sum; the association differs, so
+// GPU and reference draws agree except within rounding of a boundary —
+// counted as near-boundary draws.)
 template <int BLOCK>
 struct Cdf {
   long long seg;  // segment length S
@@ -202,6 +204,10 @@ __device__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
   c.seg = (((n + W - 1) / W) + 31) / 32 * 32;
   if (c.seg < 32) c.seg = 32;
   const long long lo = min((long long)w * c.seg, n), hi = min(lo + c.seg, n);
+  // Segment total: lane-private sums (2-3 instructions per element) then a
+  // fixed-order warp reduction.  The owner search below walks the segment
+  // with slab scans; if rounding puts the target between its running sum and
+  // this total, the segment's last element is taken (a near-boundary draw).
   double run = 0.0;
   for (long long base = lo; base < hi; base += 32 * kCdfUnroll) {
     double xs[kCdfUnroll];
@@ -211,12 +217,10 @@ __device__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
       xs[u] = (k < hi) ? wf(k) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < kCdfUnroll; ++u) {
-      if (base + 32 * u >= hi) break;
-      const double p = warp_incl_scan(xs[u]);
-      run += __shfl_sync(0xffffffffu, p, 31);
-    }
+    for (int u = 0; u < kCdfUnroll; ++u) run += xs[u];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) run += __shfl_down_sync(0xffffffffu, run, o);
   if (lane == 0) s.wincl[w] = run;  // segment total (temporarily)
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -300,10 +304,12 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
         }
       }
     }
-    if (!done && lane == 0) {  // unreachable for consistent sums; defensive
+    if (!done && lane == 0) {
+      // target within rounding of the segment's end: its last element owns
+      // the interval up to incl_w
       s.idx = hi - 1;
       s.lo_c = prev;
-      s.hi_c = prev;
+      s.hi_c = s.wincl[w];
     }
   }
   __syncthreads();
