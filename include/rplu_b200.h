@@ -11,9 +11,11 @@
  *   rplu_cauchy_run  replaces rplu.cauchy.structured_eliminate with plan=None
  *                    (pkg/src/rplu/cauchy.py:177-256) and exact_row_norms
  *                    (cauchy.py:129-137)
- *   rplu_cur_run     replaces rplu.lowmem_cur.cur_build
- *                    (pkg/src/rplu/lowmem_cur.py:212-300) for device
- *                    operators (dense matrix, Gaussian kernel on points)
+ *   rplu_gauss_*, rplu_cur_downdate, rplu_sample_index
+ *                    the device primitives of rplu.lowmem_cur.cur_build
+ *                    (pkg/src/rplu/lowmem_cur.py:212-300) for the
+ *                    Gaussian-kernel operator; the host driver sequences them
+ *   rplu_shard_*     row-block sharded eliminate across GPUs
  *
  * Conventions
  *   - extern "C", plain pointers and sizes, no exceptions cross the ABI.
@@ -115,9 +117,10 @@ int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* o
  * driver (paper_2601_22344_b200.distributed) interleaves these calls with two
  * collectives per step on the same stream:
  *   begin -> allgather(local_total) ->
- *   for t: select(t) -> allreduce_sum(header[4], U[t,:]) -> update(t)
- *          -> allgather(local_total)
+ *   for t: select(t) -> allreduce_sum(msg) -> update(t) -> allgather(local_total)
  *   select(steps) (final residual norm) -> finish.
+ * With t = -1 the kernels read the step from a device counter, so one step
+ * (kernels + collectives) can be captured in a CUDA graph and replayed.
  * Non-owning ranks contribute -0.0, so the sums reproduce the owner's bits. */
 
 typedef struct rplu_shard_args {
@@ -142,11 +145,14 @@ typedef struct rplu_shard_args {
  * mass total to local_total (device double). */
 int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_total);
 /* Global owner selection from totals[world] (device), owner's row/column draw;
- * writes header[4] (device doubles) and U[t,:] (owner bits or -0.0). */
+ * writes the pivot message msg (device, 32 + m*sizeof(element) bytes):
+ * [i_global, j, a_re, a_im] as fp64, then the pivot row (owner bits, or -0.0
+ * on the other ranks).  t < 0: take the step from the device counter. */
 int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* totals,
-                      double* header);
-/* Post the reduced header, K3 fused update of the local rows, local total. */
-int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* header,
+                      void* msg);
+/* Post the reduced message (state + U[t,:]), K3 fused update of the local
+ * rows, local total; advances the device step counter. */
+int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const void* msg,
                       double* local_total);
 /* 1 if the loop is still running (synchronizes the stream). */
 int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active);

@@ -365,6 +365,7 @@ __global__ void shard_init_state(DevState* st) {
   st->status = 0;
   st->fro0 = 0.0;
   st->done = 0;
+  st->step = 0;
 }
 
 int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_total) {
@@ -390,34 +391,32 @@ int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_tota
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
                                  masses, nullptr, 0, false, s)))
       return rc;
-    return shard_total_impl(masses, a->n_local, local_total, s);
   }
-  RPLU_CUDA(cudaMemsetAsync(local_total, 0, sizeof(double), s));
-  return RPLU_OK;
+  return shard_total_impl(masses, a->n_local, local_total, nullptr, s);
 }
 
 int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* totals,
-                      double* header) {
+                      void* msg) {
   int rc;
   if ((rc = shard_check(ctx, a))) return rc;
-  if (!totals || !header || t < 0 || t > a->steps) {
+  if (!totals || !msg || t > a->steps) {
     set_error("rplu_shard_select: bad arguments");
     return RPLU_ERR_ARG;
   }
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
   ShardParams p = shard_params(ctx, a);
-  p.t = t;
+  p.t = t < 0 ? -1 : t;
   p.totals = totals;
-  p.header = header;
+  p.msg = msg;
   return shard_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
 }
 
-int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* header,
+int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const void* msg,
                       double* local_total) {
   int rc;
   if ((rc = shard_check(ctx, a))) return rc;
-  if (!header || !local_total || t < 0 || t >= a->steps) {
+  if (!msg || !local_total || t >= a->steps) {
     set_error("rplu_shard_update: bad arguments");
     return RPLU_ERR_ARG;
   }
@@ -425,17 +424,15 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   if (g.rc) return g.rc;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
   ShardParams p = shard_params(ctx, a);
-  p.t = t;
-  p.header = const_cast<double*>(header);
+  p.t = t < 0 ? -1 : t;
+  p.msg = const_cast<void*>(msg);
   if ((rc = shard_post_impl(p, s))) return rc;
   if (a->n_local > 0) {
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
-                                 p.masses, p.st, t, true, s)))
+                                 p.masses, p.st, p.t, true, s)))
       return rc;
-    return shard_total_impl(p.masses, a->n_local, local_total, s);
   }
-  RPLU_CUDA(cudaMemsetAsync(local_total, 0, sizeof(double), s));
-  return RPLU_OK;
+  return shard_total_impl(p.masses, a->n_local, local_total, p.st, s);
 }
 
 int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active) {

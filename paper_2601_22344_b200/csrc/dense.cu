@@ -94,6 +94,9 @@ __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
   if (UPDATE && !p.st->active) return;
   const long long row0 = (long long)blockIdx.x * RB;
   const long long n = p.n, m = p.m, ld = p.ld;
+  // step index: the launch argument, or the device counter (t < 0, sharded
+  // graph replay)
+  const long long t = (UPDATE && p.t < 0) ? p.st->step : p.t;
   T* R = reinterpret_cast<T*>(p.R);
   __shared__ T lval[RB];
   if (UPDATE) {
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
       if (k < n) {
         typename S::coef_t cf = load_coef<T>(p.st);
         lv = S::scale(R[k * ld + p.st->pj], cf);
-        reinterpret_cast<T*>(p.Lt)[p.t * n + k] = lv;
+        reinterpret_cast<T*>(p.Lt)[t * n + k] = lv;
       }
       lval[threadIdx.x] = lv;
     }
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
   T lv[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) lv[r] = UPDATE ? lval[r] : S::zero();
-  const T* prow = UPDATE ? reinterpret_cast<const T*>(p.U) + p.t * p.ldu : nullptr;
+  const T* prow = UPDATE ? reinterpret_cast<const T*>(p.U) + t * p.ldu : nullptr;
 
   double acc[RB];
   double mx[RB];

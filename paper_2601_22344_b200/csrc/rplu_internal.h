@@ -17,6 +17,7 @@ struct DevState {
   long long pi, pj;         // pivot of the current step
   long long err_i, err_j;   // zero pivot location
   long long done;           // pivots committed
+  long long step;           // device step counter (sharded graph replay)
   int active;               // 1 while the loop runs
   int status;               // 0 running/ok, 1 clean stop, 2 tol stop, 3 degenerate,
                             // -2 zero pivot, -1 uniform stream exhausted
@@ -63,14 +64,15 @@ struct ShardParams {
   int world, rank;
   const double* uniforms;
   long long n_uniforms;
-  double* header;  // 4 doubles: i_global, j, a_re, a_im
+  void* msg;  // [i_global, j, a_re, a_im] (fp64) followed by the pivot row (T)
   double* resid;
   long long* pivots;
   double stop_tol;
 };
 int shard_select_impl(const ShardParams& p, cudaStream_t s);
 int shard_post_impl(const ShardParams& p, cudaStream_t s);
-int shard_total_impl(const double* masses, long long n, double* out, cudaStream_t s);
+int shard_total_impl(const double* masses, long long n, double* out, DevState* advance,
+                     cudaStream_t s);
 
 // K1 (update=false) / K3 (update=true) on a row block, from dense.cu; the
 // pivot (pj, coefficients) is read from *st and the pivot row from U[t,:].

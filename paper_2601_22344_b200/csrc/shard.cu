@@ -6,16 +6,21 @@
 //                      owning shard with u1 (every rank computes the same
 //                      owner from the same totals); the owner draws the local
 //                      row (absolute target u1*T - prefix) and the column
-//                      (u2 over |R_i,:|^2) and writes the message
-//                      header = [i_global, j, a_re, a_im] (fp64) and the pivot
-//                      row into U[t,:]; the other ranks write -0.0 everywhere
-//   (host)   allreduce(sum) of header and U[t,:]: x + (-0) == x exactly, so
-//            the sum reproduces the owner's bits on every rank (root-free: no
-//            host round trip to learn the owner)
-//   update   post the header into the device state, K3 fused Schur update +
-//            masses on the local rows (the same kernel as one GPU), local total
+//                      (u2 over |R_i,:|^2) and writes the pivot message
+//                      msg = [i_global, j, a_re, a_im (4 fp64) | pivot row];
+//                      the other ranks write -0.0 everywhere
+//   (host)   ONE allreduce(sum) of msg: x + (-0) == x exactly, so the sum
+//            reproduces the owner's bits on every rank (root-free: no host
+//            round trip to learn the owner)
+//   update   post the header into the device state and copy the pivot row
+//            into U[t,:] (multi-CTA), K3 fused Schur update + masses on the
+//            local rows (the same kernel as one GPU), local total; the step
+//            counter advances on the device
 //   (host)   allgather of the local totals for the next step
-// The stop rules use the global total, so every rank stops at the same step.
+// With t < 0 every kernel takes the step from the device counter, so one
+// step (kernels + collectives) can be captured once in a CUDA graph and
+// replayed.  Stop rules use the global total: every rank stops at the same
+// step, and stopped ranks keep contributing -0.0 so collectives stay matched.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,22 +41,31 @@ template <> __device__ __forceinline__ double neg_zero<double>() { return -0.0; 
 template <> __device__ __forceinline__ float neg_zero<float>() { return -0.0f; }
 template <> __device__ __forceinline__ double2 neg_zero<double2>() { return make_double2(-0.0, -0.0); }
 
+__device__ __forceinline__ long long shard_step(const ShardParams& p) {
+  return p.t >= 0 ? p.t : p.st->step;
+}
+
+template <typename T>
+__device__ __forceinline__ void msg_neg_zero(const ShardParams& p) {
+  double* hdr = reinterpret_cast<double*>(p.msg);
+  T* prow = reinterpret_cast<T*>(hdr + 4);
+  for (long long k = threadIdx.x; k < p.m; k += blockDim.x) prow[k] = neg_zero<T>();
+  if (threadIdx.x < 4) hdr[threadIdx.x] = -0.0;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(1024) shard_select_kernel(ShardParams p) {
   using S = Scalar<T>;
   constexpr int B = 1024;
   DevState* st = p.st;
-  const long long t = p.t;
-  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
   __shared__ CdfSmem<B> sm;
   __shared__ int s_owner, s_stop;
-  __shared__ double s_target, s_total;
+  __shared__ double s_target;
   if (!st->active) {
-    // keep the collective well-formed after a stop: contribute -0
-    for (long long k = threadIdx.x; k < p.m; k += B) urow[k] = neg_zero<T>();
-    if (threadIdx.x < 4) p.header[threadIdx.x] = -0.0;
+    msg_neg_zero<T>(p);  // keep the collective well-formed after a stop
     return;
   }
+  const long long t = shard_step(p);
   if (threadIdx.x == 0) {
     // global total over shards, in rank order (identical on every rank)
     double T_all = 0.0;
@@ -104,18 +118,11 @@ __global__ void __launch_bounds__(1024) shard_select_kernel(ShardParams p) {
     s_stop = stop;
     s_owner = owner;
     s_target = target;
-    s_total = T_all;
   }
   __syncthreads();
-  if (s_stop) {
-    for (long long k = threadIdx.x; k < p.m; k += B) urow[k] = neg_zero<T>();
-    if (threadIdx.x < 4) p.header[threadIdx.x] = -0.0;
-    return;
-  }
-  if (s_owner != p.rank) {
-    for (long long k = threadIdx.x; k < p.m; k += B) urow[k] = neg_zero<T>();
-    if (threadIdx.x < 4) p.header[threadIdx.x] = -0.0;
-    if (threadIdx.x == 0) st->ucount += 2;
+  if (s_stop || s_owner != p.rank) {
+    msg_neg_zero<T>(p);
+    if (!s_stop && threadIdx.x == 0) st->ucount += 2;
     return;
   }
   // owner: local row draw against the absolute target, then the column draw
@@ -135,28 +142,39 @@ __global__ void __launch_bounds__(1024) shard_select_kernel(ShardParams p) {
     const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
     if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
   }
-  for (long long k = threadIdx.x; k < p.m; k += B) urow[k] = row[k];
+  double* hdr = reinterpret_cast<double*>(p.msg);
+  T* prow = reinterpret_cast<T*>(hdr + 4);
+  for (long long k = threadIdx.x; k < p.m; k += B) prow[k] = row[k];
   if (threadIdx.x == 0) {
     const double2 a = to_pair<T>(row[j]);
-    p.header[0] = (double)(p.row_offset + i);
-    p.header[1] = (double)j;
-    p.header[2] = a.x;
-    p.header[3] = a.y;
+    hdr[0] = (double)(p.row_offset + i);
+    hdr[1] = (double)j;
+    hdr[2] = a.x;
+    hdr[3] = a.y;
     st->ucount += 2;
     st->near_boundary += near;
   }
 }
 
-// After the allreduce: every rank posts the pivot into its state.
+// After the allreduce: every rank posts the pivot into its state (CTA 0,
+// thread 0) and copies the reduced pivot row into U[t,:] (all CTAs).
 template <typename T>
 __global__ void shard_post_kernel(ShardParams p) {
   DevState* st = p.st;
   if (!st->active) return;
-  const long long ig = (long long)p.header[0];
-  const long long j = (long long)p.header[1];
+  const long long t = shard_step(p);
+  const double* hdr = reinterpret_cast<const double*>(p.msg);
+  const T* prow = reinterpret_cast<const T*>(hdr + 4);
+  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
+       k += (long long)gridDim.x * blockDim.x)
+    urow[k] = prow[k];
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const long long ig = (long long)hdr[0];
+  const long long j = (long long)hdr[1];
   T a;
-  if constexpr (sizeof(T) == sizeof(double2)) a = make_double2(p.header[2], p.header[3]);
-  else a = (T)p.header[2];
+  if constexpr (sizeof(T) == sizeof(double2)) a = make_double2(hdr[2], hdr[3]);
+  else a = (T)hdr[2];
   if (Scalar<T>::is_zero(a)) {
     st->status = kZeroPivot;
     st->active = 0;
@@ -166,32 +184,38 @@ __global__ void shard_post_kernel(ShardParams p) {
   }
   st->pi = ig;
   st->pj = j;
-  // reuse the dense coefficient layout (dense.cu store_coef)
+  // the dense coefficient layout (dense.cu store_coef)
   if constexpr (sizeof(T) == sizeof(double2)) {
-    CDivCoef c = cdiv_coef(make_double2(p.header[2], p.header[3]));
+    CDivCoef c = cdiv_coef(make_double2(hdr[2], hdr[3]));
     st->rat = c.rat;
     st->scl = c.scl;
     st->branch = c.branch;
   } else if constexpr (sizeof(T) == sizeof(double)) {
-    st->inv_d = __ddiv_rn(1.0, p.header[2]);
+    st->inv_d = __ddiv_rn(1.0, hdr[2]);
   } else {
-    st->inv_f = __fdiv_rn(1.0f, (float)p.header[2]);
+    st->inv_f = __fdiv_rn(1.0f, (float)hdr[2]);
   }
-  st->a_re = p.header[2];
-  st->a_im = p.header[3];
-  p.pivots[2 * p.t] = ig;
-  p.pivots[2 * p.t + 1] = j;
-  st->done = p.t + 1;
+  st->a_re = hdr[2];
+  st->a_im = hdr[3];
+  p.pivots[2 * t] = ig;
+  p.pivots[2 * t + 1] = j;
+  st->done = t + 1;
 }
 
-// local total of the masses, fixed order (chunk sums then serial)
+// Local total of the masses (the CDF code's fixed association); advances the
+// device step counter.
 __global__ void __launch_bounds__(1024) shard_total_kernel(const double* masses, long long n,
-                                                          double* out) {
+                                                          double* out, DevState* advance) {
   constexpr int B = 1024;
   __shared__ CdfSmem<B> sm;
-  auto w = [&](long long k) { return masses[k]; };
-  Cdf<B> c = cdf_build<B>(w, n, sm);
-  if (threadIdx.x == 0) *out = c.total;
+  if (n > 0) {
+    auto w = [&](long long k) { return masses[k]; };
+    Cdf<B> c = cdf_build<B>(w, n, sm);
+    if (threadIdx.x == 0) *out = c.total;
+  } else if (threadIdx.x == 0) {
+    *out = 0.0;
+  }
+  if (advance && threadIdx.x == 0) advance->step += 1;
 }
 
 template <typename T>
@@ -203,7 +227,8 @@ static int shard_select_t(const ShardParams& p, cudaStream_t s) {
 
 template <typename T>
 static int shard_post_t(const ShardParams& p, cudaStream_t s) {
-  shard_post_kernel<T><<<1, 1, 0, s>>>(p);
+  const int blocks = (int)((p.m + 1023) / 1024 < 64 ? (p.m + 1023) / 1024 : 64);
+  shard_post_kernel<T><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(p);
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
 }
@@ -228,8 +253,9 @@ int shard_post_impl(const ShardParams& p, cudaStream_t s) {
   return RPLU_ERR_ARG;
 }
 
-int shard_total_impl(const double* masses, long long n, double* out, cudaStream_t s) {
-  shard_total_kernel<<<1, 1024, 0, s>>>(masses, n, out);
+int shard_total_impl(const double* masses, long long n, double* out, DevState* advance,
+                     cudaStream_t s) {
+  shard_total_kernel<<<1, 1024, 0, s>>>(masses, n, out, advance);
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
 }

@@ -35,7 +35,8 @@ from .accessors import CapabilityError
 from .dense_pivots import EliminationTrace, PivotRule
 from .rng import UniformBlock
 
-__all__ = ["shard_rows", "run_sharded", "sharded_eliminate", "CudaShardBackend"]
+__all__ = ["shard_rows", "run_sharded", "run_sharded_graph", "sharded_eliminate",
+           "CudaShardBackend"]
 
 
 def shard_rows(n, world, rank):
@@ -45,29 +46,30 @@ def shard_rows(n, world, rank):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def _all_gather_scalar(x, group, world):
+def _all_gather_scalar(x, group, world, out=None):
     if not dist.is_initialized():
         return x.reshape(1)
-    parts = [torch.empty_like(x.reshape(1)) for _ in range(world)]
-    dist.all_gather(parts, x.reshape(1), group=group)
-    return torch.cat(parts)
+    out = torch.empty(world, dtype=x.dtype, device=x.device) if out is None else out
+    dist.all_gather_into_tensor(out, x.reshape(1), group=group)
+    return out
 
 
 def run_sharded(backend, steps, group=None, poll_every=32, step_hook=None):
-    """Collective choreography of one sharded elimination (see module doc)."""
+    """Collective choreography of one sharded elimination (see module doc):
+    per step one sum-allreduce of the pivot message and one allgather of the
+    shard totals."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     local_total = backend.begin()
     totals = _all_gather_scalar(local_total, group, world)
     for t in range(steps + 1):
-        header = backend.select(t, totals)
+        msg = backend.select(t, totals)
         if t == steps:
             break
         if dist.is_initialized():   # (also at world 1: exercises the NCCL path)
-            dist.all_reduce(header, op=dist.ReduceOp.SUM, group=group)
-            dist.all_reduce(backend.u_row(t), op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(msg, op=dist.ReduceOp.SUM, group=group)
         if step_hook is not None:
             step_hook("pre_update", t)
-        local_total = backend.update(t, header)
+        local_total = backend.update(t, msg)
         if step_hook is not None:
             step_hook("post_update", t)
         totals = _all_gather_scalar(local_total, group, world)
@@ -75,6 +77,41 @@ def run_sharded(backend, steps, group=None, poll_every=32, step_hook=None):
         # rank breaks at the same step
         if poll_every and (t + 1) % poll_every == 0 and not backend.active():
             break
+    return backend.finish()
+
+
+def run_sharded_graph(backend, steps, group=None, chunk=32):
+    """The same choreography with one step (select, allreduce, update,
+    allgather) captured once in a CUDA graph and replayed: the kernels read
+    the step index from the device counter, the collectives run on static
+    buffers.  Replays go in chunks of `chunk` steps with a stop poll between
+    chunks."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    local_total = backend.begin()
+    totals = torch.empty(world, dtype=torch.float64, device=backend.dev)
+    totals.copy_(_all_gather_scalar(local_total, group, world))
+    if steps == 0:
+        backend.select(-1, totals)
+        return backend.finish()
+    # capture on a side stream (torch.cuda.graph); the backend launches on
+    # the current stream, which the capture context switches for us
+    torch.cuda.synchronize(backend.dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        msg = backend.select(-1, totals)
+        if dist.is_initialized():
+            dist.all_reduce(msg, op=dist.ReduceOp.SUM, group=group)
+        lt = backend.update(-1, msg)
+        _all_gather_scalar(lt, group, world, out=totals)
+    done = 0
+    while done < steps:
+        n = min(chunk, steps - done)
+        for _ in range(n):
+            g.replay()
+        done += n
+        if done < steps and not backend.active():
+            break
+    backend.select(-1, totals)          # final residual norm / stop flags
     return backend.finish()
 
 
@@ -91,7 +128,13 @@ class CudaShardBackend:
         self.ldu = ((m + vec - 1) // vec) * vec
         self.Lt = torch.empty((max(steps, 1), max(n_local, 1)), dtype=R.dtype, device=self.dev)
         self.U = torch.empty((max(steps, 1) + 1, self.ldu), dtype=R.dtype, device=self.dev)
-        self.header = torch.empty(4, dtype=torch.float64, device=self.dev)
+        # pivot message: 4 fp64 header + the pivot row, reduced as one buffer
+        # (fp64 view for fp64/complex128 rows, fp32 view for fp32 rows)
+        esz = R.element_size()
+        nbytes = 32 + m * esz
+        red = torch.float32 if R.dtype == torch.float32 else torch.float64
+        self.msg = torch.empty(nbytes // torch.empty(0, dtype=red).element_size(), dtype=red,
+                               device=self.dev)
         self.total = torch.empty(1, dtype=torch.float64, device=self.dev)
         self.block = UniformBlock(rule.rng, 2 * steps + 2)
         self.steps = steps
@@ -102,44 +145,44 @@ class CudaShardBackend:
             ld=R.stride(0), row_offset=row_offset, steps=steps, stop_tol=float(stop_tol),
             R=R.data_ptr() if n_local else None, Lt=self.Lt.data_ptr(), U=self.U.data_ptr(),
             ldu=self.ldu, uniforms=self.block.pointer(), n_uniforms=self.block.values.size,
-            stream=torch.cuda.current_stream(self.dev).cuda_stream)
+            stream=None)
         c = ctx if ctx is not None else _device.ctx(self.dev)
         self._ctx = c
         self._lib, self._h = c._lib, c.handle
         self.pivots = np.zeros(2 * max(steps, 1), dtype=np.int64)
         self.resid = np.zeros(steps + 1)
-        self.out = None
 
-    def u_row(self, t):
-        return self.U[t, :self.m] if self.ldu == self.m else self.U[t]
+    def _args(self):
+        # launch on whatever stream is current (a graph capture switches it)
+        self.args.stream = torch.cuda.current_stream(self.dev).cuda_stream
+        return ctypes.byref(self.args)
 
     def begin(self):
-        _ffi.check(self._lib.rplu_shard_begin(self._h, ctypes.byref(self.args),
-                                              self.total.data_ptr()))
+        _ffi.check(self._lib.rplu_shard_begin(self._h, self._args(), self.total.data_ptr()))
         return self.total
 
     def select(self, t, totals):
         totals = totals.contiguous()
         self._totals = totals   # keep alive until the kernel ran
-        _ffi.check(self._lib.rplu_shard_select(self._h, ctypes.byref(self.args), t,
-                                               totals.data_ptr(), self.header.data_ptr()))
-        return self.header
+        _ffi.check(self._lib.rplu_shard_select(self._h, self._args(), t, totals.data_ptr(),
+                                               self.msg.data_ptr()))
+        return self.msg
 
-    def update(self, t, header):
-        _ffi.check(self._lib.rplu_shard_update(self._h, ctypes.byref(self.args), t,
-                                               header.data_ptr(), self.total.data_ptr()))
+    def update(self, t, msg):
+        _ffi.check(self._lib.rplu_shard_update(self._h, self._args(), t, msg.data_ptr(),
+                                               self.total.data_ptr()))
         return self.total
 
     def active(self):
         a = ctypes.c_int32(0)
-        _ffi.check(self._lib.rplu_shard_active(self._h, ctypes.byref(self.args), ctypes.byref(a)))
+        _ffi.check(self._lib.rplu_shard_active(self._h, self._args(), ctypes.byref(a)))
         return bool(a.value)
 
     def finish(self):
         out = _ffi.DenseOut(
             pivots=self.pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
             resid_fro=self.resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-        status = self._lib.rplu_shard_finish(self._h, ctypes.byref(self.args), ctypes.byref(out))
+        status = self._lib.rplu_shard_finish(self._h, self._args(), ctypes.byref(out))
         self.block.commit(out.uniforms_consumed)
         _ffi.check(status)
         k = int(out.steps_done)
@@ -153,7 +196,7 @@ class CudaShardBackend:
 
 
 def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None,
-                      compute_dtype=None, overwrite_a=False, step_hook=None):
+                      compute_dtype=None, overwrite_a=False, step_hook=None, graph=False):
     """RPLU on a row-block shard (call on every rank with the same rule seed).
 
     ``A_local`` is this rank's contiguous row block (global rows
@@ -174,7 +217,10 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
         R = _device.padded_residual(src)[0]
     n_local, m = src.shape
     backend = CudaShardBackend(R, row_offset, world, rank, rule, steps, stop_tol)
-    res = run_sharded(backend, steps, group=group, step_hook=step_hook)
+    if graph and step_hook is None:
+        res = run_sharded_graph(backend, steps, group=group)
+    else:
+        res = run_sharded(backend, steps, group=group, step_hook=step_hook)
     tr = EliminationTrace(
         pivots=res["pivots"], L=res["L_local"], U=res["U"], resid_fro=res["resid_fro"],
         residual=R[:, :m], steps=res["steps"], clean_early_stop=res["clean_early_stop"],
@@ -191,7 +237,7 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
     CUDA events per rank, max over ranks.
     """
     import json
-    import time
+    import os
 
     from . import gen
 
@@ -211,9 +257,12 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
         e.record()
         sweep_ev.append(e)
 
+    use_graph = os.environ.get("RPLU_SHARD_GRAPH", "1") == "1"
+
     def one(timed=False):
         return sharded_eliminate(A_loc, lo, PivotRule("rplu", _rng(seed)), k,
-                                 compute_dtype=tdtype, step_hook=hook if timed else None)
+                                 compute_dtype=tdtype, step_hook=hook if timed else None,
+                                 graph=use_graph and not timed)
 
     for _ in range(args.warmup):
         one()
@@ -222,10 +271,16 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        tr = one(timed=True)
+        tr = one(timed=not use_graph)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if use_graph:
+        # per-update durations from a second, hook-timed (non-graph) pass
+        dist_mod.barrier()
+        for _ in range(args.steps):
+            one(timed=True)
+        torch.cuda.synchronize()
     upd = sum(sweep_ev[2 * q].elapsed_time(sweep_ev[2 * q + 1])
               for q in range(len(sweep_ev) // 2))
     nupd = len(sweep_ev) // 2
@@ -265,6 +320,7 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
             "dtype": cfg["dtype"], "data": "synthetic (seeded BASELINE construction)",
             "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": k, "seed": seed,
                        "parallelism": f"row-block shards x{world} (NCCL allgather + allreduce)",
+                       "step_loop": "CUDA graph of one step replayed" if use_graph else "host loop",
                        "step": f"one full elimination of {k} pivot steps",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -25,7 +25,7 @@ class NumpyShardBackend:
         self.stop_tol = stop_tol
         self.U = torch.zeros((steps + 1, self.m), dtype=torch.float64)
         self.L = np.zeros((self.n_local, steps))
-        self.header = torch.zeros(4, dtype=torch.float64)
+        self.msg = torch.zeros(4 + self.m, dtype=torch.float64)   # header | pivot row
         self.pivots, self.resid = [], []
         self.active_flag, self.status = True, None
         self.fro0 = None
@@ -33,22 +33,18 @@ class NumpyShardBackend:
     def _masses(self):
         return np.einsum("ij,ij->i", self.R, self.R)
 
-    def u_row(self, t):
-        return self.U[t]
-
     def begin(self):
         self.masses = self._masses()
         return torch.tensor([self.masses.sum()], dtype=torch.float64)
 
     def _neg_zero(self, t):
-        self.U[t].fill_(-0.0)
-        self.header.fill_(-0.0)
+        self.msg.fill_(-0.0)
 
     def select(self, t, totals):
         tot = totals.numpy()
         if not self.active_flag:
             self._neg_zero(t)
-            return self.header
+            return self.msg
         T = 0.0
         for s in range(self.world):
             T += tot[s]
@@ -67,7 +63,7 @@ class NumpyShardBackend:
             self.active_flag = False
             self.status = stop
             self._neg_zero(t)
-            return self.header
+            return self.msg
         u1, u2 = self.u[self.uc], self.u[self.uc + 1]
         self.uc += 2
         tg = u1 * T
@@ -81,22 +77,23 @@ class NumpyShardBackend:
             target = tot[owner]
         if owner != self.rank:
             self._neg_zero(t)
-            return self.header
+            return self.msg
         cdf = np.cumsum(self.masses)
         i = min(int(np.searchsorted(cdf, target, side="right")), self.n_local - 1)
         while i > 0 and not self.masses[i] > 0:
             i -= 1
         row = self.R[i].copy()
         j = oracle.sample_index(row * row, u2)
-        self.U[t] = torch.from_numpy(row)
-        self.header.copy_(torch.tensor([float(self.row_offset + i), float(j), row[j], 0.0]))
-        return self.header
+        self.msg[4:] = torch.from_numpy(row)
+        self.msg[:4] = torch.tensor([float(self.row_offset + i), float(j), row[j], 0.0])
+        return self.msg
 
-    def update(self, t, header):
+    def update(self, t, msg):
         if not self.active_flag:
             return torch.tensor([self.masses.sum()], dtype=torch.float64)
-        ig, j, a = int(header[0]), int(header[1]), float(header[2])
+        ig, j, a = int(msg[0]), int(msg[1]), float(msg[2])
         self.pivots.append((ig, j))
+        self.U[t] = msg[4:]
         prow = self.U[t].numpy()
         col = self.R[:, j] * (1.0 / a)
         self.L[:, t] = col

@@ -28,6 +28,21 @@ def test_world1_equals_eliminate(cuda_device):
     np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-12)
 
 
+def test_world1_graph_replay_equals_eliminate(cuda_device):
+    """One step captured in a CUDA graph and replayed (device step counter)."""
+    A = torch.from_numpy(gen.c1_dense(5, n=300, m=260)).cuda()
+    tr = sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(5)), 90, graph=True)
+    ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(5)), 90)
+    assert tr.pivots == ref.pivots
+    assert torch.equal(tr.L, ref.L) and torch.equal(tr.U, ref.U)
+    np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-12)
+    # a tol stop inside a replay chunk stops every later replay
+    trs = sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(5)), 250, stop_tol=0.5,
+                            graph=True)
+    refs = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(5)), 250, stop_tol=0.5)
+    assert trs.tol_stop and refs.tol_stop and trs.pivots == refs.pivots
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_emulated_shards(world, cuda_device):
     A = gen.c1_dense(6, n=500, m=333)
@@ -45,19 +60,16 @@ def test_emulated_shards(world, cuda_device):
         bes.append(CudaShardBackend(R, lo, world, r, rp.PivotRule("rplu", rp.RngState(seed)),
                                     steps, ctx=_ffi.Context(0)))
     totals = torch.cat([b.begin().clone() for b in bes])
+    device_t = world == 3   # exercise the device step counter (t = -1) too
     for t in range(steps + 1):
-        hs = [b.select(t, totals).clone() for b in bes]
+        tt = -1 if device_t else t
+        ms = [b.select(tt, totals).clone() for b in bes]
         if t == steps:
             break
-        h = hs[0]
-        for x in hs[1:]:
-            h = h + x
-        u = bes[0].u_row(t).clone()
-        for b in bes[1:]:
-            u = u + b.u_row(t)
-        for b in bes:
-            b.u_row(t).copy_(u)
-        totals = torch.cat([b.update(t, h).clone() for b in bes])
+        msg = ms[0]
+        for x in ms[1:]:
+            msg = msg + x     # the allreduce(sum) with -0.0 contributions
+        totals = torch.cat([b.update(tt, msg).clone() for b in bes])
     res = [b.finish() for b in bes]
     ref = oracle.eliminate_real(A, "rplu", steps, seed=seed, margins=True)
     for r in res:
