@@ -2,6 +2,7 @@
 // validation with the reference's error classes, dispatch to the paths.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -57,15 +58,21 @@ int run_maybe_graph(rplu_ctx* ctx, cudaStream_t user, bool use_graph, int slot,
   }
   if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
   cudaGraphExec_t& ex = ctx->graph_exec[slot];
+  static const bool debug = getenv("RPLU_DEBUG_GRAPH") != nullptr;
   if (ex) {
     cudaGraphExecUpdateResultInfo info;
-    if (cudaGraphExecUpdate(ex, g, &info) != cudaSuccess) {
-      cudaGetLastError();  // clear the sticky-free update error
+    cudaError_t ue = cudaGraphExecUpdate(ex, g, &info);
+    if (ue != cudaSuccess) {
+      if (debug)
+        fprintf(stderr, "[rplu] graph slot %d: exec update failed (%s, result %d)\n", slot,
+                cudaGetErrorName(ue), (int)info.result);
+      cudaGetLastError();  // clear the non-sticky update error
       cudaGraphExecDestroy(ex);
       ex = nullptr;
     }
   }
   if (!ex) {
+    if (debug) fprintf(stderr, "[rplu] graph slot %d: instantiate\n", slot);
     ec = cudaGraphInstantiate(&ex, g, 0);
     if (ec != cudaSuccess) {
       cudaGraphDestroy(g);

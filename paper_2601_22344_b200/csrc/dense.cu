@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <vector>
 
 #include "rplu_common.cuh"
@@ -87,7 +89,28 @@ template <> __device__ __forceinline__ void store_coef<double2>(DevState* st, do
 // The pivot-column entries R[k,j] are captured before any write of the row
 // (WAR hazard), L[:,t] is written transposed (Lt[t,k]) so the
 // store is coalesced.
-template <typename T, int VEC, int RB, bool UPDATE, bool TRACK_MAX>
+// 16-byte vector load/store, optionally with the streaming (evict-first)
+// cache hint so the once-per-step residual stream does not push the pivot row
+// and the masses out of L2.
+template <bool STREAM, typename V>
+__device__ __forceinline__ V vload(const V* ptr) {
+  if constexpr (STREAM && sizeof(V) == 16) {
+    uint4 u = __ldcs(reinterpret_cast<const uint4*>(ptr));
+    return *reinterpret_cast<V*>(&u);
+  } else {
+    return *ptr;
+  }
+}
+template <bool STREAM, typename V>
+__device__ __forceinline__ void vstore(V* ptr, const V& v) {
+  if constexpr (STREAM && sizeof(V) == 16) {
+    __stcs(reinterpret_cast<uint4*>(ptr), *reinterpret_cast<const uint4*>(&v));
+  } else {
+    *ptr = v;
+  }
+}
+
+template <typename T, int VEC, int RB, bool UPDATE, bool TRACK_MAX, bool STREAM = false>
 __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
   using S = Scalar<T>;
   constexpr int NT = 256;
@@ -130,7 +153,8 @@ __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
     VecT<T, VEC> rv[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r)
-      if (row0 + r < n) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (row0 + r) * ld + l);
+      if (row0 + r < n)
+        rv[r] = vload<STREAM>(reinterpret_cast<const VecT<T, VEC>*>(R + (row0 + r) * ld + l));
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       if (row0 + r < n) {
@@ -142,7 +166,7 @@ __global__ void __launch_bounds__(256) dense_sweep_kernel(DenseParams p) {
           acc[r] += S::mass(x);
           if (TRACK_MAX) argmax_merge(mx[r], mi[r], S::absval(x), l + e);
         }
-        if (UPDATE) *reinterpret_cast<VecT<T, VEC>*>(R + (row0 + r) * ld + l) = rv[r];
+        if (UPDATE) vstore<STREAM>(reinterpret_cast<VecT<T, VEC>*>(R + (row0 + r) * ld + l), rv[r]);
       }
     }
   }
@@ -333,11 +357,37 @@ static void launch_sweep(const DenseParams& p, bool update, bool track, cudaStre
   }
 }
 
+// K3 variant for experiments (RPLU_SWEEP_VARIANT, read once): 0 = 4 rows per
+// CTA (default), 1 = 4 rows + streaming hints, 2 = 8 rows, 3 = 2 rows,
+// 4 = 8 rows + streaming hints.  Only the vectorised update path varies.
+static int sweep_variant() {
+  static int v = [] {
+    const char* e = getenv("RPLU_SWEEP_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <typename T, int VEC, int RB, bool STREAM>
+static void launch_update_variant(const DenseParams& p, cudaStream_t s) {
+  dim3 grid((unsigned)((p.n + RB - 1) / RB));
+  dense_sweep_kernel<T, VEC, RB, true, false, STREAM><<<grid, 256, 0, s>>>(p);
+}
+
 template <typename T>
 static void sweep(const DenseParams& p, bool update, bool track, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   bool vec_ok = (p.ld % VEC == 0) && ((uintptr_t)p.R % 16 == 0) &&
                 (!update || ((p.ldu % VEC == 0) && ((uintptr_t)p.U % 16 == 0)));
+  if (vec_ok && update && !track) {
+    switch (sweep_variant()) {
+      case 1: launch_update_variant<T, VEC, 4, true>(p, s); return;
+      case 2: launch_update_variant<T, VEC, 8, false>(p, s); return;
+      case 3: launch_update_variant<T, VEC, 2, false>(p, s); return;
+      case 4: launch_update_variant<T, VEC, 8, true>(p, s); return;
+      default: break;
+    }
+  }
   if (vec_ok) launch_sweep<T, VEC, 4>(p, update, track, s);
   else launch_sweep<T, 1, 4>(p, update, track, s);
 }

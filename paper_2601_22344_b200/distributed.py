@@ -48,6 +48,9 @@ def shard_rows(n, world, rank):
 
 def _all_gather_scalar(x, group, world, out=None):
     if not dist.is_initialized():
+        if out is not None:      # static buffer (graph replay)
+            out.copy_(x.reshape(1))
+            return out
         return x.reshape(1)
     out = torch.empty(world, dtype=x.dtype, device=x.device) if out is None else out
     dist.all_gather_into_tensor(out, x.reshape(1), group=group)
