@@ -432,23 +432,28 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     graphable = n * n <= 64 * 1024 * 1024
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # a bench step of a small config is `reps` eliminations, so the timed
+    # region is long enough (>= ~50 ms) not to be dominated by host noise
+    reps = 20 if graphable else 1
     ev0.record()
     for _ in range(args.steps):
-        tr = one_run(time_kernels=not graphable)
-        stats.append(tr.kernel_stats)
+        for _ in range(reps):
+            tr = one_run(time_kernels=not graphable)
+            stats.append(tr.kernel_stats)
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
+    timed_launches = sum(s["kernel_launches"] for s in stats)
     if graphable:
         stats = [one_run(time_kernels=True).kernel_stats for _ in range(args.steps)]
     clk = clocks.stop()
     pivots_done = tr.steps
-    value = args.steps * pivots_done / (total_ms / 1e3)
+    value = args.steps * reps * pivots_done / (total_ms / 1e3)
 
     sweep_ms = sum(s["sweep_ms"] for s in stats)
     sweep_n = sum(s["sweep_launches"] for s in stats)
     select_ms = sum(s["select_ms"] for s in stats)
-    launches = sum(s["kernel_launches"] for s in stats)
+    launches = timed_launches
     bytes_per_launch = 2.0 * n * n * esize
     avg_s = (sweep_ms / sweep_n) / 1e3
     achieved = bytes_per_launch / avg_s / 1e9
@@ -487,7 +492,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded BASELINE construction, built on device with cuBLAS)",
         "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": rank, "seed": seed,
-                   "step": f"one full elimination of {rank} pivot steps",
+                   "step": (f"{reps} full eliminations of {rank} pivot steps" if reps > 1
+                            else f"one full elimination of {rank} pivot steps"),
                    "l2": f"inputs larger than L2 ({n * n * esize / 1e9:.1f} GB residual)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(cfg, n),
@@ -495,8 +501,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src},
         "step_breakdown_ms": {"sweep_per_pivot": sweep_ms / sweep_n,
-                              "select_per_pivot": select_ms / (args.steps * (pivots_done + 1)),
-                              "total_per_pivot": total_ms / (args.steps * pivots_done)},
+                              "select_per_pivot": select_ms / (len(stats) * (pivots_done + 1)),
+                              "total_per_pivot": total_ms / (args.steps * reps * pivots_done)},
         "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{cpu_steps} pivot steps of the oracle real-fp64 port on the "
                                    f"same {n}x{n} bytes ({cb_dt:.1f}s), row blocks over "
