@@ -480,8 +480,14 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   // bound: enqueue the whole loop as one CUDA graph.
   // (per-kernel CUDA-event timing needs plain stream launches: events
   // recorded by graph nodes cannot be timed)
+  static const int graph_env = [] {  // RPLU_GRAPH=always|never (experiments)
+    const char* e = getenv("RPLU_GRAPH");
+    if (!e) return 0;
+    return e[0] == 'a' ? 1 : (e[0] == 'n' ? -1 : 0);
+  }();
+  const bool small = (double)n * (double)m <= 64.0 * 1024 * 1024;
   const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
-                     (double)n * (double)m <= 64.0 * 1024 * 1024 && steps >= 4;
+                     steps >= 4 && graph_env >= 0 && (small || graph_env > 0);
   rc = run_maybe_graph(ctx, s, graph, 0, [&](cudaStream_t q) -> int {
     init_state_kernel<<<1, 1, 0, q>>>(st);
     switch (a->dtype) {
