@@ -454,9 +454,13 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     sweep_n = sum(s["sweep_launches"] for s in stats)
     select_ms = sum(s["select_ms"] for s in stats)
     launches = timed_launches
-    bytes_per_launch = 2.0 * n * n * esize
+    # algorithmic bytes of the timed update launches: 2*n*m*s for an eager
+    # update or a delayed-update flush, n*m*s for a delayed-update read pass
+    sweep_bytes = sum(s.get("sweep_bytes", 0.0) for s in stats)
+    lazy_block = stats[-1].get("lazy_block", 0)
+    bytes_per_launch = sweep_bytes / sweep_n
     avg_s = (sweep_ms / sweep_n) / 1e3
-    achieved = bytes_per_launch / avg_s / 1e9
+    achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
     peak, peak_src = _peaks()
 
     # e2e: public drop-in call with host buffers (pinned numpy in, numpy out)
@@ -497,8 +501,12 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                    "l2": f"inputs larger than L2 ({n * n * esize / 1e9:.1f} GB residual)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(cfg, n),
-                     "kernel": "dense_sweep_kernel (K3 fused Schur update + row masses)",
+                     "kernel": ("lazy_pass_kernel (K3 delayed-update pass + row masses)"
+                                if lazy_block else
+                                "dense_sweep_kernel (K3 fused Schur update + row masses)"),
                      "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "update": (f"delayed (read R per step, write every {lazy_block} steps)"
+                                if lazy_block else "eager (read + write R per step)"),
                      "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src},
         "step_breakdown_ms": {"sweep_per_pivot": sweep_ms / sweep_n,
                               "select_per_pivot": select_ms / (len(stats) * (pivots_done + 1)),

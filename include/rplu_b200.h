@@ -55,6 +55,9 @@ extern "C" {
 /* flags */
 #define RPLU_FLAG_TIME_KERNELS 1 /* bracket K2/K3 launches with CUDA events */
 #define RPLU_FLAG_NO_GRAPH 2     /* never capture the step loop into a CUDA graph */
+#define RPLU_FLAG_LAZY 4         /* dense: force the delayed-update loop */
+#define RPLU_FLAG_EAGER 8        /* dense: force the eager (update every step) loop;
+                                    default: delayed updates when R exceeds L2 */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0
@@ -108,6 +111,11 @@ typedef struct rplu_dense_out {
   double select_ms;
   int64_t sweep_launches;
   int64_t kernel_launches;
+  /* algorithmic HBM bytes of the timed update launches (2*n*m*s for an eager
+   * update or a lazy flush, n*m*s for a lazy read-only pass), and the
+   * delayed-update flush interval used (0 = eager loop) */
+  double sweep_bytes;
+  int64_t lazy_block;
 } rplu_dense_out;
 
 int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* out);

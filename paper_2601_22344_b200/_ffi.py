@@ -32,6 +32,8 @@ RULE_IDS = {"rplu": 0, "c2plu": 1, "cplu": 2}
 
 FLAG_TIME_KERNELS = 1
 FLAG_NO_GRAPH = 2
+FLAG_LAZY = 4
+FLAG_EAGER = 8
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -58,7 +60,7 @@ class DenseOut(ctypes.Structure):
         ("clean_early_stop", c_i32), ("tol_stop", c_i32),
         ("zero_pivot_i", c_i64), ("zero_pivot_j", c_i64),
         ("sweep_ms", c_dbl), ("select_ms", c_dbl), ("sweep_launches", c_i64),
-        ("kernel_launches", c_i64),
+        ("kernel_launches", c_i64), ("sweep_bytes", c_dbl), ("lazy_block", c_i64),
     ]
 
 

@@ -44,6 +44,11 @@ struct DenseParams {
   long long* pivots;
   double stop_tol;
   int rule;
+  // delayed-update (lazy) mode: R holds the residual R^(t0) of the last
+  // flush; steps t0..t-1 are applied on the fly from Lt / U
+  long long t0;
+  int lazy;
+  int force;  // run the pass even after a stop (final flush)
 };
 
 template <typename T, int VEC>
@@ -265,6 +270,24 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
   long long near = 0;
   long long i = 0, j = 0;
   T a = S::zero();
+  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+  // The pivot row of the current residual.  Lazy mode reconstructs it into
+  // U[t,:] as R^(t0)[i,:] minus the pending rank-1 terms, applied in step
+  // order with one rounding per product and per subtraction -- the exact
+  // operation sequence of the eager update, so the bits are identical.
+  auto pivot_row = [&](long long ii) -> const T* {
+    if (!p.lazy) return R + ii * ld;
+    const T* Lt = reinterpret_cast<const T*>(p.Lt);
+    const T* U = reinterpret_cast<const T*>(p.U);
+    for (long long k = threadIdx.x; k < m; k += B) {
+      T x = R[ii * ld + k];
+      for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + ii], U[s * p.ldu + k]);
+      urow[k] = x;
+    }
+    __syncthreads();
+    return urow;
+  };
+  const T* row = nullptr;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (p.rule == RPLU_RULE_RPLU) {
       if (uc + 2 > p.n_uniforms) {
@@ -280,9 +303,9 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
         double tol = kNearBoundaryRel * total, tg = u1 * total;
         if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
       }
-      const T* row = R + i * ld;
-      auto wcol = [&](long long k) { return S::weight(row[k]); };
       __syncthreads();
+      row = pivot_row(i);
+      auto wcol = [&](long long k) { return S::weight(row[k]); };
       Cdf<B> cc = cdf_build<B>(wcol, m, sm);
       j = cdf_find<B>(wcol, m, cc, u2, sm);
       if (threadIdx.x == 0) {
@@ -291,16 +314,17 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
       }
     } else if (p.rule == RPLU_RULE_C2PLU) {
       i = block_argmax<B>(wrow, n, nullptr);
-      const T* row = R + i * ld;
+      row = pivot_row(i);
       auto wabs = [&](long long k) { return S::absval(row[k]); };
       j = block_argmax<B>(wabs, m, nullptr);
-    } else {  // CPLU: flat argmax of |R| from the per-row maxima
+    } else {  // CPLU (eager only): flat argmax of |R| from the per-row maxima
       const double* rm = p.rowmax;
       auto wmax = [&](long long k) { return rm[k]; };
       i = block_argmax<B>(wmax, n, nullptr);
       j = p.rowarg[i];
+      row = R + i * ld;
     }
-    a = R[i * ld + j];
+    a = row[j];
     if (!S::is_zero(a)) break;
     if (attempt == 1 || p.rule != RPLU_RULE_RPLU) {
       if (threadIdx.x == 0) {
@@ -315,10 +339,10 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
     }
     __syncthreads();
   }
-  // U[t,:] = R[i,:] (the pre-update pivot row; K3 reads it from here)
-  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
-  const T* row = R + i * ld;
-  for (long long k = threadIdx.x; k < m; k += B) urow[k] = row[k];
+  // U[t,:] = R[i,:] (the pre-update pivot row; K3 reads it from here; the
+  // lazy path already reconstructed it in place)
+  if (!p.lazy)
+    for (long long k = threadIdx.x; k < m; k += B) urow[k] = row[k];
   if (threadIdx.x == 0) {
     st->ucount = uc;
     st->near_boundary += near;
@@ -328,6 +352,110 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
     p.pivots[2 * t] = i;
     p.pivots[2 * t + 1] = j;
     st->done = t + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Delayed-update (lazy) dense loop.  Between flushes R keeps R^(t0); each
+// step reads R once (no write) and applies the pending rank-1 terms
+// s = t0..t on the fly, in step order with the eager kernel's rounding, to
+// get the masses of R^(t+1); every `block` steps the same pass writes
+// R^(t+1) back (flush).  HBM traffic per step: n*m*s read (+ n*m*s write
+// every block steps) instead of 2*n*m*s, at the cost of 2q FP ops per
+// element (q = pending terms); the residual, L and U stay bit-identical to
+// the eager path.
+constexpr int kLazyMaxBlock = 16;
+
+// L[:,t] = R^(t)[:,j] / a, the pivot column reconstructed on the fly.
+template <typename T>
+__global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  if (!p.st->active) return;
+  const long long n = p.n, j = p.st->pj, t = p.t;
+  const T* R = reinterpret_cast<const T*>(p.R);
+  T* Lt = reinterpret_cast<T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U);
+  const typename S::coef_t cf = load_coef<T>(p.st);
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    T x = R[k * p.ld + j];
+    for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + k], U[s * p.ldu + j]);
+    Lt[t * n + k] = S::scale(x, cf);
+  }
+}
+
+// Masses of R^(t+1) = R^(t0) - sum_{s=t0..t} L_s U_s (and, FLUSH, write it).
+// One CTA owns RB rows; its pending L values sit in shared memory, the
+// pending U rows are read per column chunk (L2-resident: q rows of m).
+template <typename T, int VEC, int RB, bool FLUSH>
+__global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  constexpr int NT = 256;
+  if (!p.force && !p.st->active) return;
+  const long long row0 = (long long)blockIdx.x * RB;
+  const long long n = p.n, m = p.m, ld = p.ld;
+  const int q = (int)(p.t - p.t0 + 1);
+  T* R = reinterpret_cast<T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
+  __shared__ T Ls[kLazyMaxBlock][RB];
+  for (int idx = threadIdx.x; idx < q * RB; idx += NT) {
+    const int s = idx / RB, r = idx % RB;
+    Ls[s][r] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
+  }
+  __syncthreads();
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+  const int nr = (int)min((long long)RB, n - row0);
+  const long long mv = (m / VEC) * VEC;
+  for (long long l = (long long)threadIdx.x * VEC; l < mv; l += (long long)NT * VEC) {
+    VecT<T, VEC> rv[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (r < nr) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (row0 + r) * ld + l);
+    for (int s = 0; s < q; ++s) {
+      const VecT<T, VEC> u = *reinterpret_cast<const VecT<T, VEC>*>(U + s * p.ldu + l);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const T lv = Ls[s][r];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (r < nr) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
+        if (FLUSH) *reinterpret_cast<VecT<T, VEC>*>(R + (row0 + r) * ld + l) = rv[r];
+      }
+    }
+  }
+  for (long long l = mv + threadIdx.x; l < m; l += NT) {  // scalar tail
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (r < nr) {
+        T x = R[(row0 + r) * ld + l];
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][r], U[s * p.ldu + l]);
+        acc[r] += S::mass(x);
+        if (FLUSH) R[(row0 + r) * ld + l] = x;
+      }
+    }
+  }
+  __shared__ double red[NT / 32][RB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    const double s = warp_sum(acc[r]);
+    if (lane == 0) red[w][r] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < RB && (int)threadIdx.x < nr) {
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NT / 32; ++ww) s += red[ww][threadIdx.x];
+    p.masses[row0 + threadIdx.x] = s;
   }
 }
 
@@ -434,6 +562,86 @@ static int dense_loop(const DenseParams& base, cudaStream_t s, LoopTiming& tm, l
   return RPLU_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <typename T, int RB>
+static void launch_lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
+  constexpr int VEC = Scalar<T>::kVec;
+  dim3 grid((unsigned)((p.n + RB - 1) / RB));
+  if (flush) lazy_pass_kernel<T, VEC, RB, true><<<grid, 256, 0, s>>>(p);
+  else lazy_pass_kernel<T, VEC, RB, false><<<grid, 256, 0, s>>>(p);
+}
+
+template <typename T>
+static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
+  static const int rb = env_int("RPLU_LAZY_RB", sizeof(T) == 16 ? 8 : 16);
+  if (rb <= 8) launch_lazy_pass<T, 8>(p, flush, s);
+  else launch_lazy_pass<T, 16>(p, flush, s);
+}
+
+// Default flush interval: where the 2q FP ops per element of the last
+// pending steps start to exceed the read time of the element (fp64 10,
+// fp32 8, complex128 6 on B200), overridable with RPLU_LAZY_BLOCK.
+template <typename T>
+static int lazy_block() {
+  const int dflt = sizeof(T) == 16 ? 6 : (sizeof(T) == 4 ? 8 : 10);
+  int b = env_int("RPLU_LAZY_BLOCK", dflt);
+  return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
+}
+
+template <typename T>
+static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& tm,
+                           long long* launches) {
+  DenseParams p = base;
+  p.lazy = 1;
+  const int block = lazy_block<T>();
+  sweep<T>(p, false, false, s);  // K1: masses of A
+  RPLU_CUDA(cudaGetLastError());
+  long long nl = 1;
+  long long t0 = 0;
+  const int pc_blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
+  for (long long t = 0; t <= p.steps; ++t) {
+    p.t = t;
+    p.t0 = t0;
+    tm.mark(0, s, true);
+    dense_select_kernel<T><<<1, 1024, 0, s>>>(p);
+    tm.mark(0, s, false);
+    ++nl;
+    if (t < p.steps) {
+      lazy_pivcol_kernel<T><<<pc_blocks, 256, 0, s>>>(p);
+      const bool flush = (t - t0 + 1 == block) || (t == p.steps - 1);
+      tm.mark(flush ? 2 : 1, s, true);
+      lazy_pass<T>(p, flush, s);
+      tm.mark(flush ? 2 : 1, s, false);
+      nl += 2;
+      if (flush) t0 = t + 1;
+    }
+  }
+  RPLU_CUDA(cudaGetLastError());
+  *launches = nl;
+  return RPLU_OK;
+}
+
+// After an early stop the residual holds R^(t0) of the last flush; apply
+// the pending steps t0..done-1 (no-op when the loop ran to the end).
+template <typename T>
+static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_t s) {
+  const long long block = lazy_block<T>();
+  const long long t0 = (done / block) * block;
+  if (done <= t0 || done >= base.steps) return RPLU_OK;
+  DenseParams p = base;
+  p.lazy = 1;
+  p.force = 1;
+  p.t = done - 1;
+  p.t0 = t0;
+  lazy_pass<T>(p, true, s);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
 int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
   const long long n = a->n, m = a->m, steps = a->steps;
@@ -488,12 +696,31 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   const bool small = (double)n * (double)m <= 64.0 * 1024 * 1024;
   const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      steps >= 4 && graph_env >= 0 && (small || graph_env > 0);
+  // Residuals that do not fit in L2 take the delayed-update loop (one read
+  // of R per step instead of read + write); RPLU_LAZY=0/1 overrides.
+  const int esize = a->dtype == RPLU_F32 ? 4 : (a->dtype == RPLU_F64 ? 8 : 16);
+  const int vec = 16 / esize;
+  const bool vec_ok = (a->ld % vec == 0) && ((uintptr_t)a->R % 16 == 0) &&
+                      (a->ldu % vec == 0) && ((uintptr_t)a->U % 16 == 0);
+  static const int lazy_env = env_int("RPLU_LAZY", -1);
+  int want = -1;  // -1 auto, 0 eager, 1 lazy
+  if (a->flags & RPLU_FLAG_EAGER) want = 0;
+  else if (a->flags & RPLU_FLAG_LAZY) want = 1;
+  else if (lazy_env >= 0) want = lazy_env;
+  const bool lazy = a->rule != RPLU_RULE_CPLU && vec_ok && steps >= 2 &&
+                    (want == 1 || (want < 0 && (double)n * m * esize > 256.0e6));
   rc = run_maybe_graph(ctx, s, graph, 0, [&](cudaStream_t q) -> int {
     init_state_kernel<<<1, 1, 0, q>>>(st);
     switch (a->dtype) {
-      case RPLU_F64: return dense_loop<double>(p, q, tm, &launches);
-      case RPLU_F32: return dense_loop<float>(p, q, tm, &launches);
-      case RPLU_C128: return dense_loop<double2>(p, q, tm, &launches);
+      case RPLU_F64:
+        return lazy ? dense_loop_lazy<double>(p, q, tm, &launches)
+                    : dense_loop<double>(p, q, tm, &launches);
+      case RPLU_F32:
+        return lazy ? dense_loop_lazy<float>(p, q, tm, &launches)
+                    : dense_loop<float>(p, q, tm, &launches);
+      case RPLU_C128:
+        return lazy ? dense_loop_lazy<double2>(p, q, tm, &launches)
+                    : dense_loop<double2>(p, q, tm, &launches);
     }
     set_error("unknown dtype");
     return RPLU_ERR_ARG;
@@ -504,6 +731,20 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   RPLU_CUDA(cudaMemcpyAsync(&hs, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   RPLU_CUDA(cudaStreamSynchronize(s));
   const long long done = hs.done;
+  if (lazy && done < steps) {
+    switch (a->dtype) {
+      case RPLU_F64: rc = lazy_final_flush<double>(p, done, s); break;
+      case RPLU_F32: rc = lazy_final_flush<float>(p, done, s); break;
+      case RPLU_C128: rc = lazy_final_flush<double2>(p, done, s); break;
+    }
+    if (rc) return rc;
+    RPLU_CUDA(cudaStreamSynchronize(s));
+  }
+  out->lazy_block = lazy ? (a->dtype == RPLU_F64 ? lazy_block<double>()
+                                                 : (a->dtype == RPLU_F32 ? lazy_block<float>()
+                                                                         : lazy_block<double2>()))
+                         : 0;
+  out->sweep_bytes = 0.0;
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,
                          cudaMemcpyDeviceToHost));
@@ -519,8 +760,15 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     for (size_t q = 0; q < tm.kind.size(); ++q) {
       float ms = 0.f;
       RPLU_CUDA(cudaEventElapsedTime(&ms, tm.ev[2 * q], tm.ev[2 * q + 1]));
-      if (tm.kind[q] == 1) {
-        if ((long long)out->sweep_launches < done) { out->sweep_ms += ms; out->sweep_launches++; }
+      if (tm.kind[q] >= 1) {
+        // algorithmic bytes: eager update and lazy flush read + write R,
+        // a lazy pass reads it
+        const double pass_bytes = (double)n * m * esize * ((lazy && tm.kind[q] == 1) ? 1 : 2);
+        if ((long long)out->sweep_launches < done) {
+          out->sweep_ms += ms;
+          out->sweep_launches++;
+          out->sweep_bytes += pass_bytes;
+        }
       } else {
         out->select_ms += ms;
       }

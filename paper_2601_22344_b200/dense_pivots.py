@@ -103,7 +103,7 @@ def _input_tensor(A, compute_dtype):
 
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
-              return_device=None, time_kernels=False):
+              return_device=None, time_kernels=False, update="auto"):
     """Run pivoted elimination for up to ``steps`` pivots (dense_pivots.py:129).
 
     Stops early, with a flag, when the residual Frobenius norm falls to
@@ -116,8 +116,13 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     CUDA input tensor as the residual buffer instead of copying it), and
     ``return_device`` (keep L/U/residual as CUDA tensors; default: True iff
     the input was a CUDA tensor), ``time_kernels`` (bracket the K2/K3 launches
-    with CUDA events; results in ``trace.kernel_stats``).
+    with CUDA events; results in ``trace.kernel_stats``), ``update``
+    ("auto" | "eager" | "lazy": update the residual every step, or apply the
+    pending rank-1 terms on the fly and write R every few steps — same bits,
+    half the HBM traffic; "auto" = lazy when R does not fit in L2).
     """
+    if update not in ("auto", "eager", "lazy"):
+        raise ValueError(f"unknown update mode {update!r}")
     if isinstance(rule, str):
         rule = PivotRule(rule)
     if rule.tag not in _DEVICE_RULES:
@@ -157,7 +162,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         uniforms=block.pointer() if block else None,
         n_uniforms=block.values.size if block else 0,
         stream=torch.cuda.current_stream(dev).cuda_stream,
-        flags=_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
+        flags=((_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
+               | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]))
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)
@@ -182,6 +188,7 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         tol_stop=bool(out.tol_stop), near_boundary_draws=int(out.near_boundary_draws),
         uniforms_consumed=int(out.uniforms_consumed), host=not return_device)
     trace.kernel_stats = {"sweep_ms": out.sweep_ms, "select_ms": out.select_ms,
+                          "sweep_bytes": out.sweep_bytes, "lazy_block": int(out.lazy_block),
                           "sweep_launches": int(out.sweep_launches),
                           "kernel_launches": int(out.kernel_launches)}
     return trace

@@ -53,4 +53,4 @@ def test_library_is_sm100a():
 def test_struct_layouts_match_header():
     # rplu_dense_args: 2 int32 + 4 int64 + double + 3 ptr + int64 + ptr + int64 + ptr
     assert ctypes.sizeof(_ffi.DenseArgs) == 8 + 8 * 4 + 8 + 8 * 3 + 8 + 8 + 8 + 8 + 8
-    assert ctypes.sizeof(_ffi.DenseOut) == 8 * 2 + 8 * 3 + 4 * 2 + 8 * 2 + 8 * 4
+    assert ctypes.sizeof(_ffi.DenseOut) == 8 * 2 + 8 * 3 + 4 * 2 + 8 * 2 + 8 * 4 + 8 * 2

@@ -210,6 +210,53 @@ def test_device_tensor_inputs_stay_on_device(cuda_device):
     assert float(err) <= 1e-13
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.complex128])
+@pytest.mark.parametrize("n,m,steps", [(700, 530, 97), (257, 1024, 40)])
+def test_lazy_update_is_bit_identical(dtype, n, m, steps, cuda_device):
+    """Delayed updates (R read per step, written every few steps) reproduce
+    the eager path's residual, L, U and pivots bit for bit."""
+    rs = np.random.default_rng(n + m)
+    A = rs.standard_normal((n, m)) @ np.diag(0.97 ** np.arange(m))
+    if dtype == torch.complex128:
+        A = A + 1j * rs.standard_normal((n, m)) @ np.diag(0.97 ** np.arange(m))
+    At = torch.from_numpy(A).to("cuda", dtype)
+    e = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(3)), steps, update="eager")
+    z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(3)), steps, update="lazy",
+                     time_kernels=True)
+    assert z.kernel_stats["lazy_block"] > 0 and e.kernel_stats["lazy_block"] == 0
+    assert z.pivots == e.pivots
+    assert torch.equal(z.L, e.L) and torch.equal(z.U, e.U)
+    assert torch.equal(z.residual, e.residual)
+    np.testing.assert_array_equal(z.resid_fro, e.resid_fro)
+
+
+@pytest.mark.parametrize("rule", ["rplu", "c2plu"])
+def test_lazy_early_stops_flush_the_residual(rule, cuda_device):
+    A = torch.from_numpy(gen.c1_dense(2, n=600, m=512)).cuda()
+    mk = (lambda: rp.PivotRule("rplu", rp.RngState(2))) if rule == "rplu" else (lambda: "c2plu")
+    e = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="eager")
+    z = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="lazy")
+    assert e.tol_stop and z.tol_stop and z.steps == e.steps
+    assert torch.equal(z.residual, e.residual) and torch.equal(z.L, e.L)
+    # clean stop on an exactly low-rank matrix
+    B = torch.from_numpy(np.diag(np.arange(1.0, 31.0))).cuda()
+    e = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30, update="eager")
+    z = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30, update="lazy")
+    assert z.pivots == e.pivots and torch.equal(z.residual, e.residual)
+
+
+def test_lazy_matches_oracle_c3_reduced(cuda_device):
+    A = gen.c3_dense_host(1, n=4096)
+    ref = oracle.eliminate_real(A, "rplu", 128, seed=1, margins=True)
+    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 128, update="lazy")
+    mism = [t for t, (a, b) in enumerate(zip(tr.pivots, ref["pivots"])) if a != b]
+    if mism:
+        assert ref["margins"][mism[0]] <= oracle.NEAR_REL
+    else:
+        np.testing.assert_array_equal(tr.L, ref["L"])
+        np.testing.assert_array_equal(tr.U, ref["U"])
+
+
 @pytest.mark.slow
 def test_c3_full_size_properties(cuda_device):
     """Full C3 (32768^2 fp64, r=512): size-independent identities.
