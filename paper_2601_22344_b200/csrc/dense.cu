@@ -51,6 +51,8 @@ struct DenseParams {
   int force;  // run the pass even after a stop (final flush)
 };
 
+constexpr int kLazyMaxBlock = 12;  // longest delayed-update block
+
 template <typename T, int VEC>
 struct alignas(sizeof(T) * VEC) VecT {
   T v[VEC];
@@ -275,13 +277,25 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
   // U[t,:] as R^(t0)[i,:] minus the pending rank-1 terms, applied in step
   // order with one rounding per product and per subtraction -- the exact
   // operation sequence of the eager update, so the bits are identical.
+  __shared__ T s_lpiv[kLazyMaxBlock];
   auto pivot_row = [&](long long ii) -> const T* {
     if (!p.lazy) return R + ii * ld;
     const T* Lt = reinterpret_cast<const T*>(p.Lt);
-    const T* U = reinterpret_cast<const T*>(p.U);
+    const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
+    const int q = (int)(t - p.t0);
+    if ((int)threadIdx.x < q) s_lpiv[threadIdx.x] = Lt[(p.t0 + threadIdx.x) * n + ii];
+    __syncthreads();
     for (long long k = threadIdx.x; k < m; k += B) {
       T x = R[ii * ld + k];
-      for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + ii], U[s * p.ldu + k]);
+      for (int s0 = 0; s0 < q; s0 += 4) {  // 4 pending U loads in flight at a time
+        T uu[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + u < q) uu[u] = U[(s0 + u) * p.ldu + k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + u < q) x = S::sub_outer(x, s_lpiv[s0 + u], uu[u]);
+      }
       urow[k] = x;
     }
     __syncthreads();
@@ -364,7 +378,6 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
 // every block steps) instead of 2*n*m*s, at the cost of 2q FP ops per
 // element (q = pending terms); the residual, L and U stay bit-identical to
 // the eager path.
-constexpr int kLazyMaxBlock = 16;
 
 // L[:,t] = R^(t)[:,j] / a, the pivot column reconstructed on the fly.
 template <typename T>
@@ -376,10 +389,20 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
   T* Lt = reinterpret_cast<T*>(p.Lt);
   const T* U = reinterpret_cast<const T*>(p.U);
   const typename S::coef_t cf = load_coef<T>(p.st);
+  const int q = (int)(t - p.t0);
+  __shared__ T s_upiv[kLazyMaxBlock];  // U[s][j] of the pending steps
+  if ((int)threadIdx.x < q) s_upiv[threadIdx.x] = U[(p.t0 + threadIdx.x) * p.ldu + j];
+  __syncthreads();
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x) {
     T x = R[k * p.ld + j];
-    for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + k], U[s * p.ldu + j]);
+    T ll[kLazyMaxBlock];
+#pragma unroll
+    for (int s = 0; s < kLazyMaxBlock; ++s)
+      if (s < q) ll[s] = Lt[(p.t0 + s) * n + k];
+#pragma unroll
+    for (int s = 0; s < kLazyMaxBlock; ++s)
+      if (s < q) x = S::sub_outer(x, ll[s], s_upiv[s]);
     Lt[t * n + k] = S::scale(x, cf);
   }
 }
@@ -456,6 +479,94 @@ __global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
 #pragma unroll
     for (int ww = 0; ww < NT / 32; ++ww) s += red[ww][threadIdx.x];
     p.masses[row0 + threadIdx.x] = s;
+  }
+}
+
+// Same pass with a 2-D CTA: 64 threads across a column chunk of 64*VEC
+// columns x 4 row groups of RPT rows (32 rows per CTA).  The pending U rows
+// of the chunk are staged once in shared memory and reused by all 32 rows
+// (L2 traffic for U = q/32 of the R stream), so each thread only holds its
+// RPT x VEC residual values in registers and 4 CTAs fit per SM.
+template <typename T, int VEC, int RPT, bool FLUSH>
+__global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  constexpr int NT = 256, TX = 64, TY = NT / TX, ROWS = TY * RPT, CW = TX * VEC;
+  if (!p.force && !p.st->active) return;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const long long row0 = (long long)blockIdx.x * ROWS;
+  const long long n = p.n, m = p.m, ld = p.ld;
+  const int q = (int)(p.t - p.t0 + 1);
+  T* R = reinterpret_cast<T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
+  __shared__ VecT<T, VEC> Us[kLazyMaxBlock][TX];
+  __shared__ T Ls[kLazyMaxBlock][ROWS];
+  for (int idx = threadIdx.x; idx < q * ROWS; idx += NT) {
+    const int s = idx / ROWS, r = idx % ROWS;
+    Ls[s][r] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
+  }
+  const long long myrow0 = row0 + ty * RPT;
+  const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
+  double acc[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+  const long long mv = (m / VEC) * VEC;
+  for (long long l0 = 0; l0 < mv; l0 += CW) {
+    const long long l = l0 + (long long)tx * VEC;
+    const bool inb = l < mv;
+    __syncthreads();  // previous chunk's Us reads are done
+    for (int idx = threadIdx.x; idx < q * TX; idx += NT) {
+      const int s = idx / TX, v = idx % TX;
+      const long long lc = l0 + (long long)v * VEC;
+      if (lc < mv) Us[s][v] = *reinterpret_cast<const VecT<T, VEC>*>(U + s * p.ldu + lc);
+    }
+    VecT<T, VEC> rv[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      if (inb && r < nr) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (myrow0 + r) * ld + l);
+    __syncthreads();
+    if (inb) {
+      for (int s = 0; s < q; ++s) {
+        const VecT<T, VEC> u = Us[s][tx];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const T lv = Ls[s][ty * RPT + r];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        if (r < nr) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
+          if (FLUSH) *reinterpret_cast<VecT<T, VEC>*>(R + (myrow0 + r) * ld + l) = rv[r];
+        }
+      }
+    }
+  }
+  for (long long l = mv + tx; l < m; l += TX) {  // scalar tail (m % VEC columns)
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      if (r < nr) {
+        T x = R[(myrow0 + r) * ld + l];
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        acc[r] += S::mass(x);
+        if (FLUSH) R[(myrow0 + r) * ld + l] = x;
+      }
+    }
+  }
+  __shared__ double red[NT / 32][RPT];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const double sm = warp_sum(acc[r]);
+    if (lane == 0) red[w][r] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x < ROWS) {
+    const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;  // row group g = warps 2g, 2g+1
+    if (row0 + threadIdx.x < n) p.masses[row0 + threadIdx.x] = red[2 * g][r] + red[2 * g + 1][r];
   }
 }
 
@@ -575,11 +686,26 @@ static void launch_lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   else lazy_pass_kernel<T, VEC, RB, false><<<grid, 256, 0, s>>>(p);
 }
 
+template <typename T, int RPT>
+static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) {
+  constexpr int VEC = Scalar<T>::kVec;
+  constexpr int ROWS = 4 * RPT;
+  dim3 grid((unsigned)((p.n + ROWS - 1) / ROWS));
+  if (flush) lazy_pass2_kernel<T, VEC, RPT, true><<<grid, 256, 0, s>>>(p);
+  else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
+}
+
 template <typename T>
 static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
-  static const int rb = env_int("RPLU_LAZY_RB", sizeof(T) == 16 ? 8 : 16);
-  if (rb <= 8) launch_lazy_pass<T, 8>(p, flush, s);
-  else launch_lazy_pass<T, 16>(p, flush, s);
+  // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA)
+  static const int kernel = env_int("RPLU_LAZY_KERNEL", 2);
+  if (kernel == 1) {
+    static const int rb = env_int("RPLU_LAZY_RB", sizeof(T) == 16 ? 8 : 16);
+    if (rb <= 8) launch_lazy_pass<T, 8>(p, flush, s);
+    else launch_lazy_pass<T, 16>(p, flush, s);
+    return;
+  }
+  launch_lazy_pass2<T, sizeof(T) == 16 ? 4 : 8>(p, flush, s);
 }
 
 // Default flush interval: where the 2q FP ops per element of the last
