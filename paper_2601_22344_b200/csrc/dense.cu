@@ -273,34 +273,9 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
   long long i = 0, j = 0;
   T a = S::zero();
   T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
-  // The pivot row of the current residual.  Lazy mode reconstructs it into
-  // U[t,:] as R^(t0)[i,:] minus the pending rank-1 terms, applied in step
-  // order with one rounding per product and per subtraction -- the exact
-  // operation sequence of the eager update, so the bits are identical.
-  __shared__ T s_lpiv[kLazyMaxBlock];
-  auto pivot_row = [&](long long ii) -> const T* {
-    if (!p.lazy) return R + ii * ld;
-    const T* Lt = reinterpret_cast<const T*>(p.Lt);
-    const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
-    const int q = (int)(t - p.t0);
-    if ((int)threadIdx.x < q) s_lpiv[threadIdx.x] = Lt[(p.t0 + threadIdx.x) * n + ii];
-    __syncthreads();
-    for (long long k = threadIdx.x; k < m; k += B) {
-      T x = R[ii * ld + k];
-      for (int s0 = 0; s0 < q; s0 += 4) {  // 4 pending U loads in flight at a time
-        T uu[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (s0 + u < q) uu[u] = U[(s0 + u) * p.ldu + k];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (s0 + u < q) x = S::sub_outer(x, s_lpiv[s0 + u], uu[u]);
-      }
-      urow[k] = x;
-    }
-    __syncthreads();
-    return urow;
-  };
+  // (eager loop: the residual in R is current; the lazy loop uses
+  // lazy_select_row / lazy_row / lazy_select_col instead)
+  auto pivot_row = [&](long long ii) -> const T* { return R + ii * ld; };
   const T* row = nullptr;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (p.rule == RPLU_RULE_RPLU) {
@@ -353,10 +328,164 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
     }
     __syncthreads();
   }
-  // U[t,:] = R[i,:] (the pre-update pivot row; K3 reads it from here; the
-  // lazy path already reconstructed it in place)
-  if (!p.lazy)
-    for (long long k = threadIdx.x; k < m; k += B) urow[k] = row[k];
+  // U[t,:] = R[i,:] (the pre-update pivot row; K3 reads it from here)
+  for (long long k = threadIdx.x; k < m; k += B) urow[k] = row[k];
+  if (threadIdx.x == 0) {
+    st->ucount = uc;
+    st->near_boundary += near;
+    st->pi = i;
+    st->pj = j;
+    store_coef<T>(st, a);
+    p.pivots[2 * t] = i;
+    p.pivots[2 * t + 1] = j;
+    st->done = t + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Lazy-mode select, split in three launches so the pivot-row reconstruction
+// (m elements x q pending terms) runs on the whole GPU instead of one CTA:
+//   row select (1 CTA): residual norm, stop rules, row draw (u1)
+//   row rebuild (grid): U[t,:] = R^(t0)[i,:] - pending terms
+//   column select (1 CTA): column draw (u2) over U[t,:], zero-pivot resample
+
+template <typename T>
+__global__ void __launch_bounds__(1024) lazy_select_row_kernel(DenseParams p) {
+  constexpr int B = 1024;
+  DevState* st = p.st;
+  if (!st->active) return;
+  __shared__ CdfSmem<B> sm;
+  __shared__ int s_stop;
+  const long long n = p.n, t = p.t;
+  const double* masses = p.masses;
+  auto wrow = [&](long long k) { return masses[k]; };
+  Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+  const double total = cr.total;
+  const double resid = sqrt(total);
+  if (threadIdx.x == 0) {
+    p.resid[t] = resid;
+    if (t == 0) st->fro0 = resid;
+    const double fro0 = (t == 0) ? resid : st->fro0;
+    int stop = 0;
+    if (t > 0 && p.stop_tol > 0.0 && resid <= p.stop_tol * fro0) {
+      st->status = kTolStop;
+      stop = 1;
+    } else if (t >= p.steps) {
+      stop = 1;
+    } else if (resid == 0.0) {
+      st->status = kCleanStop;
+      stop = 1;
+    } else if (p.rule == RPLU_RULE_RPLU && st->ucount + 2 > p.n_uniforms) {
+      st->status = kUniformsExhausted;
+      stop = 1;
+    }
+    if (stop) st->active = 0;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) return;
+  long long i;
+  if (p.rule == RPLU_RULE_RPLU) {
+    const double u1 = p.uniforms[st->ucount];
+    i = cdf_find<B>(wrow, n, cr, u1, sm);
+    if (threadIdx.x == 0) {
+      const double tol = kNearBoundaryRel * total, tg = u1 * total;
+      if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) st->near_boundary++;
+      st->ucount += 1;
+    }
+  } else {
+    i = block_argmax<B>(wrow, n, nullptr);
+  }
+  if (threadIdx.x == 0) st->pi = i;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) lazy_row_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  if (!p.st->active) return;
+  const long long i = p.st->pi, t = p.t, n = p.n;
+  const int q = (int)(t - p.t0);
+  const T* R = reinterpret_cast<const T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
+  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+  __shared__ T s_l[kLazyMaxBlock];
+  if ((int)threadIdx.x < q) s_l[threadIdx.x] = Lt[(p.t0 + threadIdx.x) * n + i];
+  __syncthreads();
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
+       k += (long long)gridDim.x * blockDim.x) {
+    T x = R[i * p.ld + k];
+    for (int s = 0; s < q; ++s) x = S::sub_outer(x, s_l[s], U[s * p.ldu + k]);
+    urow[k] = x;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) lazy_select_col_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  constexpr int B = 1024;
+  DevState* st = p.st;
+  if (!st->active) return;
+  __shared__ CdfSmem<B> sm;
+  const long long n = p.n, m = p.m, t = p.t;
+  T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+  const T* R = reinterpret_cast<const T*>(p.R);
+  long long uc = st->ucount;
+  long long near = 0;
+  long long i = st->pi, j = 0;
+  T a = S::zero();
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      // zero pivot (probability-zero event): resample the row with the next
+      // uniform and rebuild its residual row inside this CTA
+      const double* masses = p.masses;
+      auto wrow = [&](long long k) { return masses[k]; };
+      __syncthreads();
+      Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+      if (uc + 2 > p.n_uniforms) {
+        if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
+        return;
+      }
+      const double u1 = p.uniforms[uc];
+      uc += 1;
+      i = cdf_find<B>(wrow, n, cr, u1, sm);
+      const T* Lt = reinterpret_cast<const T*>(p.Lt);
+      const T* U = reinterpret_cast<const T*>(p.U);
+      for (long long k = threadIdx.x; k < m; k += B) {
+        T x = R[i * p.ld + k];
+        for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + i], U[s * p.ldu + k]);
+        urow[k] = x;
+      }
+      __syncthreads();
+    }
+    if (p.rule == RPLU_RULE_RPLU) {
+      const double u2 = p.uniforms[uc];
+      uc += 1;
+      auto wcol = [&](long long k) { return S::weight(urow[k]); };
+      Cdf<B> cc = cdf_build<B>(wcol, m, sm);
+      j = cdf_find<B>(wcol, m, cc, u2, sm);
+      if (threadIdx.x == 0) {
+        const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+        if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+      }
+    } else {
+      auto wabs = [&](long long k) { return S::absval(urow[k]); };
+      j = block_argmax<B>(wabs, m, nullptr);
+    }
+    a = urow[j];
+    if (!S::is_zero(a)) break;
+    if (attempt == 1 || p.rule != RPLU_RULE_RPLU) {
+      if (threadIdx.x == 0) {
+        st->status = kZeroPivot;
+        st->active = 0;
+        st->err_i = i;
+        st->err_j = j;
+        st->ucount = uc;
+        st->near_boundary += near;
+      }
+      return;
+    }
+  }
   if (threadIdx.x == 0) {
     st->ucount = uc;
     st->near_boundary += near;
@@ -570,6 +699,132 @@ __global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
   }
 }
 
+// Pipelined version: the next column chunk of the CTA's residual rows and of
+// the pending U rows is copied global->shared with cp.async (LDGSTS) while
+// the current chunk is computed, so the HBM stream and the 2q FP operations
+// per element overlap.  Each thread reads back only the residual elements it
+// copied itself; the U chunk is shared by the CTA's rows.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <typename T, int VEC, int RPT>
+struct LazyPipeSmem {
+  static constexpr int TX = 64, TY = 4, ROWS = TY * RPT;
+  VecT<T, VEC> Rs[2][ROWS][TX];
+  VecT<T, VEC> Us[2][kLazyMaxBlock][TX];
+  T Ls[kLazyMaxBlock][ROWS];
+  double red[8][RPT];
+};
+
+template <typename T, int VEC, int RPT, bool FLUSH>
+__global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
+  using S = Scalar<T>;
+  using SM = LazyPipeSmem<T, VEC, RPT>;
+  constexpr int NT = 256, TX = SM::TX, ROWS = SM::ROWS, CW = TX * VEC;
+  static_assert(sizeof(VecT<T, VEC>) == 16, "16-byte vectors");
+  if (!p.force && !p.st->active) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const long long row0 = (long long)blockIdx.x * ROWS;
+  const long long n = p.n, m = p.m, ld = p.ld;
+  const int q = (int)(p.t - p.t0 + 1);
+  T* R = reinterpret_cast<T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
+  for (int idx = threadIdx.x; idx < q * ROWS; idx += NT) {
+    const int s = idx / ROWS, r = idx % ROWS;
+    sm.Ls[s][r] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
+  }
+  const long long myrow0 = row0 + ty * RPT;
+  const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
+  const long long mv = (m / VEC) * VEC;
+  const long long nchunks = (mv + CW - 1) / CW;
+
+  auto issue = [&](long long c, int buf) {
+    const long long l = c * CW + (long long)tx * VEC;
+    if (l < mv) {
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        if (r < nr) cp_async16(&sm.Rs[buf][ty * RPT + r][tx], R + (myrow0 + r) * ld + l);
+    }
+    for (int idx = threadIdx.x; idx < q * TX; idx += NT) {
+      const int s = idx / TX, v = idx % TX;
+      const long long lc = c * CW + (long long)v * VEC;
+      if (lc < mv) cp_async16(&sm.Us[buf][s][v], U + s * p.ldu + lc);
+    }
+    cp_async_commit();
+  };
+
+  double acc[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+  if (nchunks > 0) issue(0, 0);
+  for (long long c = 0; c < nchunks; ++c) {
+    const int buf = (int)(c & 1);
+    __syncthreads();  // every thread is done reading buffer buf^1 (chunk c-1)
+    if (c + 1 < nchunks) {
+      issue(c + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // chunk c (R rows and the shared U chunk) has landed
+    const long long l = c * CW + (long long)tx * VEC;
+    if (l < mv) {
+      VecT<T, VEC> rv[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) rv[r] = sm.Rs[buf][ty * RPT + r][tx];
+      for (int s = 0; s < q; ++s) {
+        const VecT<T, VEC> u = sm.Us[buf][s][tx];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const T lv = sm.Ls[s][ty * RPT + r];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        if (r < nr) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
+          if (FLUSH) *reinterpret_cast<VecT<T, VEC>*>(R + (myrow0 + r) * ld + l) = rv[r];
+        }
+      }
+    }
+  }
+  for (long long l = mv + tx; l < m; l += TX) {  // scalar tail (m % VEC columns)
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      if (r < nr) {
+        T x = R[(myrow0 + r) * ld + l];
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        acc[r] += S::mass(x);
+        if (FLUSH) R[(myrow0 + r) * ld + l] = x;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const double sv = warp_sum(acc[r]);
+    if (lane == 0) sm.red[w][r] = sv;
+  }
+  __syncthreads();
+  if (threadIdx.x < ROWS) {
+    const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
+    if (row0 + threadIdx.x < n) p.masses[row0 + threadIdx.x] = sm.red[2 * g][r] + sm.red[2 * g + 1][r];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host-side launchers
 
@@ -695,10 +950,36 @@ static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) 
   else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
 }
 
+template <typename T, int RPT>
+static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
+  constexpr int VEC = Scalar<T>::kVec;
+  using SM = LazyPipeSmem<T, VEC, RPT>;
+  const int smem = (int)sizeof(SM);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid((unsigned)((p.n + SM::ROWS - 1) / SM::ROWS));
+  if (flush) lazy_pass3_kernel<T, VEC, RPT, true><<<grid, 256, smem, s>>>(p);
+  else lazy_pass3_kernel<T, VEC, RPT, false><<<grid, 256, smem, s>>>(p);
+}
+
 template <typename T>
 static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
-  // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA)
-  static const int kernel = env_int("RPLU_LAZY_KERNEL", 2);
+  // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA);
+  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D
+  static const int kernel = env_int("RPLU_LAZY_KERNEL", 3);
+  if (kernel == 3) {
+    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 4);
+    if (rpt >= 8) launch_lazy_pass3<T, 8>(p, flush, s);
+    else if (rpt >= 4) launch_lazy_pass3<T, 4>(p, flush, s);
+    else launch_lazy_pass3<T, 2>(p, flush, s);
+    return;
+  }
   if (kernel == 1) {
     static const int rb = env_int("RPLU_LAZY_RB", sizeof(T) == 16 ? 8 : 16);
     if (rb <= 8) launch_lazy_pass<T, 8>(p, flush, s);
@@ -729,11 +1010,17 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
   long long nl = 1;
   long long t0 = 0;
   const int pc_blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
+  const int row_blocks = (int)((p.m + 255) / 256 < 1024 ? (p.m + 255) / 256 : 1024);
   for (long long t = 0; t <= p.steps; ++t) {
     p.t = t;
     p.t0 = t0;
     tm.mark(0, s, true);
-    dense_select_kernel<T><<<1, 1024, 0, s>>>(p);
+    lazy_select_row_kernel<T><<<1, 1024, 0, s>>>(p);
+    if (t < p.steps) {
+      lazy_row_kernel<T><<<row_blocks, 256, 0, s>>>(p);
+      lazy_select_col_kernel<T><<<1, 1024, 0, s>>>(p);
+      nl += 2;
+    }
     tm.mark(0, s, false);
     ++nl;
     if (t < p.steps) {
