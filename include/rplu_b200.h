@@ -217,6 +217,32 @@ typedef struct rplu_cauchy_out {
 
 int rplu_cauchy_run(rplu_ctx* ctx, const rplu_cauchy_args* args, rplu_cauchy_out* out);
 
+/* Certified row-norm upper bounds from a quadtree interaction plan
+ * (treebounds.py:213-242, Alg C.2): exact <= u_i <= nu*exact.  The plan is
+ * built on the host (Alg C.1, paper_2601_22344_b200.treebounds.build_plan)
+ * and flattened into device CSR arrays (int64 / fp64). */
+typedef struct rplu_tree_plan {
+  int64_t n, m;            /* target / source point counts */
+  int32_t p;               /* displacement rank */
+  int32_t reserved;
+  int64_t n_tleaves;       /* target leaves */
+  const int64_t* tperm;    /* [n] target points grouped by leaf */
+  const int64_t* tstart;   /* [n_tleaves+1] */
+  const int64_t* agg_start;  /* [n_tleaves+1] aggregated list per leaf */
+  const int64_t* agg_node;   /* source node of each aggregated entry */
+  const double* agg_alpha;   /* 1 / d_min^2(node, leaf) */
+  const int64_t* ex_start;   /* [n_tleaves+1] exact list per leaf */
+  const int64_t* ex_leaf;    /* source leaf index of each exact entry */
+  int64_t n_snodes, n_sleaves;
+  const int64_t* spts;     /* [m] source points grouped by source leaf */
+  const int64_t* sstart;   /* [n_sleaves+1] */
+  const int64_t* bstart;   /* [n_snodes+1] source leaves below each node */
+  const int64_t* bleaf;
+} rplu_tree_plan;
+
+int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
+                     const void* G, const void* Bt, double* u, void* stream);
+
 /* exact_row_norms (cauchy.py:129-137): u_i = sum_j |G_i.B_:,j / (x_i-y_j)|^2
  * into the device array `out` (n doubles). */
 int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,

@@ -19,6 +19,8 @@ from .lowmem_cur import (CurBuildInfo, CurFactorization, core_extend, cur_build,
                          residual_row)
 from .operators import GaussianKernelOperator
 from .rng import RngState, sample_index
+from .treebounds import (CoincidentPointsError, InteractionPlan, PointQuadtree, build_plan,
+                         certified_upper_bounds)
 
 __all__ = [
     "CallableOperator", "CapabilityError", "DenseMatrix", "MatrixAccessor", "materialize",
@@ -28,4 +30,6 @@ __all__ = [
     "CurBuildInfo", "CurFactorization", "core_extend", "cur_build", "residual_column",
     "residual_row", "GaussianKernelOperator",
     "RngState", "sample_index",
+    "CoincidentPointsError", "InteractionPlan", "PointQuadtree", "build_plan",
+    "certified_upper_bounds",
 ]

@@ -97,6 +97,16 @@ class ShardArgs(ctypes.Structure):
     ]
 
 
+class TreePlan(ctypes.Structure):
+    _fields_ = [
+        ("n", c_i64), ("m", c_i64), ("p", c_i32), ("reserved", c_i32), ("n_tleaves", c_i64),
+        ("tperm", c_vp), ("tstart", c_vp), ("agg_start", c_vp), ("agg_node", c_vp),
+        ("agg_alpha", c_vp), ("ex_start", c_vp), ("ex_leaf", c_vp),
+        ("n_snodes", c_i64), ("n_sleaves", c_i64), ("spts", c_vp), ("sstart", c_vp),
+        ("bstart", c_vp), ("bleaf", c_vp),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/rplu_b200.h
 SIGNATURES = {
     "rplu_abi_version": (ctypes.c_int, []),
@@ -112,6 +122,8 @@ SIGNATURES = {
     "rplu_cauchy_row_norms": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                              c_vp, c_vp]),
     "rplu_diag_fp64_peak": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
+    "rplu_tree_bounds": (ctypes.c_int, [c_vp, ctypes.POINTER(TreePlan), c_vp, c_vp, c_vp, c_vp,
+                                        c_vp, c_vp]),
     # Gaussian-kernel operator struct is passed by pointer (operators._GaussOpStruct)
     "rplu_gauss_apply": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(c_dbl),
                                         c_vp]),

@@ -168,6 +168,28 @@ def exact_row_norms_device(M):
     return out
 
 
+def tree_bounds_device(plan, M):
+    """Certified upper bounds of M's squared row norms from a plan (Alg C.2),
+    as a float64 CUDA tensor (``rplu_tree_bounds``)."""
+    from .treebounds import device_plan
+    dp = device_plan(plan, M.device)
+    n, m = M.shape
+    out = torch.empty(n, dtype=torch.float64, device=M.device)
+    s = _ffi.TreePlan(
+        n=n, m=m, p=M.displacement_rank, n_tleaves=dp.n_tleaves,
+        tperm=dp.tperm.data_ptr(), tstart=dp.tstart.data_ptr(),
+        agg_start=dp.agg_start.data_ptr(), agg_node=dp.agg_node.data_ptr(),
+        agg_alpha=dp.agg_alpha.data_ptr(), ex_start=dp.ex_start.data_ptr(),
+        ex_leaf=dp.ex_leaf.data_ptr(), n_snodes=dp.n_snodes, n_sleaves=dp.n_sleaves,
+        spts=dp.spts.data_ptr(), sstart=dp.sstart.data_ptr(), bstart=dp.bstart.data_ptr(),
+        bleaf=dp.bleaf.data_ptr())
+    c = _device.ctx(M.device)
+    _ffi.check(c._lib.rplu_tree_bounds(c.handle, ctypes.byref(s), M.x.data_ptr(), M.y.data_ptr(),
+                                       M.G.data_ptr(), M.Bt.data_ptr(), out.data_ptr(),
+                                       _device.stream_handle(M.device)))
+    return out
+
+
 def generator_schur_update(M, pivot):
     """Eliminate one pivot by updating the generators (cauchy.py:140-154).
 
@@ -222,6 +244,130 @@ class StructuredPivotTrace:
         return (C[:k] / a[:k, None]).T, R[:k]
 
 
+class _UniformCursor:
+    """Uniforms from a pre-drawn block, committed exactly at the end."""
+
+    def __init__(self, rng, cap):
+        self.block = UniformBlock(rng, cap) if rng is not None else None
+        self.used = 0
+
+    def next(self):
+        if self.used >= self.block.values.size:     # extend (rare): keep exactness
+            extra = self.block._gen.random(self.block.values.size)
+            self.block.values = np.concatenate([self.block.values, extra])
+        u = float(self.block.values[self.used])
+        self.used += 1
+        return u
+
+    def commit(self):
+        if self.block is not None:
+            self.block.commit(self.used)
+
+
+def _row_dev(cur, i):
+    return (cur.Bt @ cur.G[i]) / (cur.x[i] - cur.y)
+
+
+def _column_dev(cur, j):
+    return (cur.G @ cur.Bt[j]) / (cur.x - cur.y[j])
+
+
+def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_steps, host_steps):
+    """Alg 3 with certified tree bounds and rejection sampling
+    (cauchy.py:177-277, plan branch).
+
+    Per step: device bounds u (``rplu_tree_bounds``), max/sum, stop rules;
+    rplu: propose i ~ u (one uniform), accept when rho = ||r_i||^2 >= u_i or
+    with probability rho/u_i (one more uniform); after 64*nu proposals fall
+    back to exact norms (K5) with a warning; column j ~ |r|^2; relative
+    zero-pivot guard with one column resample; generator update on the
+    device.  The proposal/acceptance counters match the reference's trace.
+    """
+    import warnings
+
+    from .rng import sample_index
+    tgt, src = plan.target_tree, plan.source_tree
+    if tgt.points.size != M.shape[0] or src.points.size != M.shape[1]:
+        raise ValueError("generator dimensions do not match the plan's points")
+    cur = M.copy()
+    n, m = M.shape
+    cap = int(REJECTION_CAP_FACTOR * max(nu, 1.0))
+    stream = _UniformCursor(rng if rule == "rplu" else None, max(8, (2 * cap + 3) * rank))
+    tr = StructuredPivotTrace(residual=cur)
+    u0_max = None
+    steps_dev = []
+    try:
+        for _ in range(rank):
+            u = tree_bounds_device(plan, cur)
+            umax, usum = float(u.max()), float(u.sum())
+            tr.bound_maxes.append(umax)
+            tr.bound_sums.append(usum)
+            u0_max = umax if u0_max is None else u0_max
+            if umax <= 0.0:
+                tr.degenerate_stop = True
+                break
+            if stop_tol > 0 and umax <= (stop_tol ** 2) * u0_max:
+                tr.tol_stop = True
+                break
+            if rule == "c2plu":
+                i = int(torch.argmax(u))
+                r = _row_dev(cur, i)
+            else:
+                i = r = None
+                for _p in range(cap):
+                    ii = sample_index(u, stream.next())
+                    rr = _row_dev(cur, ii)
+                    rho = float((rr.real ** 2 + rr.imag ** 2).sum())
+                    tr.proposals += 1
+                    ui = float(u[ii])
+                    if rho >= ui or stream.next() <= rho / ui:
+                        tr.acceptances += 1
+                        i, r = ii, rr
+                        break
+                if i is None:
+                    tr.exact_fallbacks += 1
+                    warnings.warn("rejection sampling exceeded its proposal budget; this step "
+                                  "used exact row norms (possible bound violation)",
+                                  stacklevel=3)
+                    i = sample_index(exact_row_norms_device(cur), stream.next())
+                    r = _row_dev(cur, i)
+            ra = r.abs()
+            if rule == "c2plu":
+                j = int(torch.argmax(ra))
+            else:
+                j = sample_index(ra ** 2, stream.next())
+            thr = PIVOT_REL_TOL * float(ra.max())
+            a = r[j]
+            if float(a.abs()) <= thr:
+                if rule == "c2plu":
+                    raise ZeroDivisionError(f"pivot ({i}, {j}) is numerically zero")
+                j = sample_index(ra ** 2, stream.next())
+                a = r[j]
+                if float(a.abs()) <= thr:
+                    raise ZeroDivisionError(
+                        f"pivot ({i}, {j}) is numerically zero after resampling")
+            c = _column_dev(cur, j)
+            gi, bj = cur.G[i].clone(), cur.Bt[j].clone()
+            cur.G -= torch.outer(c / a, gi)
+            cur.Bt -= torch.outer(r / a, bj)
+            tr.row_indices.append(int(i))
+            tr.col_indices.append(int(j))
+            if keep_steps:
+                steps_dev.append((c, r, a))
+    finally:
+        stream.commit()
+    tr.uniforms_consumed = stream.used
+    if keep_steps and steps_dev:
+        C = torch.stack([s[0] for s in steps_dev])
+        R = torch.stack([s[1] for s in steps_dev])
+        A = torch.stack([s[2] for s in steps_dev])
+        tr.steps_device = (C, R, A)
+        if host_steps:
+            Ch, Rh, Ah = C.cpu().numpy(), R.cpu().numpy(), A.cpu().numpy()
+            tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(len(steps_dev))]
+    return tr
+
+
 def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=None,
                          keep_steps=False, *, host_steps=True, time_kernels=False):
     """Pivoted elimination of a Cauchy-like matrix via generator updates
@@ -237,12 +383,14 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
     n, m = M.shape
     if not 0 <= rank <= min(n, m):
         raise ValueError(f"rank {rank} out of range [0, {min(n, m)}]")
-    if plan is not None:
-        raise CapabilityError(
-            "certified-bound rejection sampling (plan) is not on the B200 path yet "
-            "(SURVEY §8(f1)); pass plan=None for exact row norms")
     if not isinstance(M, CauchyLikeMatrix):
         raise CapabilityError("structured_eliminate needs a CauchyLikeMatrix")
+    if plan is not None:
+        from .treebounds import InteractionPlan
+        if not isinstance(plan, InteractionPlan):
+            raise ValueError("plan must be an InteractionPlan (treebounds.build_plan)")
+        return _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_steps,
+                                          host_steps)
     cur = M.copy()
     dev = cur.device
     p = cur.displacement_rank

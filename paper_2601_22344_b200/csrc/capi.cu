@@ -94,6 +94,8 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, lon
                       int* near, cudaStream_t s);
 int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out);
 int fp64_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
+int tree_bounds_impl(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
+                     const void* G, const void* Bt, double* u, cudaStream_t s);
 int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
                     cudaStream_t s, float* ms);
 int gauss_line_impl(const double* pts, long long count, const double* base, double c, double* out,
@@ -568,6 +570,19 @@ int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, c
                              reinterpret_cast<cudaStream_t>(stream));
   *clamped = c;
   return rc;
+}
+
+int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
+                     const void* G, const void* Bt, double* u, void* stream) {
+  if (!ctx || !plan || !x || !y || !G || !Bt || !u || plan->n < 1 || plan->m < 1 ||
+      plan->p < 1 || plan->p > 8 || plan->n_tleaves < 1 || plan->n_snodes < 1 ||
+      plan->n_sleaves < 1) {
+    set_error("rplu_tree_bounds: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return tree_bounds_impl(ctx, plan, x, y, G, Bt, u, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {

@@ -152,6 +152,56 @@ def cauchy_cases():
     save("cauchy", arrays, info)
 
 
+def _plan_signature(plan):
+    """Per target leaf (keyed by its smallest point index): sorted aggregated
+    alphas and the sorted point sets of the exact source leaves — a
+    numbering-independent description of an InteractionPlan."""
+    tgt, src = plan.target_tree, plan.source_tree
+    sig = {}
+    for leaf in tgt.leaves:
+        key = int(np.min(tgt.nodes[leaf].points))
+        alphas = sorted(float(a) for _, a in plan.aggregated[leaf])
+        exact = sorted(sorted(int(i) for i in src.nodes[s].points) for s in plan.exact[leaf])
+        sig[str(key)] = {"alphas": alphas, "exact": exact,
+                         "points": sorted(int(i) for i in tgt.nodes[leaf].points)}
+    return sig
+
+
+def cauchy_plan_cases():
+    """structured_eliminate WITH a plan (certified bounds + rejection
+    sampling), the path every in-package Cauchy caller takes."""
+    arrays, info = {}, []
+    cases = []
+    x, y, G, B = gen.c2_cauchy(0, n=300)
+    cases.append(("c2_300_plan", x, y, G, B, "rplu", 40, 9, 0.0, 5.0, 32))
+    x, y, G, B = gen.c4_cauchy_like(3, n=400, m=350, p=2)
+    cases.append(("c4_400x350_p2_plan", x, y, G, B, "rplu", 30, 5, 0.0, 5.0, 16))
+    x, y, G, B = gen.c4_cauchy_like(4, n=256, p=4)
+    cases.append(("c4_256_c2plu_plan", x, y, G, B, "c2plu", 20, None, 0.0, 3.0, 32))
+    for name, x, y, G, B, rule, rank, seed, tol, nu, leaf in cases:
+        M = rplu.CauchyLikeMatrix(x, y, G, B)
+        plan = rplu.build_plan(x, y, nu=nu, leaf_size=leaf)
+        u0 = rplu.certified_upper_bounds(plan, M.G, M.B)
+        rng = rplu.RngState(seed) if seed is not None else None
+        tr = rplu.structured_eliminate(M, rule, rank, stop_tol=tol, nu=nu, plan=plan, rng=rng,
+                                       keep_steps=True)
+        after = rng.uniform() if rng is not None else None
+        arrays[name + "_x"], arrays[name + "_y"] = x, y
+        arrays[name + "_G"], arrays[name + "_B"] = G, B
+        arrays[name + "_u0"] = u0
+        arrays[name + "_exact0"] = rplu.exact_row_norms(M)
+        if tr.steps:
+            arrays[name + "_r"] = np.stack([s[1] for s in tr.steps])
+        info.append({"name": name, "rule": rule, "rank": rank, "seed": seed, "stop_tol": tol,
+                     "nu": nu, "leaf_size": leaf, "rows": tr.row_indices,
+                     "cols": tr.col_indices, "proposals": tr.proposals,
+                     "acceptances": tr.acceptances, "exact_fallbacks": tr.exact_fallbacks,
+                     "bound_sums": tr.bound_sums, "bound_maxes": tr.bound_maxes,
+                     "tol_stop": tr.tol_stop, "degenerate_stop": tr.degenerate_stop,
+                     "next_uniform": after, "plan": _plan_signature(plan)})
+    save("cauchy_plan", arrays, info)
+
+
 class _Gauss(rplu.CallableOperator):
     def __init__(self, P, Q, h=0.1):
         d2 = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(-1)
@@ -205,6 +255,7 @@ if __name__ == "__main__":
     sample_index_cases()
     dense_cases()
     cauchy_cases()
+    cauchy_plan_cases()
     cur_cases()
     if "--c1" in sys.argv:
         c1_runs()

@@ -70,7 +70,7 @@ def test_validation(cuda_device):
         rp.structured_eliminate(M, "rplu", 2)
     with pytest.raises(ValueError):
         rp.structured_eliminate(M, "rplu", 33, rng=rp.RngState(0))
-    with pytest.raises(rp.CapabilityError):
+    with pytest.raises(ValueError):
         rp.structured_eliminate(M, "rplu", 2, rng=rp.RngState(0), plan=object())
     with pytest.raises(ValueError):
         rp.CauchyLikeMatrix(x, x, G, B)          # coincident points
