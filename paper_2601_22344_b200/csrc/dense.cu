@@ -723,7 +723,10 @@ struct LazyPipeSmem {
   double red[8][RPT];
 };
 
-template <typename T, int VEC, int RPT, bool FLUSH>
+// QC > 0: the number of pending terms is a compile-time constant (one
+// instantiation per q), so the term loop is fully unrolled with immediate
+// shared-memory offsets and the FP64 pipe is not starved by address math.
+template <typename T, int VEC, int RPT, bool FLUSH, int QC = 0>
 __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
   using S = Scalar<T>;
   using SM = LazyPipeSmem<T, VEC, RPT>;
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const long long row0 = (long long)blockIdx.x * ROWS;
   const long long n = p.n, m = p.m, ld = p.ld;
-  const int q = (int)(p.t - p.t0 + 1);
+  const int q = QC > 0 ? QC : (int)(p.t - p.t0 + 1);
   T* R = reinterpret_cast<T*>(p.R);
   const T* Lt = reinterpret_cast<const T*>(p.Lt);
   const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
@@ -782,7 +785,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
       VecT<T, VEC> rv[RPT];
 #pragma unroll
       for (int r = 0; r < RPT; ++r) rv[r] = sm.Rs[buf][ty * RPT + r][tx];
-      for (int s = 0; s < q; ++s) {
+      auto term = [&](int s) {
         const VecT<T, VEC> u = sm.Us[buf][s][tx];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
@@ -790,6 +793,12 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
 #pragma unroll
           for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
         }
+      };
+      if constexpr (QC > 0) {
+#pragma unroll
+        for (int s = 0; s < QC; ++s) term(s);
+      } else {
+        for (int s = 0; s < q; ++s) term(s);
       }
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -950,22 +959,40 @@ static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) 
   else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
 }
 
-template <typename T, int RPT>
-static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
+template <typename T, int RPT, bool FLUSH, int QC>
+static void launch_lazy_pass3_q(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   using SM = LazyPipeSmem<T, VEC, RPT>;
   const int smem = (int)sizeof(SM);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, false>,
+    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   dim3 grid((unsigned)((p.n + SM::ROWS - 1) / SM::ROWS));
-  if (flush) lazy_pass3_kernel<T, VEC, RPT, true><<<grid, 256, smem, s>>>(p);
-  else lazy_pass3_kernel<T, VEC, RPT, false><<<grid, 256, smem, s>>>(p);
+  lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC><<<grid, 256, smem, s>>>(p);
+}
+
+template <typename T, int RPT, bool FLUSH>
+static void launch_lazy_pass3_f(const DenseParams& p, cudaStream_t s) {
+  switch ((int)(p.t - p.t0 + 1)) {
+    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1>(p, s); return;
+    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2>(p, s); return;
+    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3>(p, s); return;
+    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4>(p, s); return;
+    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5>(p, s); return;
+    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6>(p, s); return;
+    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7>(p, s); return;
+    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8>(p, s); return;
+    default: launch_lazy_pass3_q<T, RPT, FLUSH, 0>(p, s); return;
+  }
+}
+
+template <typename T, int RPT>
+static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
+  if (flush) launch_lazy_pass3_f<T, RPT, true>(p, s);
+  else launch_lazy_pass3_f<T, RPT, false>(p, s);
 }
 
 template <typename T>
@@ -974,7 +1001,7 @@ static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D
   static const int kernel = env_int("RPLU_LAZY_KERNEL", 3);
   if (kernel == 3) {
-    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 4);
+    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 8);
     if (rpt >= 8) launch_lazy_pass3<T, 8>(p, flush, s);
     else if (rpt >= 4) launch_lazy_pass3<T, 4>(p, flush, s);
     else launch_lazy_pass3<T, 2>(p, flush, s);
