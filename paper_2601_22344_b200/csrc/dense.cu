@@ -1016,12 +1016,14 @@ static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   launch_lazy_pass2<T, sizeof(T) == 16 ? 4 : 8>(p, flush, s);
 }
 
-// Default flush interval: where the 2q FP ops per element of the last
-// pending steps start to exceed the read time of the element (fp64 10,
-// fp32 8, complex128 6 on B200), overridable with RPLU_LAZY_BLOCK.
+// Default flush interval: the pass is HBM-bound up to q ~ 3 pending terms and
+// then grows ~0.12 ms per term at C3 while a flush costs a full write of R;
+// the per-step minimum on B200 is at 5 (fp64; measured 1.25 / 1.23 / 1.26 /
+// 1.38 ms for q = 1..4, 2.7 ms for a flush), overridable with
+// RPLU_LAZY_BLOCK.
 template <typename T>
 static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 6 : (sizeof(T) == 4 ? 8 : 10);
+  const int dflt = sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 5 : 5);
   int b = env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
