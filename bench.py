@@ -60,13 +60,21 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _traffic(cfg, n):
+def _traffic(cfg, n, lazy_frac_flush=None):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_traffic.json), when it matches."""
+    --set full capture (profiles/ncu_traffic.json), when it matches; for the
+    delayed-update loop the read-pass / flush captures weighted by the timed
+    launch mix (lazy_frac_flush = share of flush launches)."""
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
         key = "c3" + cfg["dtype"]
+        if lazy_frac_flush is not None:
+            e = t.get(key + "_lazy")
+            if e and e["n"] == n:
+                return ((1.0 - lazy_frac_flush) * e["read_pass_traffic_bytes"]
+                        + lazy_frac_flush * e["flush_traffic_bytes"])
+            return None
         if key in t and t[key]["n"] == n:
             return t[key]["traffic_bytes"]
     except Exception:
@@ -459,6 +467,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     sweep_bytes = sum(s.get("sweep_bytes", 0.0) for s in stats)
     lazy_block = stats[-1].get("lazy_block", 0)
     bytes_per_launch = sweep_bytes / sweep_n
+    # share of flush launches (read + write R) among the timed update launches
+    flush_share = (sweep_bytes / (float(n) * n * esize) - sweep_n) / sweep_n
     avg_s = (sweep_ms / sweep_n) / 1e3
     achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
     peak, peak_src = _peaks()
@@ -500,7 +510,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                             else f"one full elimination of {rank} pivot steps"),
                    "l2": f"inputs larger than L2 ({n * n * esize / 1e9:.1f} GB residual)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(cfg, n),
+                     "frac": achieved / peak,
+                     "traffic": _traffic(cfg, n, flush_share if lazy_block else None),
                      "kernel": ("lazy_pass_kernel (K3 delayed-update pass + row masses)"
                                 if lazy_block else
                                 "dense_sweep_kernel (K3 fused Schur update + row masses)"),

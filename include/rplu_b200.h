@@ -58,6 +58,13 @@ extern "C" {
 #define RPLU_FLAG_LAZY 4         /* dense: force the delayed-update loop */
 #define RPLU_FLAG_EAGER 8        /* dense: force the eager (update every step) loop;
                                     default: delayed updates when R exceeds L2 */
+#define RPLU_FLAG_FUSED 16       /* dense delayed-update loop: apply each pending term
+                                    with fused multiply-adds (x - l*u rounded once; 4
+                                    FMAs per complex term) instead of the reference's
+                                    multiply-then-subtract;
+                                    residual / L / U then differ from the reference by
+                                    rounding (not bit-identical), pivots agree except
+                                    at counted near-boundary draws */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0
@@ -129,12 +136,19 @@ int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* o
  *   select(steps) (final residual norm) -> finish.
  * With t = -1 the kernels read the step from a device counter, so one step
  * (kernels + collectives) can be captured in a CUDA graph and replayed.
- * Non-owning ranks contribute -0.0, so the sums reproduce the owner's bits. */
+ * Non-owning ranks contribute -0.0, so the sums reproduce the owner's bits.
+ * With lazy_block != 0 the local rows take the delayed-update loop of
+ * rplu_dense_run (one read of the row block per step, a write every block
+ * steps; the owner rebuilds its pivot row on the fly) and finish applies the
+ * pending steps after an early stop; the results are bit-identical. */
 
 typedef struct rplu_shard_args {
   int32_t dtype;          /* RPLU_F32 | RPLU_F64 | RPLU_C128 */
   int32_t world, rank;    /* shard count and this shard's index */
-  int32_t reserved;
+  int32_t lazy_block;     /* 0: eager K3 update; > 0 (<= 12): delayed-update
+                           * block (flush every lazy_block steps; needs the
+                           * host step loop, t >= 0, and 16-byte aligned rows
+                           * of R and U); < 0: the single-GPU default */
   int64_t n_local, m;     /* local row block shape */
   int64_t ld;             /* row stride of R (elements) */
   int64_t row_offset;     /* global index of local row 0 */
@@ -147,6 +161,8 @@ typedef struct rplu_shard_args {
   const double* uniforms; /* host uniform stream (uploaded by begin) */
   int64_t n_uniforms;
   void* stream;
+  int32_t flags;          /* RPLU_FLAG_FUSED (delayed-update terms as one FMA) */
+  int32_t reserved;
 } rplu_shard_args;
 
 /* K1 masses of the local rows, state reset, uniforms upload; writes the local
@@ -216,6 +232,51 @@ typedef struct rplu_cauchy_out {
 } rplu_cauchy_out;
 
 int rplu_cauchy_run(rplu_ctx* ctx, const rplu_cauchy_args* args, rplu_cauchy_out* out);
+
+/* Row-block sharded Cauchy-like RPLU: x and G are sharded
+ * by rows, y and B replicated (B updated redundantly on every rank).  Per step
+ * the host driver runs
+ *   select(t) -> allreduce_sum(msg) -> update(t) -> allgather(local_stats)
+ * where local_stats = [sum_i u_i, max_i u_i] of the local rows (device
+ * doubles) and totals = the allgathered [world][2] stats.  The owner shard
+ * (CDF over shard sums with u1, or the first shard holding the global max
+ * for c2plu) writes the pivot message msg (RPLU_CAUCHY_MSG_DOUBLES fp64):
+ * [i_global, 0, x_i (re, im), G_i (p complex)]; the other ranks write -0.0.
+ * update regenerates the pivot row r from the message on every rank
+ * (identical bits), draws the column with u2 (same draw everywhere), and
+ * updates the local G rows and all of B, then K5 masses of the local rows.
+ * With C / Rrow / a set, the kept steps hold the LOCAL c rows (rank x
+ * n_local).  Host step loop (t >= 0); no tree plan on this path. */
+#define RPLU_CAUCHY_MSG_DOUBLES 20
+
+typedef struct rplu_cauchy_shard_args {
+  int32_t rule;           /* RPLU_RULE_RPLU | RPLU_RULE_C2PLU */
+  int32_t p;              /* displacement rank, 1..8 */
+  int32_t world, rank;    /* shard count and this shard's index */
+  int64_t n_local, m;     /* local rows, all columns */
+  int64_t row_offset;     /* global index of local row 0 */
+  int64_t steps;          /* pivots requested (the global rank) */
+  double stop_tol;
+  const void* x;          /* device complex128[n_local] (local rows) */
+  const void* y;          /* device complex128[m] (replicated) */
+  void* G;                /* device complex128 n_local x p (local rows) */
+  void* Bt;               /* device complex128 m x p (replicated) */
+  void* C;                /* device complex128 steps x n_local, or NULL */
+  void* Rrow;             /* device complex128 steps x m, or NULL */
+  void* a;                /* device complex128[steps], or NULL */
+  const double* uniforms; /* host uniform stream (uploaded by begin) */
+  int64_t n_uniforms;
+  void* stream;
+} rplu_cauchy_shard_args;
+
+int rplu_cauchy_shard_begin(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* local_stats);
+int rplu_cauchy_shard_select(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int64_t t,
+                             const double* totals, void* msg);
+int rplu_cauchy_shard_update(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int64_t t,
+                             const void* msg, double* local_stats);
+int rplu_cauchy_shard_active(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int32_t* active);
+int rplu_cauchy_shard_finish(rplu_ctx* ctx, const rplu_cauchy_shard_args* a,
+                             rplu_cauchy_out* out);
 
 /* Certified row-norm upper bounds from a quadtree interaction plan
  * (treebounds.py:213-242, Alg C.2): exact <= u_i <= nu*exact.  The plan is

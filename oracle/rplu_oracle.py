@@ -20,7 +20,7 @@ import numpy as np
 import scipy.linalg
 
 __all__ = [
-    "NEAR_REL", "sample_index", "draw_margin", "uniform_stream",
+    "NEAR_REL", "PIVOT_REL_TOL", "sample_index", "draw_margin", "uniform_stream",
     "eliminate_c128", "eliminate_real", "replay_pivots",
     "cauchy_row", "cauchy_column", "exact_row_norms", "structured_eliminate",
     "generator_schur_update", "GaussianKernelHost", "DenseHost", "cur_build",

@@ -34,6 +34,7 @@ FLAG_TIME_KERNELS = 1
 FLAG_NO_GRAPH = 2
 FLAG_LAZY = 4
 FLAG_EAGER = 8
+FLAG_FUSED = 16
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -88,13 +89,28 @@ class CauchyOut(ctypes.Structure):
 
 class ShardArgs(ctypes.Structure):
     _fields_ = [
-        ("dtype", c_i32), ("world", c_i32), ("rank", c_i32), ("reserved", c_i32),
+        ("dtype", c_i32), ("world", c_i32), ("rank", c_i32), ("lazy_block", c_i32),
         ("n_local", c_i64), ("m", c_i64), ("ld", c_i64), ("row_offset", c_i64),
         ("steps", c_i64), ("stop_tol", c_dbl),
         ("R", c_vp), ("Lt", c_vp), ("U", c_vp), ("ldu", c_i64),
         ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
+        ("stream", c_vp), ("flags", c_i32), ("reserved", c_i32),
+    ]
+
+
+class CauchyShardArgs(ctypes.Structure):
+    _fields_ = [
+        ("rule", c_i32), ("p", c_i32), ("world", c_i32), ("rank", c_i32),
+        ("n_local", c_i64), ("m", c_i64), ("row_offset", c_i64), ("steps", c_i64),
+        ("stop_tol", c_dbl),
+        ("x", c_vp), ("y", c_vp), ("G", c_vp), ("Bt", c_vp),
+        ("C", c_vp), ("Rrow", c_vp), ("a", c_vp),
+        ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
         ("stream", c_vp),
     ]
+
+
+CAUCHY_MSG_DOUBLES = 20   # RPLU_CAUCHY_MSG_DOUBLES
 
 
 class TreePlan(ctypes.Structure):
@@ -138,6 +154,15 @@ SIGNATURES = {
     "rplu_shard_active": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), ctypes.POINTER(c_i32)]),
     "rplu_shard_finish": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs),
                                          ctypes.POINTER(DenseOut)]),
+    "rplu_cauchy_shard_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs), c_vp]),
+    "rplu_cauchy_shard_select": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs), c_i64,
+                                                c_vp, c_vp]),
+    "rplu_cauchy_shard_update": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs), c_i64,
+                                                c_vp, c_vp]),
+    "rplu_cauchy_shard_active": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs),
+                                                ctypes.POINTER(c_i32)]),
+    "rplu_cauchy_shard_finish": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs),
+                                                ctypes.POINTER(CauchyOut)]),
 }
 
 

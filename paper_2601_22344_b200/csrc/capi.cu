@@ -339,7 +339,21 @@ static int shard_check(rplu_ctx* ctx, const rplu_shard_args* a) {
     set_error("rplu_shard: unknown dtype");
     return RPLU_ERR_ARG;
   }
+  if (a->lazy_block != 0) {
+    const long long vec = 16 / (a->dtype == RPLU_F32 ? 4 : (a->dtype == RPLU_F64 ? 8 : 16));
+    if (a->lazy_block > kLazyMaxBlock || a->ld % vec || a->ldu % vec ||
+        (uintptr_t)a->R % 16 || (uintptr_t)a->U % 16 || !a->Lt) {
+      set_error("rplu_shard: lazy_block needs <= 12, 16-byte aligned rows of R and U, and Lt");
+      return RPLU_ERR_ARG;
+    }
+  }
   return RPLU_OK;
+}
+
+static int shard_block(const rplu_shard_args* a) {
+  return a->lazy_block < 0
+             ? dense_lazy_block_default(a->dtype, (a->flags & RPLU_FLAG_FUSED) != 0)
+             : a->lazy_block;
 }
 
 static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
@@ -362,6 +376,9 @@ static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
   p.resid = reinterpret_cast<double*>(ctx->resid.ptr);
   p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
   p.stop_tol = a->stop_tol;
+  p.Lt = a->Lt;
+  p.lazy_block = shard_block(a);
+  p.fused = p.lazy_block > 0 && (a->flags & RPLU_FLAG_FUSED) != 0;
   return p;
 }
 
@@ -418,6 +435,13 @@ int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   p.t = t < 0 ? -1 : t;
   p.totals = totals;
   p.msg = msg;
+  if (p.lazy_block > 0) {
+    if (t < 0) {
+      set_error("rplu_shard_select: the delayed-update loop needs explicit steps (t >= 0)");
+      return RPLU_ERR_ARG;
+    }
+    return shard_lazy_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
+  }
   return shard_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
 }
 
@@ -435,8 +459,19 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   ShardParams p = shard_params(ctx, a);
   p.t = t < 0 ? -1 : t;
   p.msg = const_cast<void*>(msg);
+  if (p.lazy_block > 0 && t < 0) {
+    set_error("rplu_shard_update: the delayed-update loop needs explicit steps (t >= 0)");
+    return RPLU_ERR_ARG;
+  }
   if ((rc = shard_post_impl(p, s))) return rc;
-  if (a->n_local > 0) {
+  if (p.lazy_block > 0) {
+    const long long b = p.lazy_block, t0 = (t / b) * b;
+    const bool flush = (t + 1 - t0 == b) || (t == a->steps - 1);
+    if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
+                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, p.fused,
+                                     s)))
+      return rc;
+  } else if (a->n_local > 0) {
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
                                  p.masses, p.st, p.t, true, s)))
       return rc;
@@ -471,6 +506,20 @@ int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* o
   RPLU_CUDA(cudaMemcpyAsync(&hs, ctx->state.ptr, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   RPLU_CUDA(cudaStreamSynchronize(s));
   const long long done = hs.done;
+  const int block = shard_block(a);
+  out->lazy_block = block;
+  if (block > 0 && done < a->steps) {
+    // early stop: the local rows hold R^(t0) of the last flush
+    const long long t0 = (done / block) * block;
+    if (done > t0) {
+      if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
+                                       a->ldu, reinterpret_cast<double*>(ctx->masses.ptr),
+                                       reinterpret_cast<DevState*>(ctx->state.ptr), done - 1, t0,
+                                       false, true, true, (a->flags & RPLU_FLAG_FUSED) != 0, s)))
+        return rc;
+      RPLU_CUDA(cudaStreamSynchronize(s));
+    }
+  }
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, ctx->pivots.ptr, sizeof(long long) * 2 * done,
                          cudaMemcpyDeviceToHost));
@@ -493,6 +542,94 @@ int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* o
     return RPLU_ERR_ARG;
   }
   return RPLU_OK;
+}
+
+static int cauchy_shard_check(rplu_ctx* ctx, const rplu_cauchy_shard_args* a) {
+  if (!ctx || !a || a->world < 1 || a->rank < 0 || a->rank >= a->world || a->n_local < 0 ||
+      a->m < 1 || a->p < 1 || a->p > 8 || a->steps < 0 || !a->y || !a->Bt ||
+      (a->n_local > 0 && (!a->x || !a->G)) || a->row_offset < 0) {
+    set_error("rplu_cauchy_shard: bad arguments");
+    return RPLU_ERR_ARG;
+  }
+  if (a->rule != RPLU_RULE_RPLU && a->rule != RPLU_RULE_C2PLU) {
+    set_error("rplu_cauchy_shard: rule must be rplu or c2plu");
+    return RPLU_ERR_ARG;
+  }
+  return RPLU_OK;
+}
+
+int rplu_cauchy_shard_begin(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* local_stats) {
+  int rc;
+  if ((rc = cauchy_shard_check(ctx, a))) return rc;
+  if (!local_stats || (a->rule == RPLU_RULE_RPLU && (!a->uniforms || a->n_uniforms < 2))) {
+    set_error("rplu_cauchy_shard_begin: needs local_stats and (rplu) a uniform stream");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_shard_begin_impl(ctx, a, local_stats);
+}
+
+int rplu_cauchy_shard_select(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int64_t t,
+                             const double* totals, void* msg) {
+  int rc;
+  if ((rc = cauchy_shard_check(ctx, a))) return rc;
+  if (!totals || !msg || t < 0 || t >= a->steps) {
+    set_error("rplu_cauchy_shard_select: bad arguments (0 <= t < steps)");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_shard_select_impl(ctx, a, t, totals, msg);
+}
+
+int rplu_cauchy_shard_update(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int64_t t,
+                             const void* msg, double* local_stats) {
+  int rc;
+  if ((rc = cauchy_shard_check(ctx, a))) return rc;
+  if (!msg || !local_stats || t < 0 || t >= a->steps) {
+    set_error("rplu_cauchy_shard_update: bad arguments (0 <= t < steps)");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_shard_update_impl(ctx, a, t, msg, local_stats);
+}
+
+int rplu_cauchy_shard_active(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int32_t* active) {
+  int rc;
+  if ((rc = cauchy_shard_check(ctx, a))) return rc;
+  if (!active) { set_error("rplu_cauchy_shard_active: NULL active"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  int v = 0;
+  if ((rc = cauchy_shard_active_impl(ctx, a, &v))) return rc;
+  *active = v;
+  return RPLU_OK;
+}
+
+int rplu_cauchy_shard_finish(rplu_ctx* ctx, const rplu_cauchy_shard_args* a,
+                             rplu_cauchy_out* out) {
+  int rc;
+  if ((rc = cauchy_shard_check(ctx, a))) return rc;
+  if (!out || (a->steps > 0 && (!out->rows || !out->cols || !out->bound_maxes ||
+                                !out->bound_sums))) {
+    set_error("rplu_cauchy_shard_finish: bad output");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  rc = cauchy_shard_finish_impl(ctx, a, out);
+  if (rc == kZeroPivot) {
+    set_error("pivot (" + std::to_string(out->zero_pivot_i) + ", " +
+              std::to_string(out->zero_pivot_j) + ") is numerically zero after one resample");
+    return RPLU_ERR_ZERO_PIVOT;
+  }
+  if (rc == kUniformsExhausted) {
+    set_error("uniform stream exhausted");
+    return RPLU_ERR_ARG;
+  }
+  return rc < 0 ? rc : RPLU_OK;
 }
 
 int rplu_gauss_apply(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t adjoint, const double* v,

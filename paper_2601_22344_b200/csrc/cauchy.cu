@@ -52,6 +52,9 @@ struct CauchyParams {
   double* bsum;
   double stop_tol;
   int rule;
+  // sharded path: the pivot message [(i_global, 0), x_i, G_i[0..P)] the row
+  // and snapshot kernels read instead of G / x (null on one GPU)
+  const double2* psrc;
 };
 
 // ---------------------------------------------------------------------------
@@ -210,11 +213,19 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
 template <int P>
 __global__ void cauchy_row_kernel(CauchyParams q) {
   if (!q.st->active) return;
-  const long long i = q.st->pi;
   double2 gi[P];
+  double2 xi;
+  if (q.psrc) {
 #pragma unroll
-  for (int l = 0; l < P; ++l) gi[l] = q.G[i * P + l];
-  const double2 xi = q.x[i];
+    for (int l = 0; l < P; ++l) gi[l] = q.psrc[2 + l];
+    xi = q.psrc[1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) q.st->pi = (long long)q.psrc[0].x;
+  } else {
+    const long long i = q.st->pi;
+#pragma unroll
+    for (int l = 0; l < P; ++l) gi[l] = q.G[i * P + l];
+    xi = q.x[i];
+  }
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < q.m;
        j += (long long)gridDim.x * blockDim.x) {
     double re = 0.0, im = 0.0;
@@ -382,7 +393,7 @@ __global__ void cauchy_snapshot_kernel(CauchyParams q, double2* gsnap) {
   if (!q.st->active) return;
   const int l = threadIdx.x;
   if (l < q.p) {
-    gsnap[l] = q.G[q.st->pi * q.p + l];
+    gsnap[l] = q.psrc ? q.psrc[2 + l] : q.G[q.st->pi * q.p + l];
     gsnap[q.p + l] = q.Bt[q.st->pj * q.p + l];
   }
 }
@@ -584,6 +595,325 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
     for (auto e : ev) cudaEventDestroy(e);
   }
   return hs.status;
+}
+
+// ---------------------------------------------------------------------------
+// Row-block sharded Cauchy-like RPLU.  Rank s owns rows
+// [row_offset, row_offset + n_local) of x / G; y / Bt are replicated.
+namespace {
+
+struct CauchyShard {
+  CauchyParams q;
+  double2* gsnap;
+  int world, rank;
+  long long row_offset;
+  long long steps;
+};
+
+// Local [sum u_i (the CDF code's association), max u_i] of the local rows.
+__global__ void __launch_bounds__(1024) cauchy_shard_stats_kernel(const double* masses, long long n,
+                                                                 double* out) {
+  constexpr int B = 1024;
+  __shared__ CdfSmem<B> sm;
+  __shared__ double s_max[B / 32];
+  double mx = 0.0;
+  for (long long k = threadIdx.x; k < n; k += B) mx = fmax(mx, masses[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+  double total = 0.0;
+  if (n > 0) {
+    auto w = [&](long long k) { return masses[k]; };
+    Cdf<B> c = cdf_build<B>(w, n, sm);
+    total = c.total;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m2 = 0.0;
+    for (int k = 0; k < B / 32; ++k) m2 = fmax(m2, s_max[k]);
+    out[0] = total;
+    out[1] = m2;
+  }
+}
+
+__device__ __forceinline__ void cauchy_msg_neg_zero(double* msg) {
+  if (threadIdx.x < RPLU_CAUCHY_MSG_DOUBLES) msg[threadIdx.x] = -0.0;
+}
+
+// Global stats + stop rules + owner (every rank identically), owner's local
+// row draw, pivot message.
+__global__ void __launch_bounds__(1024) cauchy_shard_select_kernel(CauchyParams q, int world,
+                                                                  int rank, long long row_offset,
+                                                                  const double* totals,
+                                                                  double* msg) {
+  constexpr int B = 1024;
+  DevState* st = q.st;
+  __shared__ CdfSmem<B> sm;
+  __shared__ int s_owner, s_stop;
+  __shared__ double s_target;
+  if (!st->active) {
+    cauchy_msg_neg_zero(msg);
+    return;
+  }
+  const long long t = q.t;
+  if (threadIdx.x == 0) {
+    double T_all = 0.0, umax = 0.0;
+    for (int s = 0; s < world; ++s) {
+      T_all += totals[2 * s];
+      umax = fmax(umax, totals[2 * s + 1]);
+    }
+    q.bmax[t] = umax;
+    q.bsum[t] = T_all;
+    if (t == 0) st->fro0 = umax;
+    const double u0 = (t == 0) ? umax : st->fro0;
+    int stop = 0;
+    if (umax <= 0.0) {
+      st->status = kDegenerate;
+      stop = 1;
+    } else if (q.stop_tol > 0.0 && umax <= q.stop_tol * q.stop_tol * u0) {
+      st->status = kTolStop;
+      stop = 1;
+    } else if (q.rule == RPLU_RULE_RPLU && st->ucount + 1 > q.n_uniforms) {
+      st->status = kUniformsExhausted;
+      stop = 1;
+    }
+    int owner = -1;
+    double target = 0.0;
+    if (!stop) {
+      if (q.rule == RPLU_RULE_RPLU) {
+        const double tg = q.uniforms[st->ucount] * T_all;
+        double c = 0.0;
+        int last_pos = -1;
+        for (int s = 0; s < world; ++s) {
+          if (totals[2 * s] > 0.0) last_pos = s;
+          const double c2 = c + totals[2 * s];
+          if (owner < 0 && c2 > tg && totals[2 * s] > 0.0) {
+            owner = s;
+            target = tg - c;
+          }
+          c = c2;
+        }
+        if (owner < 0) {
+          owner = last_pos;
+          target = totals[2 * owner];
+        }
+        const double tol = kNearBoundaryRel * T_all;
+        double cb = 0.0;
+        for (int s = 0; s <= owner; ++s) {
+          if (fabs(cb - tg) <= tol) st->near_boundary++;
+          cb += totals[2 * s];
+        }
+        st->ucount += 1;
+      } else {
+        // greedy: the first shard holding the global maximum (np.argmax)
+        for (int s = 0; s < world && owner < 0; ++s)
+          if (totals[2 * s + 1] == umax) owner = s;
+      }
+    }
+    if (stop) st->active = 0;
+    s_stop = stop;
+    s_owner = owner;
+    s_target = target;
+  }
+  __syncthreads();
+  if (s_stop || s_owner != rank) {
+    cauchy_msg_neg_zero(msg);
+    return;
+  }
+  const double* masses = q.masses;
+  auto wrow = [&](long long k) { return masses[k]; };
+  long long i;
+  if (q.rule == RPLU_RULE_RPLU) {
+    Cdf<B> cr = cdf_build<B>(wrow, q.n, sm);
+    i = cdf_find_target<B>(wrow, q.n, cr, s_target, sm);
+  } else {
+    i = block_argmax<B>(wrow, q.n, nullptr);
+  }
+  if (threadIdx.x == 0) {
+    msg[0] = (double)(row_offset + i);
+    msg[1] = 0.0;
+    msg[2] = q.x[i].x;
+    msg[3] = q.x[i].y;
+  }
+  if (threadIdx.x < 8) {
+    const int l = threadIdx.x;
+    const double2 g = l < q.p ? q.G[i * q.p + l] : make_double2(-0.0, -0.0);
+    msg[4 + 2 * l] = g.x;
+    msg[5 + 2 * l] = g.y;
+  }
+}
+
+__global__ void cauchy_shard_init_state(DevState* st) {
+  st->ucount = 0;
+  st->near_boundary = 0;
+  st->pi = st->pj = -1;
+  st->err_i = st->err_j = -1;
+  st->active = 1;
+  st->status = kRunning;
+  st->fro0 = 0.0;
+  st->done = 0;
+  st->step = 0;
+}
+
+int cauchy_shard_setup(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, CauchyShard& sh,
+                       bool alloc) {
+  const long long n = a->n_local, m = a->m, K = a->steps;
+  CauchyParams& q = sh.q;
+  q = CauchyParams{};
+  q.n = n;
+  q.m = m;
+  q.rank = K;
+  q.p = a->p;
+  q.x = reinterpret_cast<const double2*>(a->x);
+  q.y = reinterpret_cast<const double2*>(a->y);
+  q.G = reinterpret_cast<double2*>(a->G);
+  q.Bt = reinterpret_cast<double2*>(a->Bt);
+  q.splits = n > 0 ? choose_splits(n, m, rows_per_cta(a->p), ctx->sm_count) : 1;
+  q.stop_tol = a->stop_tol;
+  q.rule = a->rule;
+  int rc;
+  if (alloc) {
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    if ((rc = ctx->scratch[0].ensure(sizeof(double) * (size_t)q.splits * nn))) return rc;
+    if ((rc = ctx->scratch[1].ensure(sizeof(double2) * (size_t)m))) return rc;
+    if ((rc = ctx->scratch[2].ensure(sizeof(double) * (size_t)m))) return rc;
+    if ((rc = ctx->scratch[3].ensure(sizeof(double2) * 16))) return rc;
+    if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
+    if ((rc = ctx->pivots.ensure(sizeof(long long) * (size_t)(2 * K + 2)))) return rc;
+    if ((rc = ctx->resid.ensure(sizeof(double) * (size_t)(2 * K + 2)))) return rc;
+    if ((rc = ctx->masses.ensure(sizeof(double) * nn))) return rc;
+    const long long nu = a->rule == RPLU_RULE_RPLU ? a->n_uniforms : 0;
+    if ((rc = ctx->uniforms.ensure(sizeof(double) * (size_t)(nu > 0 ? nu : 1)))) return rc;
+  }
+  q.partial = reinterpret_cast<double*>(ctx->scratch[0].ptr);
+  q.masses = q.splits > 1 ? reinterpret_cast<double*>(ctx->masses.ptr) : q.partial;
+  q.rbuf = reinterpret_cast<double2*>(ctx->scratch[1].ptr);
+  q.wbuf = reinterpret_cast<double*>(ctx->scratch[2].ptr);
+  sh.gsnap = reinterpret_cast<double2*>(ctx->scratch[3].ptr);
+  q.Cout = reinterpret_cast<double2*>(a->C);
+  q.Rout = reinterpret_cast<double2*>(a->Rrow);
+  q.Aout = reinterpret_cast<double2*>(a->a);
+  q.st = reinterpret_cast<DevState*>(ctx->state.ptr);
+  q.uniforms = reinterpret_cast<const double*>(ctx->uniforms.ptr);
+  q.n_uniforms = a->rule == RPLU_RULE_RPLU ? a->n_uniforms : 0;
+  long long* piv = reinterpret_cast<long long*>(ctx->pivots.ptr);
+  q.rows = piv;
+  q.cols = piv + K + 1;
+  double* bb = reinterpret_cast<double*>(ctx->resid.ptr);
+  q.bmax = bb;
+  q.bsum = bb + K + 1;
+  sh.world = a->world;
+  sh.rank = a->rank;
+  sh.row_offset = a->row_offset;
+  sh.steps = K;
+  return RPLU_OK;
+}
+
+// K5 masses of the local rows (+ split sum) and the local stats.
+int cauchy_shard_masses(CauchyShard& sh, double* stats, cudaStream_t s) {
+  CauchyParams& q = sh.q;
+  if (q.n > 0) {
+    RPLU_P_SWITCH(q.p, launch_mass<PP>(q, s));
+    if (q.splits > 1)
+      sum_partials_kernel<<<(unsigned)((q.n + 255) / 256), 256, 0, s>>>(q.partial, q.splits, q.n,
+                                                                        q.masses);
+  }
+  cauchy_shard_stats_kernel<<<1, 1024, 0, s>>>(q.masses, q.n, stats);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+}  // namespace
+
+int cauchy_shard_begin_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* stats) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  CauchyShard sh;
+  int rc;
+  if ((rc = cauchy_shard_setup(ctx, a, sh, true))) return rc;
+  if (sh.q.n_uniforms > 0)
+    RPLU_CUDA(cudaMemcpyAsync(ctx->uniforms.ptr, a->uniforms, sizeof(double) * sh.q.n_uniforms,
+                              cudaMemcpyHostToDevice, s));
+  cauchy_shard_init_state<<<1, 1, 0, s>>>(sh.q.st);
+  // K5 reads q.st->active (set by the init kernel, stream-ordered)
+  return cauchy_shard_masses(sh, stats, s);
+}
+
+int cauchy_shard_select_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, long long t,
+                             const double* totals, void* msg) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  CauchyShard sh;
+  int rc;
+  if ((rc = cauchy_shard_setup(ctx, a, sh, false))) return rc;
+  sh.q.t = t;
+  cauchy_shard_select_kernel<<<1, 1024, 0, s>>>(sh.q, sh.world, sh.rank, sh.row_offset, totals,
+                                                reinterpret_cast<double*>(msg));
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int cauchy_shard_update_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, long long t,
+                             const void* msg, double* stats) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  CauchyShard sh;
+  int rc;
+  if ((rc = cauchy_shard_setup(ctx, a, sh, false))) return rc;
+  CauchyParams& q = sh.q;
+  q.t = t;
+  q.psrc = reinterpret_cast<const double2*>(msg);
+  const int sm = ctx->sm_count;
+  const int upd_blocks = (int)std::min<long long>((q.n + q.m + 255) / 256, 8LL * sm);
+  const int row_blocks = (int)std::min<long long>((q.m + 255) / 256, 8LL * sm);
+  RPLU_P_SWITCH(q.p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, s>>>(q)));
+  cauchy_select_col_kernel<<<1, 1024, 0, s>>>(q);
+  cauchy_snapshot_kernel<<<1, 32, 0, s>>>(q, sh.gsnap);
+  RPLU_P_SWITCH(q.p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, s>>>(q, sh.gsnap)));
+  RPLU_CUDA(cudaGetLastError());
+  if (t + 1 < sh.steps) return cauchy_shard_masses(sh, stats, s);
+  return RPLU_OK;
+}
+
+int cauchy_shard_finish_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, rplu_cauchy_out* out) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  CauchyShard sh;
+  int rc;
+  if ((rc = cauchy_shard_setup(ctx, a, sh, false))) return rc;
+  const CauchyParams& q = sh.q;
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, q.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  const long long K = a->steps, done = hs.done;
+  long long nb = done + ((hs.status == kTolStop || hs.status == kDegenerate ||
+                          hs.status == kZeroPivot) ? 1 : 0);
+  if (nb > K) nb = K;
+  if (done > 0) {
+    RPLU_CUDA(cudaMemcpy(out->rows, q.rows, sizeof(long long) * done, cudaMemcpyDeviceToHost));
+    RPLU_CUDA(cudaMemcpy(out->cols, q.cols, sizeof(long long) * done, cudaMemcpyDeviceToHost));
+  }
+  if (nb > 0) {
+    RPLU_CUDA(cudaMemcpy(out->bound_maxes, q.bmax, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    RPLU_CUDA(cudaMemcpy(out->bound_sums, q.bsum, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+  }
+  out->steps_done = done;
+  out->bounds_recorded = nb;
+  out->uniforms_consumed = hs.ucount;
+  out->near_boundary_draws = hs.near_boundary;
+  out->tol_stop = hs.status == kTolStop;
+  out->degenerate_stop = hs.status == kDegenerate;
+  out->zero_pivot_i = hs.err_i;
+  out->zero_pivot_j = hs.err_j;
+  out->masses_ms = 0.0;
+  out->masses_launches = 0;
+  out->kernel_launches = 0;
+  return hs.status;
+}
+
+int cauchy_shard_active_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int* active) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
+  DevState hs;
+  RPLU_CUDA(cudaMemcpyAsync(&hs, ctx->state.ptr, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  *active = hs.active;
+  return RPLU_OK;
 }
 
 }  // namespace rplu

@@ -49,9 +49,8 @@ struct DenseParams {
   long long t0;
   int lazy;
   int force;  // run the pass even after a stop (final flush)
+  int fused;  // RPLU_FLAG_FUSED: pending terms as one FMA each
 };
-
-constexpr int kLazyMaxBlock = 12;  // longest delayed-update block
 
 template <typename T, int VEC>
 struct alignas(sizeof(T) * VEC) VecT {
@@ -415,7 +414,7 @@ __global__ void __launch_bounds__(256) lazy_row_kernel(DenseParams p) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
        k += (long long)gridDim.x * blockDim.x) {
     T x = R[i * p.ld + k];
-    for (int s = 0; s < q; ++s) x = S::sub_outer(x, s_l[s], U[s * p.ldu + k]);
+    for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, s_l[s], U[s * p.ldu + k]);
     urow[k] = x;
   }
 }
@@ -453,7 +452,7 @@ __global__ void __launch_bounds__(1024) lazy_select_col_kernel(DenseParams p) {
       const T* U = reinterpret_cast<const T*>(p.U);
       for (long long k = threadIdx.x; k < m; k += B) {
         T x = R[i * p.ld + k];
-        for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + i], U[s * p.ldu + k]);
+        for (long long s = p.t0; s < t; ++s) x = pend_sub(p.fused != 0, x, Lt[s * n + i], U[s * p.ldu + k]);
         urow[k] = x;
       }
       __syncthreads();
@@ -531,7 +530,7 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
       if (s < q) ll[s] = Lt[(p.t0 + s) * n + k];
 #pragma unroll
     for (int s = 0; s < kLazyMaxBlock; ++s)
-      if (s < q) x = S::sub_outer(x, ll[s], s_upiv[s]);
+      if (s < q) x = pend_sub(p.fused != 0, x, ll[s], s_upiv[s]);
     Lt[t * n + k] = S::scale(x, cf);
   }
 }
@@ -572,7 +571,7 @@ __global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
       for (int r = 0; r < RB; ++r) {
         const T lv = Ls[s][r];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+        for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub(p.fused != 0, rv[r].v[e], lv, u.v[e]);
       }
     }
 #pragma unroll
@@ -589,7 +588,7 @@ __global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
     for (int r = 0; r < RB; ++r) {
       if (r < nr) {
         T x = R[(row0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, Ls[s][r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(row0 + r) * ld + l] = x;
       }
@@ -661,7 +660,7 @@ __global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
         for (int r = 0; r < RPT; ++r) {
           const T lv = Ls[s][ty * RPT + r];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub(p.fused != 0, rv[r].v[e], lv, u.v[e]);
         }
       }
 #pragma unroll
@@ -679,7 +678,7 @@ __global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
     for (int r = 0; r < RPT; ++r) {
       if (r < nr) {
         T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(myrow0 + r) * ld + l] = x;
       }
@@ -726,7 +725,7 @@ struct LazyPipeSmem {
 // QC > 0: the number of pending terms is a compile-time constant (one
 // instantiation per q), so the term loop is fully unrolled with immediate
 // shared-memory offsets and the FP64 pipe is not starved by address math.
-template <typename T, int VEC, int RPT, bool FLUSH, int QC = 0>
+template <typename T, int VEC, int RPT, bool FLUSH, int QC = 0, bool FUSED = false>
 __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
   using S = Scalar<T>;
   using SM = LazyPipeSmem<T, VEC, RPT>;
@@ -791,7 +790,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
         for (int r = 0; r < RPT; ++r) {
           const T lv = sm.Ls[s][ty * RPT + r];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub<FUSED>(rv[r].v[e], lv, u.v[e]);
         }
       };
       if constexpr (QC > 0) {
@@ -815,7 +814,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
     for (int r = 0; r < RPT; ++r) {
       if (r < nr) {
         T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = pend_sub<FUSED>(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(myrow0 + r) * ld + l] = x;
       }
@@ -959,52 +958,68 @@ static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) 
   else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
 }
 
-template <typename T, int RPT, bool FLUSH, int QC>
+template <typename T, int RPT, bool FLUSH, int QC, bool FUSED>
 static void launch_lazy_pass3_q(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   using SM = LazyPipeSmem<T, VEC, RPT>;
   const int smem = (int)sizeof(SM);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC>,
+    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC, FUSED>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   dim3 grid((unsigned)((p.n + SM::ROWS - 1) / SM::ROWS));
-  lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC><<<grid, 256, smem, s>>>(p);
+  lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC, FUSED><<<grid, 256, smem, s>>>(p);
 }
 
-template <typename T, int RPT, bool FLUSH>
+template <typename T, int RPT, bool FLUSH, bool FUSED>
 static void launch_lazy_pass3_f(const DenseParams& p, cudaStream_t s) {
   switch ((int)(p.t - p.t0 + 1)) {
-    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1>(p, s); return;
-    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2>(p, s); return;
-    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3>(p, s); return;
-    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4>(p, s); return;
-    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5>(p, s); return;
-    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6>(p, s); return;
-    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7>(p, s); return;
-    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8>(p, s); return;
-    default: launch_lazy_pass3_q<T, RPT, FLUSH, 0>(p, s); return;
+    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1, FUSED>(p, s); return;
+    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2, FUSED>(p, s); return;
+    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3, FUSED>(p, s); return;
+    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4, FUSED>(p, s); return;
+    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5, FUSED>(p, s); return;
+    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6, FUSED>(p, s); return;
+    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7, FUSED>(p, s); return;
+    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8, FUSED>(p, s); return;
+    default: break;
   }
+  if constexpr (FUSED) {  // fused terms are cheap enough for longer blocks
+    switch ((int)(p.t - p.t0 + 1)) {
+      case 9: launch_lazy_pass3_q<T, RPT, FLUSH, 9, FUSED>(p, s); return;
+      case 10: launch_lazy_pass3_q<T, RPT, FLUSH, 10, FUSED>(p, s); return;
+      case 11: launch_lazy_pass3_q<T, RPT, FLUSH, 11, FUSED>(p, s); return;
+      case 12: launch_lazy_pass3_q<T, RPT, FLUSH, 12, FUSED>(p, s); return;
+      default: break;
+    }
+  }
+  launch_lazy_pass3_q<T, RPT, FLUSH, 0, FUSED>(p, s);
 }
 
-template <typename T, int RPT>
+template <typename T, int RPT, bool FUSED>
 static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
-  if (flush) launch_lazy_pass3_f<T, RPT, true>(p, s);
-  else launch_lazy_pass3_f<T, RPT, false>(p, s);
+  if (flush) launch_lazy_pass3_f<T, RPT, true, FUSED>(p, s);
+  else launch_lazy_pass3_f<T, RPT, false, FUSED>(p, s);
 }
 
 template <typename T>
 static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA);
-  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D
+  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D.
+  // Fused terms always take the default pipelined kernel.
   static const int kernel = env_int("RPLU_LAZY_KERNEL", 3);
+  constexpr int kDefRpt = sizeof(T) == 16 ? 2 : 8;
+  if (p.fused) {
+    launch_lazy_pass3<T, kDefRpt, true>(p, flush, s);
+    return;
+  }
   if (kernel == 3) {
-    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 8);
-    if (rpt >= 8) launch_lazy_pass3<T, 8>(p, flush, s);
-    else if (rpt >= 4) launch_lazy_pass3<T, 4>(p, flush, s);
-    else launch_lazy_pass3<T, 2>(p, flush, s);
+    static const int rpt = env_int("RPLU_LAZY_RPT", kDefRpt);
+    if (rpt >= 8) launch_lazy_pass3<T, 8, false>(p, flush, s);
+    else if (rpt >= 4) launch_lazy_pass3<T, 4, false>(p, flush, s);
+    else launch_lazy_pass3<T, 2, false>(p, flush, s);
     return;
   }
   if (kernel == 1) {
@@ -1021,10 +1036,14 @@ static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
 // the per-step minimum on B200 is at 5 (fp64; measured 1.25 / 1.23 / 1.26 /
 // 1.38 ms for q = 1..4, 2.7 ms for a flush), overridable with
 // RPLU_LAZY_BLOCK.
+// Fused terms (one FMA per term) halve the FP64 work of a pending term, so
+// the pass stays HBM-bound to about twice the q and the flush is amortised
+// over a longer block.
 template <typename T>
-static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 4 : 5);  // fp32: 1064 steps/s at 4
-  int b = env_int("RPLU_LAZY_BLOCK", dflt);
+static int lazy_block(bool fused) {
+  const int dflt = fused ? (sizeof(T) == 16 ? 4 : (sizeof(T) == 4 ? 8 : 9))
+                         : (sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 4 : 5));  // fp32: 1064 steps/s at 4
+  int b = env_int(fused ? "RPLU_LAZY_BLOCK_FUSED" : "RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
 
@@ -1033,7 +1052,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
                            long long* launches) {
   DenseParams p = base;
   p.lazy = 1;
-  const int block = lazy_block<T>();
+  const int block = lazy_block<T>(p.fused != 0);
   sweep<T>(p, false, false, s);  // K1: masses of A
   RPLU_CUDA(cudaGetLastError());
   long long nl = 1;
@@ -1071,7 +1090,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
 // the pending steps t0..done-1 (no-op when the loop ran to the end).
 template <typename T>
 static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_t s) {
-  const long long block = lazy_block<T>();
+  const long long block = lazy_block<T>(base.fused != 0);
   const long long t0 = (done / block) * block;
   if (done <= t0 || done >= base.steps) return RPLU_OK;
   DenseParams p = base;
@@ -1122,6 +1141,8 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
   p.stop_tol = a->stop_tol;
   p.rule = a->rule;
+  static const int fused_env = env_int("RPLU_FUSED", -1);
+  p.fused = ((a->flags & RPLU_FLAG_FUSED) != 0 || fused_env == 1) ? 1 : 0;
 
   LoopTiming tm;
   tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
@@ -1182,10 +1203,7 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     if (rc) return rc;
     RPLU_CUDA(cudaStreamSynchronize(s));
   }
-  out->lazy_block = lazy ? (a->dtype == RPLU_F64 ? lazy_block<double>()
-                                                 : (a->dtype == RPLU_F32 ? lazy_block<float>()
-                                                                         : lazy_block<double2>()))
-                         : 0;
+  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype, p.fused != 0) : 0;
   out->sweep_bytes = 0.0;
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,
@@ -1337,6 +1355,53 @@ int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long 
   }
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
+}
+
+template <typename T>
+static void lazy_step_t(const DenseParams& p, bool pivcol, bool flush, cudaStream_t s) {
+  if (pivcol) {
+    const int blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
+    lazy_pivcol_kernel<T><<<blocks, 256, 0, s>>>(p);
+  }
+  lazy_pass<T>(p, flush, s);
+}
+
+int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
+                           void* U, long long ldu, double* masses, DevState* st, long long t,
+                           long long t0, bool pivcol, bool flush, bool force, bool fused,
+                           cudaStream_t s) {
+  if (n == 0) return RPLU_OK;
+  DenseParams p{};
+  p.R = R;
+  p.ld = ld;
+  p.n = n;
+  p.m = m;
+  p.Lt = Lt;
+  p.U = U;
+  p.ldu = ldu;
+  p.masses = masses;
+  p.st = st;
+  p.t = t;
+  p.t0 = t0;
+  p.lazy = 1;
+  p.force = force ? 1 : 0;
+  p.fused = fused ? 1 : 0;
+  switch (dtype) {
+    case RPLU_F64: lazy_step_t<double>(p, pivcol, flush, s); break;
+    case RPLU_F32: lazy_step_t<float>(p, pivcol, flush, s); break;
+    case RPLU_C128: lazy_step_t<double2>(p, pivcol, flush, s); break;
+    default: set_error("unknown dtype"); return RPLU_ERR_ARG;
+  }
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int dense_lazy_block_default(int dtype, bool fused) {
+  switch (dtype) {
+    case RPLU_F64: return lazy_block<double>(fused);
+    case RPLU_F32: return lazy_block<float>(fused);
+    default: return lazy_block<double2>(fused);
+  }
 }
 
 }  // namespace rplu

@@ -68,8 +68,12 @@ struct ShardParams {
   double* resid;
   long long* pivots;
   double stop_tol;
+  void* Lt;        // [steps][n_local] local L columns
+  int lazy_block;  // 0: eager; > 0: delayed-update block (host step loop)
+  bool fused;      // delayed-update terms as one FMA (RPLU_FLAG_FUSED)
 };
 int shard_select_impl(const ShardParams& p, cudaStream_t s);
+int shard_lazy_select_impl(const ShardParams& p, cudaStream_t s);
 int shard_post_impl(const ShardParams& p, cudaStream_t s);
 int shard_total_impl(const double* masses, long long n, double* out, DevState* advance,
                      cudaStream_t s);
@@ -79,6 +83,26 @@ int shard_total_impl(const double* masses, long long n, double* out, DevState* a
 int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                        void* U, long long ldu, double* masses, DevState* st, long long t,
                        bool update, cudaStream_t s);
+
+constexpr int kLazyMaxBlock = 12;  // longest delayed-update block
+
+// Delayed-update pieces on a row block, from dense.cu: (pivcol) the pivot
+// column L[:,t] rebuilt from R^(t0) and the pending terms, then the pass
+// (masses of R^(t+1); flush writes it).  force runs the pass after a stop.
+int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
+                           void* U, long long ldu, double* masses, DevState* st, long long t,
+                           long long t0, bool pivcol, bool flush, bool force, bool fused,
+                           cudaStream_t s);
+int dense_lazy_block_default(int dtype, bool fused);
+
+// Sharded Cauchy-like steps (cauchy.cu).
+int cauchy_shard_begin_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* stats);
+int cauchy_shard_select_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, long long t,
+                             const double* totals, void* msg);
+int cauchy_shard_update_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, long long t,
+                             const void* msg, double* stats);
+int cauchy_shard_finish_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, rplu_cauchy_out* out);
+int cauchy_shard_active_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int* active);
 
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);

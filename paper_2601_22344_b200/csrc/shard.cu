@@ -156,6 +156,168 @@ __global__ void __launch_bounds__(1024) shard_select_kernel(ShardParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Delayed-update shards (lazy_block > 0): the local rows keep R^(t0) of the
+// last flush; the owner's pivot row is rebuilt on the fly (grid kernel), the
+// local pivot column and masses come from the dense lazy kernels.
+//   lazy select-row (1 CTA): global owner + local row draw (owner); header
+//                             i_global (owner) or -0.0
+//   lazy row (grid):          msg pivot row = R^(t0)[i,:] - pending (owner)
+//                             or -0.0
+//   lazy select-col (1 CTA):  owner's column draw over the message row
+template <typename T>
+__global__ void __launch_bounds__(1024) shard_lazy_select_row_kernel(ShardParams p) {
+  constexpr int B = 1024;
+  DevState* st = p.st;
+  __shared__ CdfSmem<B> sm;
+  __shared__ int s_owner, s_stop;
+  __shared__ double s_target;
+  double* hdr = reinterpret_cast<double*>(p.msg);
+  if (!st->active) {
+    if (threadIdx.x < 4) hdr[threadIdx.x] = -0.0;
+    if (threadIdx.x == 0) st->aux[0] = 0.0;  // not the owner
+    return;
+  }
+  const long long t = shard_step(p);
+  if (threadIdx.x == 0) {
+    double T_all = 0.0;
+    for (int s = 0; s < p.world; ++s) T_all += p.totals[s];
+    const double resid = sqrt(T_all);
+    p.resid[t] = resid;
+    if (t == 0) st->fro0 = resid;
+    const double fro0 = (t == 0) ? resid : st->fro0;
+    int stop = 0;
+    if (t > 0 && p.stop_tol > 0.0 && resid <= p.stop_tol * fro0) {
+      st->status = kTolStop;
+      stop = 1;
+    } else if (t >= p.steps) {
+      stop = 1;
+    } else if (resid == 0.0) {
+      st->status = kCleanStop;
+      stop = 1;
+    } else if (st->ucount + 2 > p.n_uniforms) {
+      st->status = kUniformsExhausted;
+      stop = 1;
+    }
+    int owner = -1;
+    double target = 0.0;
+    if (!stop) {
+      const double tg = p.uniforms[st->ucount] * T_all;
+      double c = 0.0;
+      int last_pos = -1;
+      for (int s = 0; s < p.world; ++s) {
+        if (p.totals[s] > 0.0) last_pos = s;
+        const double c2 = c + p.totals[s];
+        if (owner < 0 && c2 > tg && p.totals[s] > 0.0) {
+          owner = s;
+          target = tg - c;
+        }
+        c = c2;
+      }
+      if (owner < 0) {
+        owner = last_pos;
+        target = p.totals[owner];
+      }
+      const double tol = kNearBoundaryRel * T_all;
+      double cb = 0.0;
+      for (int s = 0; s <= owner; ++s) {
+        if (fabs(cb - tg) <= tol) st->near_boundary++;
+        cb += p.totals[s];
+      }
+      st->ucount += 2;  // u1 now, u2 by the column draw (at ucount - 1)
+    }
+    if (stop) st->active = 0;
+    st->aux[0] = (!stop && owner == p.rank) ? 1.0 : 0.0;
+    s_stop = stop;
+    s_owner = owner;
+    s_target = target;
+  }
+  __syncthreads();
+  if (s_stop || s_owner != p.rank) {
+    if (threadIdx.x < 4) hdr[threadIdx.x] = -0.0;
+    return;
+  }
+  const double* masses = p.masses;
+  auto wrow = [&](long long k) { return masses[k]; };
+  Cdf<B> cr = cdf_build<B>(wrow, p.n_local, sm);
+  const long long i = cdf_find_target<B>(wrow, p.n_local, cr, s_target, sm);
+  if (threadIdx.x == 0) {
+    st->pi = i;  // local row (the header carries the global index)
+    hdr[0] = (double)(p.row_offset + i);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) shard_lazy_row_kernel(ShardParams p) {
+  using S = Scalar<T>;
+  const DevState* st = p.st;
+  T* prow = reinterpret_cast<T*>(reinterpret_cast<double*>(p.msg) + 4);
+  const bool owner = st->active && st->aux[0] != 0.0;
+  const long long t = shard_step(p);
+  const long long t0 = (t / p.lazy_block) * p.lazy_block;
+  const int q = (int)(t - t0);
+  const long long i = owner ? st->pi : 0;
+  const T* R = reinterpret_cast<const T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const T* U = reinterpret_cast<const T*>(p.U) + t0 * p.ldu;
+  __shared__ T s_l[kLazyMaxBlock];
+  if (owner && (int)threadIdx.x < q) s_l[threadIdx.x] = Lt[(t0 + threadIdx.x) * p.n_local + i];
+  __syncthreads();
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
+       k += (long long)gridDim.x * blockDim.x) {
+    if (!owner) {
+      prow[k] = neg_zero<T>();
+      continue;
+    }
+    T x = R[i * p.ld + k];
+    for (int s = 0; s < q; ++s) x = pend_sub(p.fused, x, s_l[s], U[s * p.ldu + k]);
+    prow[k] = x;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) shard_lazy_select_col_kernel(ShardParams p) {
+  using S = Scalar<T>;
+  constexpr int B = 1024;
+  DevState* st = p.st;
+  if (!st->active || st->aux[0] == 0.0) return;  // owner only
+  __shared__ CdfSmem<B> sm;
+  double* hdr = reinterpret_cast<double*>(p.msg);
+  const T* prow = reinterpret_cast<const T*>(hdr + 4);
+  const double u2 = p.uniforms[st->ucount - 1];
+  auto wcol = [&](long long k) { return S::weight(prow[k]); };
+  Cdf<B> cc = cdf_build<B>(wcol, p.m, sm);
+  const long long j = cdf_find<B>(wcol, p.m, cc, u2, sm);
+  if (threadIdx.x == 0) {
+    const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+    if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) st->near_boundary++;
+    const double2 a = to_pair<T>(prow[j]);
+    hdr[1] = (double)j;
+    hdr[2] = a.x;
+    hdr[3] = a.y;
+  }
+}
+
+template <typename T>
+static int shard_lazy_select_t(const ShardParams& p, cudaStream_t s) {
+  shard_lazy_select_row_kernel<T><<<1, 1024, 0, s>>>(p);
+  const int blocks = (int)std::min<long long>((p.m + 255) / 256, 1024);
+  shard_lazy_row_kernel<T><<<blocks, 256, 0, s>>>(p);
+  shard_lazy_select_col_kernel<T><<<1, 1024, 0, s>>>(p);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int shard_lazy_select_impl(const ShardParams& p, cudaStream_t s) {
+  switch (p.dtype) {
+    case RPLU_F64: return shard_lazy_select_t<double>(p, s);
+    case RPLU_F32: return shard_lazy_select_t<float>(p, s);
+    case RPLU_C128: return shard_lazy_select_t<double2>(p, s);
+  }
+  set_error("unknown dtype");
+  return RPLU_ERR_ARG;
+}
+
 // After the allreduce: every rank posts the pivot into its state (CTA 0,
 // thread 0) and copies the reduced pivot row into U[t,:] (all CTAs).
 template <typename T>

@@ -36,7 +36,8 @@ from .dense_pivots import EliminationTrace, PivotRule
 from .rng import UniformBlock
 
 __all__ = ["shard_rows", "run_sharded", "run_sharded_graph", "sharded_eliminate",
-           "CudaShardBackend"]
+           "CudaShardBackend", "run_sharded_cauchy", "CudaCauchyShardBackend",
+           "sharded_structured_eliminate"]
 
 
 def shard_rows(n, world, rank):
@@ -121,7 +122,8 @@ def run_sharded_graph(backend, steps, group=None, chunk=32):
 class CudaShardBackend:
     """Product backend: the rplu_shard_* C ABI on this rank's GPU."""
 
-    def __init__(self, R, row_offset, world, rank, rule, steps, stop_tol=0.0, ctx=None):
+    def __init__(self, R, row_offset, world, rank, rule, steps, stop_tol=0.0, ctx=None,
+                 lazy_block=0):
         if rule.tag != "rplu":
             raise CapabilityError("the sharded path implements rule 'rplu'")
         self.dev = R.device
@@ -148,7 +150,7 @@ class CudaShardBackend:
             ld=R.stride(0), row_offset=row_offset, steps=steps, stop_tol=float(stop_tol),
             R=R.data_ptr() if n_local else None, Lt=self.Lt.data_ptr(), U=self.U.data_ptr(),
             ldu=self.ldu, uniforms=self.block.pointer(), n_uniforms=self.block.values.size,
-            stream=None)
+            stream=None, lazy_block=int(lazy_block))
         c = ctx if ctx is not None else _device.ctx(self.dev)
         self._ctx = c
         self._lib, self._h = c._lib, c.handle
@@ -189,6 +191,7 @@ class CudaShardBackend:
         self.block.commit(out.uniforms_consumed)
         _ffi.check(status)
         k = int(out.steps_done)
+        self.lazy_block_used = int(out.lazy_block)
         return dict(pivots=[(int(self.pivots[2 * t]), int(self.pivots[2 * t + 1]))
                             for t in range(k)],
                     resid_fro=self.resid[:k + 1].copy(), steps=k,
@@ -199,7 +202,8 @@ class CudaShardBackend:
 
 
 def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None,
-                      compute_dtype=None, overwrite_a=False, step_hook=None, graph=False):
+                      compute_dtype=None, overwrite_a=False, step_hook=None, graph=False,
+                      update="auto", lazy_block=None):
     """RPLU on a row-block shard (call on every rank with the same rule seed).
 
     ``A_local`` is this rank's contiguous row block (global rows
@@ -207,7 +211,15 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
     ``steps``/``stop_tol`` and an RngState with the same seed.  Returns an
     EliminationTrace whose L holds this rank's rows of L (device tensor) and
     whose U / pivots / resid_fro are the global (replicated) values.
+
+    ``update``: "eager" (fused K3 update every step; the only mode a CUDA
+    graph can replay), "lazy" (delayed updates: one read of the row block per
+    step, a write every ``lazy_block`` steps; host step loop), or "auto"
+    (lazy when not graphing and the local block exceeds 256 MB, as on one
+    GPU).  Results are bit-identical across modes.
     """
+    if update not in ("auto", "eager", "lazy"):
+        raise ValueError(f"update must be 'auto', 'eager' or 'lazy', not {update!r}")
     if isinstance(rule, str):
         rule = PivotRule(rule)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -217,9 +229,15 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
     if (overwrite_a or src is not A_local) and src.is_contiguous() and src.shape[1] % vec == 0:
         R = src
     else:
-        R = _device.padded_residual(src)[0]
+        R = _device.padded_residual(src)[1]   # (n_local, m) view, 16-byte rows
     n_local, m = src.shape
-    backend = CudaShardBackend(R, row_offset, world, rank, rule, steps, stop_tol)
+    if update == "auto":
+        big = n_local * m * R.element_size() > 256e6
+        update = "lazy" if big and not graph and steps >= 2 else "eager"
+    if update == "lazy" and graph:
+        raise ValueError("the delayed-update shard loop runs on the host (graph=False)")
+    lb = 0 if update == "eager" else (-1 if lazy_block is None else int(lazy_block))
+    backend = CudaShardBackend(R, row_offset, world, rank, rule, steps, stop_tol, lazy_block=lb)
     if graph and step_hook is None:
         res = run_sharded_graph(backend, steps, group=group)
     else:
@@ -229,6 +247,162 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
         residual=R[:, :m], steps=res["steps"], clean_early_stop=res["clean_early_stop"],
         tol_stop=res["tol_stop"], near_boundary_draws=res["near_boundary_draws"],
         uniforms_consumed=res["uniforms_consumed"], host=False)
+    tr.lazy_block = backend.lazy_block_used   # 0: eager updates
+    return tr
+
+
+# ---------------------------------------------------------------------------
+# Cauchy-like (C4): x / G row blocks, y / B replicated.
+
+def _all_gather_vec(x, group, world):
+    if not dist.is_initialized():
+        return x.reshape(-1)
+    out = torch.empty(world * x.numel(), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(out, x.reshape(-1), group=group)
+    return out
+
+
+def run_sharded_cauchy(backend, steps, group=None, poll_every=16):
+    """Per step: select (global stats, owner, pivot message), one
+    sum-allreduce of the 20-double message (i, x_i, G_i; -0.0 from
+    non-owners), update (pivot row regenerated on every rank, same column
+    draw, local G rows + replicated B, local K5 masses), allgather of the
+    [sum, max] row-mass stats."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    stats = backend.begin()
+    totals = _all_gather_vec(stats, group, world)
+    for t in range(steps):
+        msg = backend.select(t, totals)
+        if dist.is_initialized():
+            dist.all_reduce(msg, op=dist.ReduceOp.SUM, group=group)
+        stats = backend.update(t, msg)
+        if t + 1 < steps:
+            totals = _all_gather_vec(stats, group, world)
+        if poll_every and (t + 1) % poll_every == 0 and not backend.active():
+            break
+    return backend.finish()
+
+
+class CudaCauchyShardBackend:
+    """Product backend: the rplu_cauchy_shard_* C ABI on this rank's GPU.
+    M_local is a CauchyLikeMatrix holding this rank's rows of x / G and the
+    full y / B (updated in place)."""
+
+    def __init__(self, M_local, row_offset, world, rank, rule, rng, steps, stop_tol=0.0,
+                 keep_steps=False, ctx=None):
+        from .cauchy import CauchyLikeMatrix  # noqa: F401  (type of M_local)
+        self.M = M_local
+        self.dev = M_local.device
+        n_local, m = M_local.shape
+        self.steps = steps
+        self.C = self.R = self.A = None
+        if keep_steps and steps > 0:
+            self.C = torch.empty((steps, max(n_local, 1)), dtype=torch.complex128, device=self.dev)
+            self.R = torch.empty((steps, m), dtype=torch.complex128, device=self.dev)
+            self.A = torch.empty(steps, dtype=torch.complex128, device=self.dev)
+        self.block = UniformBlock(rng, 3 * steps + 2) if rule == "rplu" else None
+        self.msg = torch.empty(_ffi.CAUCHY_MSG_DOUBLES, dtype=torch.float64, device=self.dev)
+        self.stats = torch.empty(2, dtype=torch.float64, device=self.dev)
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        self.args = _ffi.CauchyShardArgs(
+            rule=_ffi.RULE_IDS[rule], p=M_local.displacement_rank, world=world, rank=rank,
+            n_local=n_local, m=m, row_offset=row_offset, steps=steps, stop_tol=float(stop_tol),
+            x=M_local.x.data_ptr() if n_local else None, y=M_local.y.data_ptr(),
+            G=M_local.G.data_ptr() if n_local else None, Bt=M_local.Bt.data_ptr(),
+            C=ptr(self.C), Rrow=ptr(self.R), a=ptr(self.A),
+            uniforms=self.block.pointer() if self.block else None,
+            n_uniforms=self.block.values.size if self.block else 0, stream=None)
+        c = ctx if ctx is not None else _device.ctx(self.dev)
+        self._ctx = c
+        self._lib, self._h = c._lib, c.handle
+        k = max(steps, 1)
+        self.rows = np.zeros(k, dtype=np.int64)
+        self.cols = np.zeros(k, dtype=np.int64)
+        self.bmax = np.zeros(k)
+        self.bsum = np.zeros(k)
+
+    def _args(self):
+        self.args.stream = torch.cuda.current_stream(self.dev).cuda_stream
+        return ctypes.byref(self.args)
+
+    def begin(self):
+        _ffi.check(self._lib.rplu_cauchy_shard_begin(self._h, self._args(),
+                                                     self.stats.data_ptr()))
+        return self.stats
+
+    def select(self, t, totals):
+        totals = totals.contiguous()
+        self._totals = totals
+        _ffi.check(self._lib.rplu_cauchy_shard_select(self._h, self._args(), t,
+                                                      totals.data_ptr(), self.msg.data_ptr()))
+        return self.msg
+
+    def update(self, t, msg):
+        _ffi.check(self._lib.rplu_cauchy_shard_update(self._h, self._args(), t, msg.data_ptr(),
+                                                      self.stats.data_ptr()))
+        return self.stats
+
+    def active(self):
+        a = ctypes.c_int32(0)
+        _ffi.check(self._lib.rplu_cauchy_shard_active(self._h, self._args(), ctypes.byref(a)))
+        return bool(a.value)
+
+    def finish(self):
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        f64p = ctypes.POINTER(ctypes.c_double)
+        out = _ffi.CauchyOut(rows=self.rows.ctypes.data_as(i64p),
+                             cols=self.cols.ctypes.data_as(i64p),
+                             bound_maxes=self.bmax.ctypes.data_as(f64p),
+                             bound_sums=self.bsum.ctypes.data_as(f64p))
+        status = self._lib.rplu_cauchy_shard_finish(self._h, self._args(), ctypes.byref(out))
+        if self.block is not None:
+            self.block.commit(out.uniforms_consumed)
+        _ffi.check(status)
+        return out
+
+
+def sharded_structured_eliminate(M_local, row_offset, rule, rank, stop_tol=0.0, rng=None,
+                                 keep_steps=False, group=None):
+    """Exact-norm structured RPLU (cauchy.py:177-256, plan=None) on a row
+    shard: call on every rank with this rank's rows of x / G (M_local, a
+    CauchyLikeMatrix whose y / B are the full, replicated generators) and an
+    RngState with the same seed.  Returns a StructuredPivotTrace with GLOBAL
+    row indices, the global bound statistics, ``residual`` = M_local after
+    the updates (local G rows, replicated B), and with keep_steps the LOCAL
+    rows of each column c (``steps_device`` = (C_local, R, a)).
+    """
+    from .cauchy import CauchyLikeMatrix, StructuredPivotTrace
+    if rule not in ("rplu", "c2plu"):
+        raise ValueError(f"unknown structured rule {rule!r}")
+    if rule == "rplu" and rng is None:
+        raise ValueError("structured rplu needs an RngState")
+    if not isinstance(M_local, CauchyLikeMatrix):
+        raise CapabilityError("sharded_structured_eliminate needs a CauchyLikeMatrix")
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank_id = dist.get_rank(group) if dist.is_initialized() else 0
+    n_local, m = M_local.shape
+    n_global = n_local
+    if dist.is_initialized():
+        nt = torch.tensor([n_local], dtype=torch.int64,
+                          device=M_local.device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(nt, group=group)
+        n_global = int(nt.item())
+    if not 0 <= rank <= min(n_global, m):
+        raise ValueError(f"rank {rank} out of range [0, {min(n_global, m)}]")
+    if rank == 0:
+        return StructuredPivotTrace(residual=M_local)
+    be = CudaCauchyShardBackend(M_local, row_offset, world, rank_id, rule, rng, rank,
+                                stop_tol=stop_tol, keep_steps=keep_steps)
+    out = run_sharded_cauchy(be, rank, group=group)
+    k, nb = int(out.steps_done), int(out.bounds_recorded)
+    tr = StructuredPivotTrace(
+        row_indices=[int(v) for v in be.rows[:k]], col_indices=[int(v) for v in be.cols[:k]],
+        bound_sums=[float(v) for v in be.bsum[:nb]], bound_maxes=[float(v) for v in be.bmax[:nb]],
+        tol_stop=bool(out.tol_stop), degenerate_stop=bool(out.degenerate_stop),
+        near_boundary_draws=int(out.near_boundary_draws),
+        uniforms_consumed=int(out.uniforms_consumed), residual=M_local)
+    if be.C is not None:
+        tr.steps_device = (be.C[:, :n_local], be.R, be.A)
     return tr
 
 
@@ -260,12 +434,19 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
         e.record()
         sweep_ev.append(e)
 
-    use_graph = os.environ.get("RPLU_SHARD_GRAPH", "1") == "1"
+    # RPLU_SHARD_UPDATE=lazy (default: delayed updates, host step loop) or
+    # eager (fused K3 update; one step captured in a CUDA graph and replayed
+    # unless RPLU_SHARD_GRAPH=0)
+    mode = os.environ.get("RPLU_SHARD_UPDATE", "lazy")
+    use_graph = mode == "eager" and os.environ.get("RPLU_SHARD_GRAPH", "1") == "1"
+    lazy_used = [0]
 
     def one(timed=False):
-        return sharded_eliminate(A_loc, lo, PivotRule("rplu", _rng(seed)), k,
-                                 compute_dtype=tdtype, step_hook=hook if timed else None,
-                                 graph=use_graph and not timed)
+        tr = sharded_eliminate(A_loc, lo, PivotRule("rplu", _rng(seed)), k,
+                               compute_dtype=tdtype, step_hook=hook if timed else None,
+                               graph=use_graph and not timed, update=mode)
+        lazy_used[0] = tr.lazy_block
+        return tr
 
     for _ in range(args.warmup):
         one()
@@ -305,7 +486,15 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
     torch.cuda.synchronize()
     ems = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     dist_mod.all_reduce(ems, op=dist_mod.ReduceOp.MAX)
-    bytes_launch = 2.0 * (hi - lo) * n * esize
+    # algorithmic bytes per update: read + write of the row block (eager, or
+    # a lazy flush), a read (lazy pass); averaged over the k steps
+    b = lazy_used[0]
+    blk = (hi - lo) * n * esize
+    if b > 0:
+        nflush = sum(1 for t in range(k) if (t + 1) % b == 0 or t == k - 1)
+        bytes_launch = blk * (k + nflush) / k
+    else:
+        bytes_launch = 2.0 * blk
     achieved = bytes_launch / (float(upd_t) / 1e3) / 1e9
     peak = 6553.6
     try:
@@ -324,17 +513,20 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
             "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": k, "seed": seed,
                        "parallelism": f"row-block shards x{world} (NCCL allgather + allreduce)",
                        "step_loop": "CUDA graph of one step replayed" if use_graph else "host loop",
+                       "update": f"delayed (flush every {b} steps)" if b else "eager (K3)",
                        "step": f"one full elimination of {k} pivot steps",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "shard update (post + K3 sweep + local total), per rank, max over ranks",
+                         "kernel": ("shard update (post + pivot column + delayed-update pass + local total)"
+                                    if b else "shard update (post + K3 sweep + local total)")
+                                   + ", per rank, max over ranks",
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "avg_launch_ms": float(upd_t)},
             "e2e": {"value": trh.steps / (float(ems) / 1e3), "unit": unit,
                     "h2d_bytes_per_step": (hi - lo) * n * esize * world,
                     "d2h_bytes_per_step": (Lh.numel() + Uh.numel()) * esize},
-            "gpu_launches": args.steps * (3 * k + 3) * 1,
+            "gpu_launches": args.steps * (((6 if b else 3) * k) + 3),
             "near_boundary_draws": tr.near_boundary_draws,
         }
         print(json.dumps(line), flush=True)

@@ -1,4 +1,4 @@
-"""C3 fp64 delayed-update run of 12 steps (flush every 10): for ncu of lazy_pass_kernel."""
+"""C3 fp64 delayed-update run of 12 steps (default flush interval): for ncu of the lazy pass."""
 import os
 import sys
 

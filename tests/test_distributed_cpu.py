@@ -28,7 +28,27 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, A, seed, steps, stop_tol, out_q):
+def _collect(q, procs, world, key, timeout=180):
+    """Results of all workers; fails as soon as one exits non-zero."""
+    import queue
+    import time
+    outs, t0 = [], time.time()
+    while len(outs) < world:
+        try:
+            outs.append(q.get(timeout=1.0))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.time() - t0 > timeout:
+                for p in procs:
+                    p.kill()
+                pytest.fail(f"shard worker failed (exit codes {dead})")
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(outs, key=key)
+
+
+def _worker(rank, world, port, A, seed, steps, stop_tol, lazy_block, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -37,27 +57,25 @@ def _worker(rank, world, port, A, seed, steps, stop_tol, out_q):
 
         from paper_2601_22344_b200.distributed import run_sharded, shard_rows
         lo, hi = shard_rows(A.shape[0], world, rank)
-        be = NumpyShardBackend(A[lo:hi], lo, world, rank, seed, steps, stop_tol)
+        be = NumpyShardBackend(A[lo:hi], lo, world, rank, seed, steps, stop_tol,
+                               lazy_block=lazy_block)
         res = run_sharded(be, steps, poll_every=4)
         out_q.put((rank, lo, hi, res["pivots"], res["resid_fro"], res["L_local"], res["U"],
-                   res["status"]))
+                   res["status"], res["residual"]))
     finally:
         dist.destroy_process_group()
 
 
-def _run(A, seed, steps, world=2, stop_tol=0.0):
+def _run(A, seed, steps, world=2, stop_tol=0.0, lazy_block=0):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, A, seed, steps, stop_tol, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, A, seed, steps, stop_tol,
+                                                   lazy_block, q))
              for r in range(world)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=120) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    return sorted(outs)
+    return _collect(q, procs, world, key=lambda o: o[:3])
 
 
 def test_shard_rows_partition():
@@ -71,13 +89,13 @@ def test_shard_rows_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_matches_single_process(world):
+@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 3), (3, 5)])
+def test_sharded_matches_single_process(world, lazy_block):
     import oracle
     from paper_2601_22344_b200 import gen
     A = gen.c1_dense(4, n=90, m=70)
     steps = 40
-    outs = _run(A, seed=4, steps=steps, world=world)
+    outs = _run(A, seed=4, steps=steps, world=world, lazy_block=lazy_block)
     ref = oracle.eliminate_real(A, "rplu", steps, seed=4, margins=True)
     pivots = outs[0][3]
     for o in outs:
@@ -92,18 +110,25 @@ def test_sharded_matches_single_process(world):
     for o in outs:
         np.testing.assert_array_equal(o[6], ref["U"])
     np.testing.assert_allclose(outs[0][4], ref["resid_fro"], rtol=1e-12)
+    np.testing.assert_array_equal(np.concatenate([o[8] for o in outs], axis=0), ref["residual"])
 
 
-def test_sharded_tol_stop_is_global():
+@pytest.mark.parametrize("lazy_block", [0, 5])
+def test_sharded_tol_stop_is_global(lazy_block):
+    """Every rank stops at the same step; with delayed updates finish applies
+    the pending steps, so the residual equals the eager one."""
     import oracle
     from paper_2601_22344_b200 import gen
     A = gen.c1_dense(3, n=64)
-    outs = _run(A, seed=3, steps=60, stop_tol=0.3)
+    outs = _run(A, seed=3, steps=60, stop_tol=0.3, lazy_block=lazy_block)
     ref = oracle.eliminate_real(A, "rplu", 60, seed=3, stop_tol=0.3)
     assert ref["tol_stop"]
+    assert ref["steps"] % 5 != 0   # the stop leaves pending steps
     for o in outs:
         assert o[7] == "tol"
         assert len(o[3]) == ref["steps"]
+    if outs[0][3] == ref["pivots"]:
+        np.testing.assert_array_equal(np.concatenate([o[8] for o in outs], axis=0), ref["residual"])
 
 
 def test_negative_zero_allreduce_is_exact():
@@ -111,3 +136,62 @@ def test_negative_zero_allreduce_is_exact():
     x = np.array([-0.0, 0.0, 5e-324, -5e-324, 1.0, -3.5, np.finfo(float).max])
     y = x + (-0.0)
     assert np.array_equal(x.view(np.int64), y.view(np.int64))
+
+
+def _cauchy_worker(rank, world, port, x, y, G, B, rule, seed, steps, stop_tol, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_cpu_backend import NumpyCauchyShardBackend
+
+        from paper_2601_22344_b200.distributed import run_sharded_cauchy, shard_rows
+        lo, hi = shard_rows(x.size, world, rank)
+        be = NumpyCauchyShardBackend(x[lo:hi], y, G[lo:hi], B, lo, world, rank, rule, seed,
+                                     steps, stop_tol)
+        res = run_sharded_cauchy(be, steps, poll_every=4)
+        out_q.put((rank, res["rows"], res["cols"], res["bound_maxes"], res["bound_sums"],
+                   res["status"], res["G"], res["B"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_cauchy(x, y, G, B, rule, seed, steps, world=2, stop_tol=0.0):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cauchy_worker,
+                         args=(r, world, port, x, y, G, B, rule, seed, steps, stop_tol, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    return _collect(q, procs, world, key=lambda o: o[0])
+
+
+@pytest.mark.parametrize("world,rule,stop_tol", [(2, "rplu", 0.0), (3, "rplu", 1e-3),
+                                                 (2, "c2plu", 0.0)])
+def test_sharded_cauchy_matches_single_process(world, rule, stop_tol):
+    """Row-sharded Cauchy-like elimination (x / G sharded, y / B replicated)
+    reproduces the single-process oracle: pivots, bound statistics, and the
+    generators after the updates."""
+    import oracle
+    from paper_2601_22344_b200 import gen
+    x, y, G, B = gen.c4_cauchy_like(5, n=150, m=130, p=3)
+    steps = 80 if stop_tol else 40     # the tol case stops at step 70
+    outs = _run_cauchy(x, y, G, B, rule, 5, steps, world=world, stop_tol=stop_tol)
+    ref = oracle.structured_eliminate(x, y, G, B, rule, steps, seed=5, stop_tol=stop_tol)
+    for o in outs:
+        assert o[1] == outs[0][1] and o[2] == outs[0][2], "ranks disagree on the pivots"
+    assert outs[0][1] == ref["row_indices"]
+    assert outs[0][2] == ref["col_indices"]
+    np.testing.assert_allclose(outs[0][3], ref["bound_maxes"], rtol=1e-12)
+    np.testing.assert_allclose(outs[0][4], ref["bound_sums"], rtol=1e-12)
+    if stop_tol:
+        assert outs[0][5] == "tol" and ref["tol_stop"]
+    # (BLAS blocks a row-block matvec differently from the full one: the
+    # generators agree to rounding, the pivots and bounds exactly / 1e-12)
+    Gs = np.concatenate([o[6] for o in outs], axis=0)
+    np.testing.assert_allclose(Gs, ref["G"], rtol=1e-10, atol=1e-13 * np.abs(ref["G"]).max())
+    for o in outs:
+        np.testing.assert_allclose(o[7], ref["B"], rtol=1e-10,
+                                   atol=1e-13 * np.abs(ref["B"]).max())

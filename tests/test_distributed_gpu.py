@@ -43,8 +43,44 @@ def test_world1_graph_replay_equals_eliminate(cuda_device):
     assert trs.tol_stop and refs.tol_stop and trs.pivots == refs.pivots
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_emulated_shards(world, cuda_device):
+@pytest.mark.parametrize("dtype,lazy_block", [(torch.float64, 3), (torch.float64, -1),
+                                              (torch.float32, 4), (torch.complex128, 2)])
+def test_world1_lazy_equals_eager(dtype, lazy_block, cuda_device):
+    """Delayed-update shard loop: pivots, L, U and the final residual are
+    bit-identical to the single-GPU eager loop (also after a tol stop that
+    leaves pending steps for finish to apply)."""
+    A = gen.c1_dense(7, n=410, m=301)
+    if dtype == torch.complex128:
+        A = A + 1j * gen.c1_dense(8, n=410, m=301)
+    A = torch.from_numpy(A).to("cuda", dtype)
+    for steps, tol in ((101, 0.0), (250, 0.45)):
+        tr = sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(7)), steps,
+                               stop_tol=tol, update="lazy", lazy_block=lazy_block)
+        ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(7)), steps, stop_tol=tol,
+                           update="eager")
+        assert tr.lazy_block > 0
+        assert tr.pivots == ref.pivots and tr.tol_stop == ref.tol_stop
+        if tol:
+            assert tr.tol_stop
+        assert torch.equal(tr.L, ref.L) and torch.equal(tr.U, ref.U)
+        assert torch.equal(tr.residual_device, ref.residual_device)
+        np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-13)
+
+
+def test_lazy_rejects_graph_and_device_steps(cuda_device):
+    A = torch.from_numpy(gen.c1_dense(2, n=64, m=64)).cuda()
+    with pytest.raises(ValueError):
+        sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(2)), 8, update="lazy",
+                          graph=True)
+    be = CudaShardBackend(A.clone(), 0, 1, 0, rp.PivotRule("rplu", rp.RngState(2)), 8,
+                          lazy_block=3)
+    tot = be.begin().clone()
+    with pytest.raises(Exception):
+        be.select(-1, tot)
+
+
+@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 4), (3, 5)])
+def test_emulated_shards(world, lazy_block, cuda_device):
     A = gen.c1_dense(6, n=500, m=333)
     steps = 120
     seed = 6
@@ -58,9 +94,10 @@ def test_emulated_shards(world, cuda_device):
             buf[:, :R.shape[1]] = R
             R = buf[:, :A.shape[1]]
         bes.append(CudaShardBackend(R, lo, world, r, rp.PivotRule("rplu", rp.RngState(seed)),
-                                    steps, ctx=_ffi.Context(0)))
+                                    steps, ctx=_ffi.Context(0), lazy_block=lazy_block))
     totals = torch.cat([b.begin().clone() for b in bes])
-    device_t = world == 3   # exercise the device step counter (t = -1) too
+    # exercise the device step counter (t = -1) too (eager only)
+    device_t = world == 3 and lazy_block == 0
     for t in range(steps + 1):
         tt = -1 if device_t else t
         ms = [b.select(tt, totals).clone() for b in bes]
@@ -83,3 +120,83 @@ def test_emulated_shards(world, cuda_device):
     np.testing.assert_array_equal(L, ref["L"])
     np.testing.assert_array_equal(res[0]["U"].cpu().numpy(), ref["U"])
     np.testing.assert_allclose(res[0]["resid_fro"], ref["resid_fro"], rtol=1e-12)
+    Rs = torch.cat([b.R for b in bes], dim=0).cpu().numpy()
+    np.testing.assert_array_equal(Rs, ref["residual"])
+
+
+# ---------------------------------------------------------------------------
+# Sharded Cauchy-like (x / G row blocks, y / B replicated)
+
+from paper_2601_22344_b200.distributed import (  # noqa: E402
+    CudaCauchyShardBackend, sharded_structured_eliminate)
+
+
+@pytest.mark.parametrize("rule", ["rplu", "c2plu"])
+def test_cauchy_world1_equals_structured(rule, cuda_device):
+    x, y, G, B = gen.c4_cauchy_like(3, n=700, m=600, p=4)
+    M = rp.CauchyLikeMatrix(x, y, G, B)
+    rng = rp.RngState(3) if rule == "rplu" else None
+    tr = sharded_structured_eliminate(M.copy(), 0, rule, 60, rng=rng, keep_steps=True)
+    rng2 = rp.RngState(3) if rule == "rplu" else None
+    ref = rp.structured_eliminate(M, rule, 60, rng=rng2, keep_steps=True)
+    assert tr.row_indices == ref.row_indices and tr.col_indices == ref.col_indices
+    assert tr.bound_maxes == ref.bound_maxes and tr.bound_sums == ref.bound_sums
+    assert tr.uniforms_consumed == ref.uniforms_consumed
+    assert torch.equal(tr.residual.G, ref.residual.G)
+    assert torch.equal(tr.residual.Bt, ref.residual.Bt)
+    for a, b in zip(tr.steps_device, ref.steps_device):
+        assert torch.equal(a, b)
+    if rng is not None:
+        assert rng.uniform() == rng2.uniform()
+
+
+@pytest.mark.parametrize("world,rule,stop_tol", [(2, "rplu", 0.0), (3, "rplu", 1e-3),
+                                                 (2, "c2plu", 0.0)])
+def test_cauchy_emulated_shards(world, rule, stop_tol, cuda_device):
+    """2 / 3 shards on one GPU (own contexts, sums of the messages in place
+    of the allreduce): pivots and bounds as the oracle, generators to
+    rounding, keep_steps columns of every shard."""
+    x, y, G, B = gen.c4_cauchy_like(5, n=900, m=700, p=3)
+    steps = 100 if stop_tol else 60
+    ref = oracle.structured_eliminate(x, y, G, B, rule, steps, seed=5, stop_tol=stop_tol,
+                                      keep_steps=True, margins=True)
+    bes, blocks = [], []
+    for r in range(world):
+        lo, hi = shard_rows(x.size, world, r)
+        blocks.append((lo, hi))
+        Ml = rp.CauchyLikeMatrix(x[lo:hi], y, G[lo:hi], B, check_points=False)
+        rng = rp.RngState(5) if rule == "rplu" else None
+        bes.append(CudaCauchyShardBackend(Ml, lo, world, r, rule, rng, steps,
+                                          stop_tol=stop_tol, keep_steps=True,
+                                          ctx=_ffi.Context(0)))
+    stats = torch.cat([b.begin().clone() for b in bes])
+    for t in range(steps):
+        ms = [b.select(t, stats).clone() for b in bes]
+        msg = ms[0]
+        for m2 in ms[1:]:
+            msg = msg + m2
+        stats = torch.cat([b.update(t, msg).clone() for b in bes])
+    outs = [b.finish() for b in bes]
+    k = int(outs[0].steps_done)
+    rows = [int(v) for v in bes[0].rows[:k]]
+    cols = [int(v) for v in bes[0].cols[:k]]
+    for b in bes[1:]:
+        assert [int(v) for v in b.rows[:k]] == rows and [int(v) for v in b.cols[:k]] == cols
+    mism = [t for t, (a, c) in enumerate(zip(rows, ref["row_indices"])) if a != c]
+    if mism:
+        assert ref["margins"][mism[0]] <= oracle.NEAR_REL
+        return
+    assert rows == ref["row_indices"] and cols == ref["col_indices"]
+    assert bool(outs[0].tol_stop) == ref["tol_stop"]
+    nb = int(outs[0].bounds_recorded)
+    np.testing.assert_allclose(bes[0].bmax[:nb], ref["bound_maxes"], rtol=1e-11)
+    np.testing.assert_allclose(bes[0].bsum[:nb], ref["bound_sums"], rtol=1e-11)
+    Gs = torch.cat([b.M.G for b in bes]).cpu().numpy()
+    np.testing.assert_allclose(Gs, ref["G"], rtol=1e-9, atol=1e-12 * np.abs(ref["G"]).max())
+    for b in bes:
+        Bt = b.M.Bt.cpu().numpy()
+        np.testing.assert_allclose(Bt.T, ref["B"], rtol=1e-9, atol=1e-12 * np.abs(ref["B"]).max())
+    C = torch.cat([b.C[:k, :hi - lo] for b, (lo, hi) in zip(bes, blocks)], dim=1).cpu().numpy()
+    for t, (c, r, a) in enumerate(ref["steps"]):
+        assert np.abs(C[t] - c).max() <= 1e-10 * np.abs(c).max()
+        assert np.abs(bes[0].R[t].cpu().numpy() - r).max() <= 1e-10 * np.abs(r).max()
