@@ -58,13 +58,6 @@ extern "C" {
 #define RPLU_FLAG_LAZY 4         /* dense: force the delayed-update loop */
 #define RPLU_FLAG_EAGER 8        /* dense: force the eager (update every step) loop;
                                     default: delayed updates when R exceeds L2 */
-#define RPLU_FLAG_FUSED 16       /* dense delayed-update loop: apply each pending term
-                                    with fused multiply-adds (x - l*u rounded once; 4
-                                    FMAs per complex term) instead of the reference's
-                                    multiply-then-subtract;
-                                    residual / L / U then differ from the reference by
-                                    rounding (not bit-identical), pivots agree except
-                                    at counted near-boundary draws */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0
@@ -161,8 +154,6 @@ typedef struct rplu_shard_args {
   const double* uniforms; /* host uniform stream (uploaded by begin) */
   int64_t n_uniforms;
   void* stream;
-  int32_t flags;          /* RPLU_FLAG_FUSED (delayed-update terms as one FMA) */
-  int32_t reserved;
 } rplu_shard_args;
 
 /* K1 masses of the local rows, state reset, uniforms upload; writes the local

@@ -34,7 +34,6 @@ FLAG_TIME_KERNELS = 1
 FLAG_NO_GRAPH = 2
 FLAG_LAZY = 4
 FLAG_EAGER = 8
-FLAG_FUSED = 16
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -94,7 +93,7 @@ class ShardArgs(ctypes.Structure):
         ("steps", c_i64), ("stop_tol", c_dbl),
         ("R", c_vp), ("Lt", c_vp), ("U", c_vp), ("ldu", c_i64),
         ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
-        ("stream", c_vp), ("flags", c_i32), ("reserved", c_i32),
+        ("stream", c_vp),
     ]
 
 

@@ -351,9 +351,7 @@ static int shard_check(rplu_ctx* ctx, const rplu_shard_args* a) {
 }
 
 static int shard_block(const rplu_shard_args* a) {
-  return a->lazy_block < 0
-             ? dense_lazy_block_default(a->dtype, (a->flags & RPLU_FLAG_FUSED) != 0)
-             : a->lazy_block;
+  return a->lazy_block < 0 ? dense_lazy_block_default(a->dtype) : a->lazy_block;
 }
 
 static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
@@ -378,7 +376,6 @@ static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
   p.stop_tol = a->stop_tol;
   p.Lt = a->Lt;
   p.lazy_block = shard_block(a);
-  p.fused = p.lazy_block > 0 && (a->flags & RPLU_FLAG_FUSED) != 0;
   return p;
 }
 
@@ -468,8 +465,7 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
     const long long b = p.lazy_block, t0 = (t / b) * b;
     const bool flush = (t + 1 - t0 == b) || (t == a->steps - 1);
     if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
-                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, p.fused,
-                                     s)))
+                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, s)))
       return rc;
   } else if (a->n_local > 0) {
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
@@ -515,7 +511,7 @@ int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* o
       if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
                                        a->ldu, reinterpret_cast<double*>(ctx->masses.ptr),
                                        reinterpret_cast<DevState*>(ctx->state.ptr), done - 1, t0,
-                                       false, true, true, (a->flags & RPLU_FLAG_FUSED) != 0, s)))
+                                       false, true, true, s)))
         return rc;
       RPLU_CUDA(cudaStreamSynchronize(s));
     }

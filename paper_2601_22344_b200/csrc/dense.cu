@@ -49,7 +49,6 @@ struct DenseParams {
   long long t0;
   int lazy;
   int force;  // run the pass even after a stop (final flush)
-  int fused;  // RPLU_FLAG_FUSED: pending terms as one FMA each
 };
 
 template <typename T, int VEC>
@@ -414,7 +413,7 @@ __global__ void __launch_bounds__(256) lazy_row_kernel(DenseParams p) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
        k += (long long)gridDim.x * blockDim.x) {
     T x = R[i * p.ld + k];
-    for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, s_l[s], U[s * p.ldu + k]);
+    for (int s = 0; s < q; ++s) x = S::sub_outer(x, s_l[s], U[s * p.ldu + k]);
     urow[k] = x;
   }
 }
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(1024) lazy_select_col_kernel(DenseParams p) {
       const T* U = reinterpret_cast<const T*>(p.U);
       for (long long k = threadIdx.x; k < m; k += B) {
         T x = R[i * p.ld + k];
-        for (long long s = p.t0; s < t; ++s) x = pend_sub(p.fused != 0, x, Lt[s * n + i], U[s * p.ldu + k]);
+        for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + i], U[s * p.ldu + k]);
         urow[k] = x;
       }
       __syncthreads();
@@ -530,7 +529,7 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
       if (s < q) ll[s] = Lt[(p.t0 + s) * n + k];
 #pragma unroll
     for (int s = 0; s < kLazyMaxBlock; ++s)
-      if (s < q) x = pend_sub(p.fused != 0, x, ll[s], s_upiv[s]);
+      if (s < q) x = S::sub_outer(x, ll[s], s_upiv[s]);
     Lt[t * n + k] = S::scale(x, cf);
   }
 }
@@ -571,7 +570,7 @@ __global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
       for (int r = 0; r < RB; ++r) {
         const T lv = Ls[s][r];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub(p.fused != 0, rv[r].v[e], lv, u.v[e]);
+        for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
       }
     }
 #pragma unroll
@@ -588,7 +587,7 @@ __global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
     for (int r = 0; r < RB; ++r) {
       if (r < nr) {
         T x = R[(row0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, Ls[s][r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(row0 + r) * ld + l] = x;
       }
@@ -660,7 +659,7 @@ __global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
         for (int r = 0; r < RPT; ++r) {
           const T lv = Ls[s][ty * RPT + r];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub(p.fused != 0, rv[r].v[e], lv, u.v[e]);
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
         }
       }
 #pragma unroll
@@ -678,7 +677,7 @@ __global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
     for (int r = 0; r < RPT; ++r) {
       if (r < nr) {
         T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = pend_sub(p.fused != 0, x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(myrow0 + r) * ld + l] = x;
       }
@@ -725,7 +724,7 @@ struct LazyPipeSmem {
 // QC > 0: the number of pending terms is a compile-time constant (one
 // instantiation per q), so the term loop is fully unrolled with immediate
 // shared-memory offsets and the FP64 pipe is not starved by address math.
-template <typename T, int VEC, int RPT, bool FLUSH, int QC = 0, bool FUSED = false>
+template <typename T, int VEC, int RPT, bool FLUSH, int QC = 0>
 __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
   using S = Scalar<T>;
   using SM = LazyPipeSmem<T, VEC, RPT>;
@@ -790,7 +789,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
         for (int r = 0; r < RPT; ++r) {
           const T lv = sm.Ls[s][ty * RPT + r];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub<FUSED>(rv[r].v[e], lv, u.v[e]);
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
         }
       };
       if constexpr (QC > 0) {
@@ -814,7 +813,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
     for (int r = 0; r < RPT; ++r) {
       if (r < nr) {
         T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = pend_sub<FUSED>(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = S::sub_outer(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(myrow0 + r) * ld + l] = x;
       }
@@ -958,68 +957,52 @@ static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) 
   else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
 }
 
-template <typename T, int RPT, bool FLUSH, int QC, bool FUSED>
+template <typename T, int RPT, bool FLUSH, int QC>
 static void launch_lazy_pass3_q(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   using SM = LazyPipeSmem<T, VEC, RPT>;
   const int smem = (int)sizeof(SM);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC, FUSED>,
+    cudaFuncSetAttribute(lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   dim3 grid((unsigned)((p.n + SM::ROWS - 1) / SM::ROWS));
-  lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC, FUSED><<<grid, 256, smem, s>>>(p);
+  lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC><<<grid, 256, smem, s>>>(p);
 }
 
-template <typename T, int RPT, bool FLUSH, bool FUSED>
+template <typename T, int RPT, bool FLUSH>
 static void launch_lazy_pass3_f(const DenseParams& p, cudaStream_t s) {
   switch ((int)(p.t - p.t0 + 1)) {
-    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1, FUSED>(p, s); return;
-    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2, FUSED>(p, s); return;
-    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3, FUSED>(p, s); return;
-    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4, FUSED>(p, s); return;
-    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5, FUSED>(p, s); return;
-    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6, FUSED>(p, s); return;
-    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7, FUSED>(p, s); return;
-    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8, FUSED>(p, s); return;
-    default: break;
+    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1>(p, s); return;
+    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2>(p, s); return;
+    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3>(p, s); return;
+    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4>(p, s); return;
+    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5>(p, s); return;
+    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6>(p, s); return;
+    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7>(p, s); return;
+    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8>(p, s); return;
+    default: launch_lazy_pass3_q<T, RPT, FLUSH, 0>(p, s); return;
   }
-  if constexpr (FUSED) {  // fused terms are cheap enough for longer blocks
-    switch ((int)(p.t - p.t0 + 1)) {
-      case 9: launch_lazy_pass3_q<T, RPT, FLUSH, 9, FUSED>(p, s); return;
-      case 10: launch_lazy_pass3_q<T, RPT, FLUSH, 10, FUSED>(p, s); return;
-      case 11: launch_lazy_pass3_q<T, RPT, FLUSH, 11, FUSED>(p, s); return;
-      case 12: launch_lazy_pass3_q<T, RPT, FLUSH, 12, FUSED>(p, s); return;
-      default: break;
-    }
-  }
-  launch_lazy_pass3_q<T, RPT, FLUSH, 0, FUSED>(p, s);
 }
 
-template <typename T, int RPT, bool FUSED>
+template <typename T, int RPT>
 static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
-  if (flush) launch_lazy_pass3_f<T, RPT, true, FUSED>(p, s);
-  else launch_lazy_pass3_f<T, RPT, false, FUSED>(p, s);
+  if (flush) launch_lazy_pass3_f<T, RPT, true>(p, s);
+  else launch_lazy_pass3_f<T, RPT, false>(p, s);
 }
 
 template <typename T>
 static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA);
-  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D.
-  // Fused terms always take the default pipelined kernel.
+  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D
   static const int kernel = env_int("RPLU_LAZY_KERNEL", 3);
-  constexpr int kDefRpt = sizeof(T) == 16 ? 2 : 8;
-  if (p.fused) {
-    launch_lazy_pass3<T, kDefRpt, true>(p, flush, s);
-    return;
-  }
   if (kernel == 3) {
-    static const int rpt = env_int("RPLU_LAZY_RPT", kDefRpt);
-    if (rpt >= 8) launch_lazy_pass3<T, 8, false>(p, flush, s);
-    else if (rpt >= 4) launch_lazy_pass3<T, 4, false>(p, flush, s);
-    else launch_lazy_pass3<T, 2, false>(p, flush, s);
+    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 8);
+    if (rpt >= 8) launch_lazy_pass3<T, 8>(p, flush, s);
+    else if (rpt >= 4) launch_lazy_pass3<T, 4>(p, flush, s);
+    else launch_lazy_pass3<T, 2>(p, flush, s);
     return;
   }
   if (kernel == 1) {
@@ -1036,14 +1019,13 @@ static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
 // the per-step minimum on B200 is at 5 (fp64; measured 1.25 / 1.23 / 1.26 /
 // 1.38 ms for q = 1..4, 2.7 ms for a flush), overridable with
 // RPLU_LAZY_BLOCK.
-// Fused terms (one FMA per term) halve the FP64 work of a pending term, so
-// the pass stays HBM-bound to about twice the q and the flush is amortised
-// over a longer block.
+// (Applying the pending terms as single FMAs instead of the reference's
+// multiply-then-subtract was measured and gives no gain at any block: the
+// pass is not FP64-throughput bound; profiles/r01/fused_terms_experiment.txt.)
 template <typename T>
-static int lazy_block(bool fused) {
-  const int dflt = fused ? (sizeof(T) == 16 ? 4 : (sizeof(T) == 4 ? 8 : 9))
-                         : (sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 4 : 5));  // fp32: 1064 steps/s at 4
-  int b = env_int(fused ? "RPLU_LAZY_BLOCK_FUSED" : "RPLU_LAZY_BLOCK", dflt);
+static int lazy_block() {
+  const int dflt = sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 4 : 5);  // fp32: 1064 steps/s at 4
+  int b = env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
 
@@ -1052,7 +1034,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
                            long long* launches) {
   DenseParams p = base;
   p.lazy = 1;
-  const int block = lazy_block<T>(p.fused != 0);
+  const int block = lazy_block<T>();
   sweep<T>(p, false, false, s);  // K1: masses of A
   RPLU_CUDA(cudaGetLastError());
   long long nl = 1;
@@ -1090,7 +1072,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
 // the pending steps t0..done-1 (no-op when the loop ran to the end).
 template <typename T>
 static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_t s) {
-  const long long block = lazy_block<T>(base.fused != 0);
+  const long long block = lazy_block<T>();
   const long long t0 = (done / block) * block;
   if (done <= t0 || done >= base.steps) return RPLU_OK;
   DenseParams p = base;
@@ -1141,8 +1123,6 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
   p.stop_tol = a->stop_tol;
   p.rule = a->rule;
-  static const int fused_env = env_int("RPLU_FUSED", -1);
-  p.fused = ((a->flags & RPLU_FLAG_FUSED) != 0 || fused_env == 1) ? 1 : 0;
 
   LoopTiming tm;
   tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
@@ -1203,7 +1183,7 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     if (rc) return rc;
     RPLU_CUDA(cudaStreamSynchronize(s));
   }
-  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype, p.fused != 0) : 0;
+  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype) : 0;
   out->sweep_bytes = 0.0;
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,
@@ -1368,8 +1348,7 @@ static void lazy_step_t(const DenseParams& p, bool pivcol, bool flush, cudaStrea
 
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
-                           long long t0, bool pivcol, bool flush, bool force, bool fused,
-                           cudaStream_t s) {
+                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s) {
   if (n == 0) return RPLU_OK;
   DenseParams p{};
   p.R = R;
@@ -1385,7 +1364,6 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   p.t0 = t0;
   p.lazy = 1;
   p.force = force ? 1 : 0;
-  p.fused = fused ? 1 : 0;
   switch (dtype) {
     case RPLU_F64: lazy_step_t<double>(p, pivcol, flush, s); break;
     case RPLU_F32: lazy_step_t<float>(p, pivcol, flush, s); break;
@@ -1396,11 +1374,11 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   return RPLU_OK;
 }
 
-int dense_lazy_block_default(int dtype, bool fused) {
+int dense_lazy_block_default(int dtype) {
   switch (dtype) {
-    case RPLU_F64: return lazy_block<double>(fused);
-    case RPLU_F32: return lazy_block<float>(fused);
-    default: return lazy_block<double2>(fused);
+    case RPLU_F64: return lazy_block<double>();
+    case RPLU_F32: return lazy_block<float>();
+    default: return lazy_block<double2>();
   }
 }
 

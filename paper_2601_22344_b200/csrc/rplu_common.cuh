@@ -94,10 +94,6 @@ template <> struct Scalar<double> {
   __device__ static __forceinline__ double sub_outer(double r, double l, double p) {
     return __dsub_rn(r, __dmul_rn(l, p));
   }
-  // r - l*p rounded once (RPLU_FLAG_FUSED delayed updates)
-  __device__ static __forceinline__ double sub_outer_fused(double r, double l, double p) {
-    return __fma_rn(-l, p, r);
-  }
   __device__ static __forceinline__ double zero() { return 0.0; }
 };
 
@@ -112,9 +108,6 @@ template <> struct Scalar<float> {
   __device__ static __forceinline__ float scale(float c, coef_t k) { return __fmul_rn(c, k); }
   __device__ static __forceinline__ float sub_outer(float r, float l, float p) {
     return __fsub_rn(r, __fmul_rn(l, p));
-  }
-  __device__ static __forceinline__ float sub_outer_fused(float r, float l, float p) {
-    return __fmaf_rn(-l, p, r);
   }
   __device__ static __forceinline__ float zero() { return 0.0f; }
 };
@@ -135,25 +128,8 @@ template <> struct Scalar<double2> {
     double2 q = cmul_np(l, p);
     return make_double2(__dsub_rn(r.x, q.x), __dsub_rn(r.y, q.y));
   }
-  // 4 FMAs instead of the reference's 2 mul/fma + 2 sub roundings per part
-  __device__ static __forceinline__ double2 sub_outer_fused(double2 r, double2 l, double2 p) {
-    return make_double2(__fma_rn(-l.x, p.x, __fma_rn(l.y, p.y, r.x)),
-                        __fma_rn(-l.x, p.y, __fma_rn(-l.y, p.x, r.y)));
-  }
   __device__ static __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
 };
-
-// one pending rank-1 term of the delayed-update loop: the reference's
-// rounding (bit-identical to the eager update) or a single FMA rounding
-template <bool FUSED, typename T>
-__device__ __forceinline__ T pend_sub(T r, T l, T p) {
-  if constexpr (FUSED) return Scalar<T>::sub_outer_fused(r, l, p);
-  else return Scalar<T>::sub_outer(r, l, p);
-}
-template <typename T>
-__device__ __forceinline__ T pend_sub(bool fused, T r, T l, T p) {
-  return fused ? Scalar<T>::sub_outer_fused(r, l, p) : Scalar<T>::sub_outer(r, l, p);
-}
 
 // ---------------------------------------------------------------------------
 // warp / block primitives

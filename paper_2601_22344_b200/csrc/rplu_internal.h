@@ -70,7 +70,6 @@ struct ShardParams {
   double stop_tol;
   void* Lt;        // [steps][n_local] local L columns
   int lazy_block;  // 0: eager; > 0: delayed-update block (host step loop)
-  bool fused;      // delayed-update terms as one FMA (RPLU_FLAG_FUSED)
 };
 int shard_select_impl(const ShardParams& p, cudaStream_t s);
 int shard_lazy_select_impl(const ShardParams& p, cudaStream_t s);
@@ -91,9 +90,8 @@ constexpr int kLazyMaxBlock = 12;  // longest delayed-update block
 // (masses of R^(t+1); flush writes it).  force runs the pass after a stop.
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
-                           long long t0, bool pivcol, bool flush, bool force, bool fused,
-                           cudaStream_t s);
-int dense_lazy_block_default(int dtype, bool fused);
+                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s);
+int dense_lazy_block_default(int dtype);
 
 // Sharded Cauchy-like steps (cauchy.cu).
 int cauchy_shard_begin_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* stats);

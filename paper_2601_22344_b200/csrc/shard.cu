@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) shard_lazy_row_kernel(ShardParams p) {
       continue;
     }
     T x = R[i * p.ld + k];
-    for (int s = 0; s < q; ++s) x = pend_sub(p.fused, x, s_l[s], U[s * p.ldu + k]);
+    for (int s = 0; s < q; ++s) x = S::sub_outer(x, s_l[s], U[s * p.ldu + k]);
     prow[k] = x;
   }
 }
