@@ -348,6 +348,17 @@ int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms);
 int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
                       int64_t* out_index, int32_t* near_boundary, void* stream);
 
+/* The same search against an ABSOLUTE target in [0, total] (first index whose
+ * running sum exceeds target; clamp / walk-back as above): the owner shard's
+ * local draw in a row-sharded elimination, where target = u*T_global minus
+ * the totals of the shards before it. */
+int rplu_sample_target(rplu_ctx* ctx, const double* weights, int64_t n, double target,
+                       int64_t* out_index, int32_t* near_boundary, void* stream);
+
+/* Total of the weights in the CDF code's summation order (the per-shard
+ * totals the shard CDF is formed from); host result. */
+int rplu_cdf_total(rplu_ctx* ctx, const double* weights, int64_t n, double* total, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

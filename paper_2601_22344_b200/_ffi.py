@@ -132,6 +132,9 @@ SIGNATURES = {
     "rplu_row_masses": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "rplu_sample_index": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_i64),
                                          ctypes.POINTER(c_i32), c_vp]),
+    "rplu_sample_target": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_i64),
+                                          ctypes.POINTER(c_i32), c_vp]),
+    "rplu_cdf_total": (ctypes.c_int, [c_vp, c_vp, c_i64, ctypes.POINTER(c_dbl), c_vp]),
     "rplu_cauchy_run": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyArgs),
                                        ctypes.POINTER(CauchyOut)]),
     "rplu_cauchy_row_norms": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,

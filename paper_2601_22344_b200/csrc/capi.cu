@@ -90,8 +90,8 @@ int run_maybe_graph(rplu_ctx* ctx, cudaStream_t user, bool use_graph, int slot,
 int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out);
 int row_masses_impl(rplu_ctx* ctx, int dtype, const void* R, long long n, long long m,
                     long long ld, double* masses, cudaStream_t s);
-int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
-                      int* near, cudaStream_t s);
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
+                      long long* idx, int* near, double* total, cudaStream_t s);
 int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* out);
 int fp64_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
 int tree_bounds_impl(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
@@ -733,11 +733,39 @@ int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
   if (g.rc) return g.rc;
   long long idx = -1;
   int near = 0;
-  int rc = sample_index_impl(ctx, weights, n, u, &idx, &near, reinterpret_cast<cudaStream_t>(stream));
+  int rc = sample_index_impl(ctx, weights, n, u, 0, &idx, &near, nullptr,
+                             reinterpret_cast<cudaStream_t>(stream));
   if (rc) return rc;
   *out_index = idx;
   if (near_boundary) *near_boundary = near;
   return RPLU_OK;
+}
+
+int rplu_sample_target(rplu_ctx* ctx, const double* weights, int64_t n, double target,
+                       int64_t* out_index, int32_t* near_boundary, void* stream) {
+  if (!ctx || !out_index) { set_error("rplu_sample_target: NULL argument"); return RPLU_ERR_ARG; }
+  if (n <= 0 || !weights) { set_error("weights must be a nonempty 1-D array"); return RPLU_ERR_ARG; }
+  if (!(target >= 0.0)) { set_error("rplu_sample_target: target must be >= 0"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  long long idx = -1;
+  int near = 0;
+  int rc = sample_index_impl(ctx, weights, n, target, 1, &idx, &near, nullptr,
+                             reinterpret_cast<cudaStream_t>(stream));
+  if (rc) return rc;
+  *out_index = idx;
+  if (near_boundary) *near_boundary = near;
+  return RPLU_OK;
+}
+
+int rplu_cdf_total(rplu_ctx* ctx, const double* weights, int64_t n, double* total, void* stream) {
+  if (!ctx || !total) { set_error("rplu_cdf_total: NULL argument"); return RPLU_ERR_ARG; }
+  if (n < 0 || (n > 0 && !weights)) { set_error("rplu_cdf_total: bad weights"); return RPLU_ERR_ARG; }
+  if (n == 0) { *total = 0.0; return RPLU_OK; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return sample_index_impl(ctx, weights, n, 0.0, 2, nullptr, nullptr, total,
+                           reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -1261,10 +1261,14 @@ struct SampleOut {
   long long idx;
   int status;  // 0 ok, 1 negative weight, 2 all zero
   int near;
+  double total;  // the CDF's total (the draw's own summation order)
 };
 
+// mode 0: u in [0,1) scaled by the CDF total (sample_index); mode 1: u is an
+// absolute target in [0, total] (the owner shard's draw of a sharded
+// elimination); mode 2: total only.
 __global__ void __launch_bounds__(1024) sample_index_kernel(const double* w, long long n, double u,
-                                                            SampleOut* out) {
+                                                            int mode, SampleOut* out) {
   constexpr int B = 1024;
   __shared__ CdfSmem<B> sm;
   __shared__ int neg;
@@ -1274,38 +1278,46 @@ __global__ void __launch_bounds__(1024) sample_index_kernel(const double* w, lon
     if (w[k] < 0.0) neg = 1;
   __syncthreads();
   if (neg) {
-    if (threadIdx.x == 0) { out->status = 1; out->idx = -1; out->near = 0; }
+    if (threadIdx.x == 0) { out->status = 1; out->idx = -1; out->near = 0; out->total = 0.0; }
     return;
   }
   auto wf = [&](long long k) { return w[k]; };
   Cdf<B> c = cdf_build<B>(wf, n, sm);
-  if (!(c.total > 0.0)) {
-    if (threadIdx.x == 0) { out->status = 2; out->idx = -1; out->near = 0; }
+  if (mode == 2 || !(c.total > 0.0)) {
+    if (threadIdx.x == 0) {
+      out->status = (mode == 2) ? 0 : 2;
+      out->idx = -1;
+      out->near = 0;
+      out->total = c.total;
+    }
     return;
   }
-  long long i = cdf_find<B>(wf, n, c, u, sm);
+  const double tg = (mode == 1) ? u : u * c.total;
+  long long i = cdf_find_target<B>(wf, n, c, tg, sm);
   if (threadIdx.x == 0) {
-    double tol = kNearBoundaryRel * c.total, tg = u * c.total;
+    double tol = kNearBoundaryRel * c.total;
     out->near = (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) ? 1 : 0;
     out->idx = i;
     out->status = 0;
+    out->total = c.total;
   }
 }
 
-int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, long long* idx,
-                      int* near, cudaStream_t s) {
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
+                      long long* idx, int* near, double* total, cudaStream_t s) {
   int rc;
   if ((rc = ctx->scratch[7].ensure(sizeof(SampleOut)))) return rc;
   SampleOut* d = reinterpret_cast<SampleOut*>(ctx->scratch[7].ptr);
-  sample_index_kernel<<<1, 1024, 0, s>>>(w, n, u, d);
+  sample_index_kernel<<<1, 1024, 0, s>>>(w, n, u, mode, d);
   RPLU_CUDA(cudaGetLastError());
   SampleOut h;
   RPLU_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   RPLU_CUDA(cudaStreamSynchronize(s));
   if (h.status == 1) { set_error("weights must be nonnegative"); return RPLU_ERR_ARG; }
   if (h.status == 2) { set_error("all weights are zero; nothing to sample"); return RPLU_ERR_ARG; }
-  *idx = h.idx;
+  if (idx) *idx = h.idx;
   if (near) *near = h.near;
+  if (total) *total = h.total;
   return RPLU_OK;
 }
 

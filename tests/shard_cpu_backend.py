@@ -265,3 +265,44 @@ class NumpyCauchyShardBackend:
     def finish(self):
         return dict(rows=self.rows, cols=self.cols, bound_maxes=self.bmax,
                     bound_sums=self.bsum, status=self.status, G=self.G, B=self.B)
+
+
+# ---------------------------------------------------------------------------
+# sharded cur_build on CPU tensors (gloo): the operator protocol and the draw /
+# downdate primitives restated with torch / numpy
+
+from paper_2601_22344_b200.operators import _DenseDeviceOp  # noqa: E402
+
+
+class CpuDenseOp(_DenseDeviceOp):
+    """_DenseDeviceOp on a CPU tensor (row norms without the CUDA kernel)."""
+
+    def row_norms_dev(self):
+        t = self.t
+        return (t.real ** 2 + (t.imag ** 2 if torch.is_complex(t) else 0)).sum(1).to(torch.float64)
+
+
+class NumpyCurOps:
+    def cdf_total(self, w):
+        w = w.numpy()
+        return float(np.cumsum(w)[-1]) if w.size else 0.0
+
+    def sample_target(self, w, target):
+        w = w.numpy()
+        c = np.cumsum(w)
+        i = min(int(np.searchsorted(c, target, side="right")), w.size - 1)
+        while i > 0 and not w[i] > 0:
+            i -= 1
+        if not w[i] > 0:
+            i = int(np.flatnonzero(w > 0)[0])
+        return i
+
+    def sample(self, w, u):
+        return oracle.sample_index(w.numpy(), u)
+
+    def downdate(self, nrow, g, v, chat, l2, floor, real):
+        nrow -= 2.0 * torch.real((g - v) * torch.conj(chat)) if not real else 2.0 * (g - v) * chat
+        nrow += l2 * chat.abs() ** 2
+        clamped = int((nrow < -floor).sum())
+        nrow.clamp_(min=0.0)
+        return clamped, float(nrow.sum())

@@ -80,6 +80,27 @@ def test_sample_index_boundaries(cuda_device):
         assert abs(rp.sample_index(big, u) - oracle.sample_index(big, u)) <= 1
 
 
+def test_sample_target_and_cdf_total(cuda_device):
+    """The owner-shard draw against an absolute target and the per-shard CDF
+    totals (rplu_sample_target / rplu_cdf_total) keep sample_index's
+    semantics: first running sum > target, clamp, zero walk-back."""
+    import torch
+
+    from paper_2601_22344_b200.sharded_cur import CudaCurOps
+    ops = CudaCurOps(torch.device("cuda"))
+    w = torch.tensor([1.0, 2.0, 0.0, 1.0, 4.0, 0.0], dtype=torch.float64, device="cuda")
+    assert ops.cdf_total(w) == 8.0
+    for target, want in [(0.0, 0), (0.999, 0), (1.0, 1), (3.0, 3), (4.0, 4), (7.9, 4),
+                         (8.0, 4), (9.0, 4)]:
+        assert ops.sample_target(w, target) == want, target
+    big = torch.from_numpy(np.random.default_rng(1).random(200_001)).cuda()
+    tot = ops.cdf_total(big)
+    assert abs(tot - float(big.sum())) <= 1e-9 * tot
+    for u in (0.05, 0.5, 0.95):
+        assert ops.sample_target(big, u * tot) == rp.sample_index(big, u)
+    assert ops.cdf_total(torch.zeros(0, dtype=torch.float64, device="cuda")) == 0.0
+
+
 def test_errors_and_validation(cuda_device):
     with pytest.raises(ValueError):
         rp.eliminate(np.eye(3), rp.PivotRule("rplu", rp.RngState(0)), 4)

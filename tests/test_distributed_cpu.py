@@ -195,3 +195,52 @@ def test_sharded_cauchy_matches_single_process(world, rule, stop_tol):
     for o in outs:
         np.testing.assert_allclose(o[7], ref["B"], rtol=1e-10,
                                    atol=1e-13 * np.abs(ref["B"]).max())
+
+
+def _cur_worker(rank, world, port, A, seed, k, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_cpu_backend import CpuDenseOp, NumpyCurOps
+
+        import paper_2601_22344_b200 as rp
+        from paper_2601_22344_b200.distributed import shard_rows
+        from paper_2601_22344_b200.sharded_cur import TorchComm, sharded_cur_build
+        lo, hi = shard_rows(A.shape[0], world, rank)
+        op = CpuDenseOp(torch.from_numpy(A))
+        fact, info = sharded_cur_build(op, (lo, hi), "rplu-cur", k, rng=rp.RngState(seed),
+                                       comm=TorchComm(), ops=NumpyCurOps())
+        out_q.put((rank, fact.row_indices, fact.col_indices, fact.core_matrix(),
+                   info.row_norms, info.total_sq_norms))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cur_matches_oracle(world):
+    """Row-sharded cur_build (replicated operator, local row norms / g / c
+    rows, g[I] by a -0.0 allreduce) picks the oracle's skeleton."""
+    import oracle
+    rs = np.random.default_rng(11)
+    n, m, k = 130, 110, 25
+    U, _ = np.linalg.qr(rs.standard_normal((n, n)))
+    V, _ = np.linalg.qr(rs.standard_normal((m, m)))
+    A = (U[:, :m] * 0.8 ** np.arange(m)) @ V.T
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cur_worker, args=(r, world, port, A, 11, k, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = _collect(q, procs, world, key=lambda o: o[0])
+    core, info = oracle.cur_build(oracle.DenseHost(A), "rplu-cur", k, seed=11)
+    for o in outs:
+        assert o[1] == core.I and o[2] == core.J
+    np.testing.assert_allclose(outs[0][3], core.W, rtol=1e-12, atol=1e-14)
+    rn = np.concatenate([o[4] for o in outs])
+    # eliminated rows sit at the downdate's rounding floor (eps * total0)
+    np.testing.assert_allclose(rn, info["row_norms"], rtol=1e-8,
+                               atol=1e-14 * info["total_sq_norms"][0])
+    np.testing.assert_allclose(outs[0][5], info["total_sq_norms"], rtol=1e-10)

@@ -200,3 +200,37 @@ def test_cauchy_emulated_shards(world, rule, stop_tol, cuda_device):
     for t, (c, r, a) in enumerate(ref["steps"]):
         assert np.abs(C[t] - c).max() <= 1e-10 * np.abs(c).max()
         assert np.abs(bes[0].R[t].cpu().numpy() - r).max() <= 1e-10 * np.abs(r).max()
+
+
+# ---------------------------------------------------------------------------
+# Sharded matrix-free CUR (C5): rows of the generated GEMV per shard
+
+from paper_2601_22344_b200.sharded_cur import sharded_cur_build  # noqa: E402
+from thread_comm import run_ranks  # noqa: E402
+
+
+@pytest.mark.parametrize("world,rule", [(1, "rplu-cur"), (2, "rplu-cur"), (3, "rplu-cur"),
+                                        (2, "c2plu-cur")])
+def test_sharded_cur_matches_single_gpu(world, rule, cuda_device):
+    """Shards emulated by threads on one GPU reproduce the single-GPU
+    cur_build skeleton (index sets) and core; the local maintained norms
+    concatenate to the single-GPU ones."""
+    P, Q = gen.c5_points(4, n=3000, m=2500)
+    A = rp.GaussianKernelOperator(P, Q, h=0.1)
+    k = 40
+    mk = (lambda: rp.RngState(4)) if rule == "rplu-cur" else (lambda: None)
+    fact, info = rp.cur_build(A, rule, k, rng=mk())
+
+    def one(r, comm):
+        lo, hi = shard_rows(3000, world, r)
+        return sharded_cur_build(A, (lo, hi), rule, k, rng=mk(), comm=comm)
+
+    res = run_ranks(world, one)
+    for f, inf in res:
+        assert f.row_indices == fact.row_indices and f.col_indices == fact.col_indices
+        np.testing.assert_allclose(f.core_matrix(), fact.core_matrix(), rtol=1e-12, atol=1e-15)
+    rn = np.concatenate([inf.row_norms for _, inf in res])
+    np.testing.assert_allclose(rn, info.row_norms, rtol=1e-7,
+                               atol=1e-13 * info.total_sq_norms[0])
+    np.testing.assert_allclose(res[0][1].total_sq_norms, info.total_sq_norms, rtol=1e-10)
+    assert res[0][1].uniforms_consumed == info.uniforms_consumed
