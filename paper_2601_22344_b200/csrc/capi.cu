@@ -343,7 +343,7 @@ static int shard_check(rplu_ctx* ctx, const rplu_shard_args* a) {
     const long long vec = 16 / (a->dtype == RPLU_F32 ? 4 : (a->dtype == RPLU_F64 ? 8 : 16));
     if (a->lazy_block > kLazyMaxBlock || a->ld % vec || a->ldu % vec ||
         (uintptr_t)a->R % 16 || (uintptr_t)a->U % 16 || !a->Lt) {
-      set_error("rplu_shard: lazy_block needs <= 12, 16-byte aligned rows of R and U, and Lt");
+      set_error("rplu_shard: lazy_block needs <= 16, 16-byte aligned rows of R and U, and Lt");
       return RPLU_ERR_ARG;
     }
   }

@@ -15,6 +15,8 @@
 // separate reduction pass over R.  K2 is a single CTA (1024 threads) that
 // scans the n masses and the m pivot-row weights; it never leaves the device,
 // so the whole loop runs without a host round trip.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -534,166 +536,235 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
   }
 }
 
-// Masses of R^(t+1) = R^(t0) - sum_{s=t0..t} L_s U_s (and, FLUSH, write it).
-// One CTA owns RB rows; its pending L values sit in shared memory, the
-// pending U rows are read per column chunk (L2-resident: q rows of m).
-template <typename T, int VEC, int RB, bool FLUSH>
-__global__ void __launch_bounds__(256) lazy_pass_kernel(DenseParams p) {
-  using S = Scalar<T>;
-  constexpr int NT = 256;
-  if (!p.force && !p.st->active) return;
-  const long long row0 = (long long)blockIdx.x * RB;
-  const long long n = p.n, m = p.m, ld = p.ld;
-  const int q = (int)(p.t - p.t0 + 1);
-  T* R = reinterpret_cast<T*>(p.R);
-  const T* Lt = reinterpret_cast<const T*>(p.Lt);
-  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
-  __shared__ T Ls[kLazyMaxBlock][RB];
-  for (int idx = threadIdx.x; idx < q * RB; idx += NT) {
-    const int s = idx / RB, r = idx % RB;
-    Ls[s][r] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
-  }
-  __syncthreads();
-  double acc[RB];
-#pragma unroll
-  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-  const int nr = (int)min((long long)RB, n - row0);
-  const long long mv = (m / VEC) * VEC;
-  for (long long l = (long long)threadIdx.x * VEC; l < mv; l += (long long)NT * VEC) {
-    VecT<T, VEC> rv[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-      if (r < nr) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (row0 + r) * ld + l);
-    for (int s = 0; s < q; ++s) {
-      const VecT<T, VEC> u = *reinterpret_cast<const VecT<T, VEC>*>(U + s * p.ldu + l);
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const T lv = Ls[s][r];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      if (r < nr) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
-        if (FLUSH) *reinterpret_cast<VecT<T, VEC>*>(R + (row0 + r) * ld + l) = rv[r];
-      }
-    }
-  }
-  for (long long l = mv + threadIdx.x; l < m; l += NT) {  // scalar tail
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      if (r < nr) {
-        T x = R[(row0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][r], U[s * p.ldu + l]);
-        acc[r] += S::mass(x);
-        if (FLUSH) R[(row0 + r) * ld + l] = x;
-      }
-    }
-  }
-  __shared__ double red[NT / 32][RB];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = 0; r < RB; ++r) {
-    const double s = warp_sum(acc[r]);
-    if (lane == 0) red[w][r] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < RB && (int)threadIdx.x < nr) {
-    double s = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < NT / 32; ++ww) s += red[ww][threadIdx.x];
-    p.masses[row0 + threadIdx.x] = s;
-  }
+// ---------------------------------------------------------------------------
+// Delayed-update pass, TMA-fed (default): masses of
+// R^(t+1) = R^(t0) - sum_{s=t0..t} L_s U_s and, FLUSH, the write of R^(t+1).
+//
+// Persistent, warp-specialised CTA (one per SM): warp 8 is the producer, one
+// lane per residual row, and streams (32 rows x 1 KB) of R plus the matching
+// 1 KB of each pending U row into a ring of STAGES shared-memory stages with
+// 1-D bulk copies (cp.async.bulk, completion counted in bytes on the stage's
+// "full" mbarrier; R with an L2 evict-first hint, U evict-last).  Warps 0..7
+// consume: 64 threads across the 1 KB column chunk x 4 groups of 8 rows, each
+// thread applies the QC pending terms in step order with the reference's
+// rounding (one multiply, one subtract per term) to its 8 x 16 bytes and
+// releases the stage with one arrive per warp on its "empty" mbarrier.  No
+// CTA-wide barrier sits in the stream, so the copy engine stays up to
+// STAGES x 33..48 KB ahead of the FP64 work; the only named barrier is at a
+// row-block switch (pending L values, mass write-out).  A CTA owns row blocks
+// b, b+grid, ...; each block's masses are summed by that CTA alone in a
+// fixed order (per-thread chunks, warp tree, two warps), so the result is
+// deterministic.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
 
-// Same pass with a 2-D CTA: 64 threads across a column chunk of 64*VEC
-// columns x 4 row groups of RPT rows (32 rows per CTA).  The pending U rows
-// of the chunk are staged once in shared memory and reused by all 32 rows
-// (L2 traffic for U = q/32 of the R stream), so each thread only holds its
-// RPT x VEC residual values in registers and 4 CTAs fit per SM.
-template <typename T, int VEC, int RPT, bool FLUSH>
-__global__ void __launch_bounds__(256) lazy_pass2_kernel(DenseParams p) {
+template <typename T, int QC>
+struct LazyTma {
+  static constexpr int TX = 64, RPT = 8, ROWS = 32, NCW = 8;  // NCW consumer warps
+  static constexpr int LINE = TX * 16;                        // bytes of one row per stage
+  static constexpr int STAGE = (ROWS + QC) * LINE;
+  static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
+  static constexpr size_t OFF_L = (size_t)STAGES * STAGE;
+  static constexpr size_t OFF_RED = OFF_L + 2 * sizeof(T) * QC * ROWS;
+  static constexpr size_t OFF_BAR = (OFF_RED + 2 * NCW * RPT * sizeof(double) + 7) & ~size_t(7);
+  static constexpr size_t SMEM = OFF_BAR + 2 * STAGES * sizeof(uint64_t) + 1024;  // + alignment
+};
+
+// tmR: R as a 2-D tensor (columns x rows, in 8-byte words for fp64 and
+// complex128, 4-byte for fp32), box = 1 KB x 32 rows; tmU: the pending rows
+// U[t0 .. t0+QC) with box 1 KB x QC rows.  Out-of-range rows and columns are
+// zero-filled by the TMA unit, so every stage carries (32 + QC) KB.
+template <typename T, int VEC, bool FLUSH, int QC>
+__global__ void __launch_bounds__(288, 1)
+    lazy_pass4_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmR,
+                      const __grid_constant__ CUtensorMap tmU) {
   using S = Scalar<T>;
-  constexpr int NT = 256, TX = 64, TY = NT / TX, ROWS = TY * RPT, CW = TX * VEC;
+  using C = LazyTma<T, QC>;
+  using V = VecT<T, VEC>;
+  constexpr int TX = C::TX, RPT = C::RPT, ROWS = C::ROWS, STAGES = C::STAGES, CW = TX * VEC;
+  constexpr int WORDS = 1024 / (sizeof(T) == 4 ? 4 : 8);  // box inner extent in map words
+  static_assert(sizeof(V) == 16, "16-byte vectors");
   if (!p.force && !p.st->active) return;
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const long long row0 = (long long)blockIdx.x * ROWS;
-  const long long n = p.n, m = p.m, ld = p.ld;
-  const int q = (int)(p.t - p.t0 + 1);
-  T* R = reinterpret_cast<T*>(p.R);
-  const T* Lt = reinterpret_cast<const T*>(p.Lt);
-  const T* U = reinterpret_cast<const T*>(p.U) + p.t0 * p.ldu;
-  __shared__ VecT<T, VEC> Us[kLazyMaxBlock][TX];
-  __shared__ T Ls[kLazyMaxBlock][ROWS];
-  for (int idx = threadIdx.x; idx < q * ROWS; idx += NT) {
-    const int s = idx / ROWS, r = idx % ROWS;
-    Ls[s][r] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
-  }
-  const long long myrow0 = row0 + ty * RPT;
-  const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
-  double acc[RPT];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-  const long long mv = (m / VEC) * VEC;
-  for (long long l0 = 0; l0 < mv; l0 += CW) {
-    const long long l = l0 + (long long)tx * VEC;
-    const bool inb = l < mv;
-    __syncthreads();  // previous chunk's Us reads are done
-    for (int idx = threadIdx.x; idx < q * TX; idx += NT) {
-      const int s = idx / TX, v = idx % TX;
-      const long long lc = l0 + (long long)v * VEC;
-      if (lc < mv) Us[s][v] = *reinterpret_cast<const VecT<T, VEC>*>(U + s * p.ldu + lc);
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* smem_raw =
+      smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB-aligned stages
+  V* tiles = reinterpret_cast<V*>(smem_raw);
+  T* Ls = reinterpret_cast<T*>(smem_raw + C::OFF_L);  // [2][QC][ROWS]
+  double* red = reinterpret_cast<double*>(smem_raw + C::OFF_RED);  // [2][NCW][RPT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
     }
-    VecT<T, VEC> rv[RPT];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-      if (inb && r < nr) rv[r] = *reinterpret_cast<const VecT<T, VEC>*>(R + (myrow0 + r) * ld + l);
-    __syncthreads();
-    if (inb) {
-      for (int s = 0; s < q; ++s) {
-        const VecT<T, VEC> u = Us[s][tx];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const T lv = Ls[s][ty * RPT + r];
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        if (r < nr) {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
-          if (FLUSH) *reinterpret_cast<VecT<T, VEC>*>(R + (myrow0 + r) * ld + l) = rv[r];
-        }
-      }
-    }
-  }
-  for (long long l = mv + tx; l < m; l += TX) {  // scalar tail (m % VEC columns)
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      if (r < nr) {
-        T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, Ls[s][ty * RPT + r], U[s * p.ldu + l]);
-        acc[r] += S::mass(x);
-        if (FLUSH) R[(myrow0 + r) * ld + l] = x;
-      }
-    }
-  }
-  __shared__ double red[NT / 32][RPT];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const double sm = warp_sum(acc[r]);
-    if (lane == 0) red[w][r] = sm;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x < ROWS) {
-    const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;  // row group g = warps 2g, 2g+1
-    if (row0 + threadIdx.x < n) p.masses[row0 + threadIdx.x] = red[2 * g][r] + red[2 * g + 1][r];
+
+  const long long n = p.n, m = p.m, ld = p.ld;
+  const long long nchunks = (m + CW - 1) / CW;
+  const long long nblocks = (n + ROWS - 1) / ROWS;
+  T* R = reinterpret_cast<T*>(p.R);
+  const T* Lt = reinterpret_cast<const T*>(p.Lt);
+
+  if (warp == C::NCW) {  // producer warp: one elected lane issues two TMA loads per stage
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmR) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmU) : "memory");
+      const uint64_t pol_r = policy_evict_first(), pol_u = policy_evict_last();
+      int stage = 0;
+      unsigned phase = 0;
+      for (long long rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+        for (long long c = 0; c < nchunks; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], (unsigned)C::STAGE);
+          V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
+          tma_load_2d(st, &tmR, (int)(c * WORDS), (int)(rb * ROWS), &full[stage], pol_r);
+          tma_load_2d(st + ROWS * TX, &tmU, (int)(c * WORDS), (int)p.t0, &full[stage], pol_u);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // consumers
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  int stage = 0;
+  unsigned phase = 0;
+  int k = 0;  // row blocks done by this CTA
+  long long prev_row0 = -1;
+  for (long long rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++k) {
+    const long long row0 = rb * ROWS;
+    const int buf = k & 1;
+    T* L = Ls + buf * QC * ROWS;
+    for (int idx = threadIdx.x; idx < QC * ROWS; idx += C::NCW * 32) {
+      const int s = idx / ROWS, r = idx % ROWS;
+      L[idx] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
+    }
+    consumer_bar();  // L visible; red[buf^1] of the previous block complete
+    if (prev_row0 >= 0 && threadIdx.x < ROWS) {
+      const double* rd = red + (buf ^ 1) * C::NCW * RPT;
+      const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
+      if (prev_row0 + threadIdx.x < n)
+        p.masses[prev_row0 + threadIdx.x] = rd[(2 * g) * RPT + r] + rd[(2 * g + 1) * RPT + r];
+    }
+    const long long myrow0 = row0 + ty * RPT;
+    const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
+    double acc[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+    for (long long c = 0; c < nchunks; ++c) {
+      mbar_wait(&full[stage], phase);
+      const V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
+      const long long l = c * CW + (long long)tx * VEC;
+      if (l < m) {
+        V rv[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) rv[r] = st[(ty * RPT + r) * TX + tx];
+#pragma unroll
+        for (int s = 0; s < QC; ++s) {
+          const V u = st[(ROWS + s) * TX + tx];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const T lv = L[s * ROWS + ty * RPT + r];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (VEC == 1 || l + VEC <= m) {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            if (r < nr) {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
+              if (FLUSH) *reinterpret_cast<V*>(R + (myrow0 + r) * ld + l) = rv[r];
+            }
+          }
+        } else {  // last, partial vector of a row (m % VEC columns)
+          for (int r = 0; r < RPT; ++r) {
+            if (r < nr) {
+              for (int e = 0; e < VEC && l + e < m; ++e) {
+                acc[r] += S::mass(rv[r].v[e]);
+                if (FLUSH) R[(myrow0 + r) * ld + l + e] = rv[r].v[e];
+              }
+            }
+          }
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    double* rd = red + buf * C::NCW * RPT;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const double sv = warp_sum(acc[r]);
+      if (lane == 0) rd[warp * RPT + r] = sv;
+    }
+    prev_row0 = row0;
+  }
+  consumer_bar();
+  if (prev_row0 >= 0 && threadIdx.x < ROWS) {
+    const double* rd = red + ((k - 1) & 1) * C::NCW * RPT;
+    const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
+    if (prev_row0 + threadIdx.x < n)
+      p.masses[prev_row0 + threadIdx.x] = rd[(2 * g) * RPT + r] + rd[(2 * g + 1) * RPT + r];
   }
 }
 
@@ -940,21 +1011,92 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <typename T, int RB>
-static void launch_lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
-  constexpr int VEC = Scalar<T>::kVec;
-  dim3 grid((unsigned)((p.n + RB - 1) / RB));
-  if (flush) lazy_pass_kernel<T, VEC, RB, true><<<grid, 256, 0, s>>>(p);
-  else lazy_pass_kernel<T, VEC, RB, false><<<grid, 256, 0, s>>>(p);
+static int sm_count() {
+  static int c = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return c;
 }
 
-template <typename T, int RPT>
-static void launch_lazy_pass2(const DenseParams& p, bool flush, cudaStream_t s) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 2-D map over a row-major (rows x cols) array of element size esize with a
+// row pitch of ld elements; box = 1 KB of columns x box_rows rows.
+static bool make_row_map(CUtensorMap* map, const void* base, int esize, long long rows,
+                         long long cols, long long ld, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int w = esize == 4 ? 4 : 8;  // complex128 = pairs of fp64 words
+  const int per = esize / w;
+  const cuuint64_t dims[2] = {(cuuint64_t)(cols * per), (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * esize)};
+  const cuuint32_t box[2] = {(cuuint32_t)(1024 / w), (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, w == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, bool FLUSH, int QC>
+static int launch_lazy_pass4_q(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
-  constexpr int ROWS = 4 * RPT;
-  dim3 grid((unsigned)((p.n + ROWS - 1) / ROWS));
-  if (flush) lazy_pass2_kernel<T, VEC, RPT, true><<<grid, 256, 0, s>>>(p);
-  else lazy_pass2_kernel<T, VEC, RPT, false><<<grid, 256, 0, s>>>(p);
+  using C = LazyTma<T, QC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const long long nblocks = (p.n + C::ROWS - 1) / C::ROWS;
+  const long long g = nblocks < sm_count() ? nblocks : sm_count();
+  if (g <= 0 || p.m <= 0) return RPLU_OK;
+  CUtensorMap tmR, tmU;
+  const long long urows = p.t0 + QC;  // U rows 0 .. t0+QC-1 exist
+  if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, C::ROWS) ||
+      !make_row_map(&tmU, p.U, (int)sizeof(T), urows, p.m, p.ldu, QC)) {
+    set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
+    return RPLU_ERR_CUDA;
+  }
+  lazy_pass4_kernel<T, VEC, FLUSH, QC><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
+  return RPLU_OK;
+}
+
+template <typename T, bool FLUSH>
+static int launch_lazy_pass4_f(const DenseParams& p, cudaStream_t s) {
+  static_assert(kLazyMaxBlock == 16, "one instantiation per pending-term count");
+  switch ((int)(p.t - p.t0 + 1)) {
+    case 1: return launch_lazy_pass4_q<T, FLUSH, 1>(p, s);
+    case 2: return launch_lazy_pass4_q<T, FLUSH, 2>(p, s);
+    case 3: return launch_lazy_pass4_q<T, FLUSH, 3>(p, s);
+    case 4: return launch_lazy_pass4_q<T, FLUSH, 4>(p, s);
+    case 5: return launch_lazy_pass4_q<T, FLUSH, 5>(p, s);
+    case 6: return launch_lazy_pass4_q<T, FLUSH, 6>(p, s);
+    case 7: return launch_lazy_pass4_q<T, FLUSH, 7>(p, s);
+    case 8: return launch_lazy_pass4_q<T, FLUSH, 8>(p, s);
+    case 9: return launch_lazy_pass4_q<T, FLUSH, 9>(p, s);
+    case 10: return launch_lazy_pass4_q<T, FLUSH, 10>(p, s);
+    case 11: return launch_lazy_pass4_q<T, FLUSH, 11>(p, s);
+    case 12: return launch_lazy_pass4_q<T, FLUSH, 12>(p, s);
+    case 13: return launch_lazy_pass4_q<T, FLUSH, 13>(p, s);
+    case 14: return launch_lazy_pass4_q<T, FLUSH, 14>(p, s);
+    case 15: return launch_lazy_pass4_q<T, FLUSH, 15>(p, s);
+    default: return launch_lazy_pass4_q<T, FLUSH, 16>(p, s);
+  }
 }
 
 template <typename T, int RPT, bool FLUSH, int QC>
@@ -972,46 +1114,18 @@ static void launch_lazy_pass3_q(const DenseParams& p, cudaStream_t s) {
   lazy_pass3_kernel<T, VEC, RPT, FLUSH, QC><<<grid, 256, smem, s>>>(p);
 }
 
-template <typename T, int RPT, bool FLUSH>
-static void launch_lazy_pass3_f(const DenseParams& p, cudaStream_t s) {
-  switch ((int)(p.t - p.t0 + 1)) {
-    case 1: launch_lazy_pass3_q<T, RPT, FLUSH, 1>(p, s); return;
-    case 2: launch_lazy_pass3_q<T, RPT, FLUSH, 2>(p, s); return;
-    case 3: launch_lazy_pass3_q<T, RPT, FLUSH, 3>(p, s); return;
-    case 4: launch_lazy_pass3_q<T, RPT, FLUSH, 4>(p, s); return;
-    case 5: launch_lazy_pass3_q<T, RPT, FLUSH, 5>(p, s); return;
-    case 6: launch_lazy_pass3_q<T, RPT, FLUSH, 6>(p, s); return;
-    case 7: launch_lazy_pass3_q<T, RPT, FLUSH, 7>(p, s); return;
-    case 8: launch_lazy_pass3_q<T, RPT, FLUSH, 8>(p, s); return;
-    default: launch_lazy_pass3_q<T, RPT, FLUSH, 0>(p, s); return;
-  }
-}
-
-template <typename T, int RPT>
-static void launch_lazy_pass3(const DenseParams& p, bool flush, cudaStream_t s) {
-  if (flush) launch_lazy_pass3_f<T, RPT, true>(p, s);
-  else launch_lazy_pass3_f<T, RPT, false>(p, s);
-}
-
 template <typename T>
-static void lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
-  // RPLU_LAZY_KERNEL=1: the 1-D variant (RPLU_LAZY_RB rows per CTA);
-  // 2: 2-D without the cp.async pipeline; 3 (default): pipelined 2-D
-  static const int kernel = env_int("RPLU_LAZY_KERNEL", 3);
+static int lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
+  // RPLU_LAZY_KERNEL=3: the round-1 cp.async double-buffered pass (one
+  // instantiation, runtime q; experiments only); default 4: TMA-fed pass
+  static const int kernel = env_int("RPLU_LAZY_KERNEL", 4);
+  constexpr int RPT3 = sizeof(T) == 16 ? 2 : 8;
   if (kernel == 3) {
-    static const int rpt = env_int("RPLU_LAZY_RPT", sizeof(T) == 16 ? 2 : 8);
-    if (rpt >= 8) launch_lazy_pass3<T, 8>(p, flush, s);
-    else if (rpt >= 4) launch_lazy_pass3<T, 4>(p, flush, s);
-    else launch_lazy_pass3<T, 2>(p, flush, s);
-    return;
+    if (flush) launch_lazy_pass3_q<T, RPT3, true, 0>(p, s);
+    else launch_lazy_pass3_q<T, RPT3, false, 0>(p, s);
+    return RPLU_OK;
   }
-  if (kernel == 1) {
-    static const int rb = env_int("RPLU_LAZY_RB", sizeof(T) == 16 ? 8 : 16);
-    if (rb <= 8) launch_lazy_pass<T, 8>(p, flush, s);
-    else launch_lazy_pass<T, 16>(p, flush, s);
-    return;
-  }
-  launch_lazy_pass2<T, sizeof(T) == 16 ? 4 : 8>(p, flush, s);
+  return flush ? launch_lazy_pass4_f<T, true>(p, s) : launch_lazy_pass4_f<T, false>(p, s);
 }
 
 // Default flush interval: the pass is HBM-bound up to q ~ 3 pending terms and
@@ -1057,7 +1171,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
       lazy_pivcol_kernel<T><<<pc_blocks, 256, 0, s>>>(p);
       const bool flush = (t - t0 + 1 == block) || (t == p.steps - 1);
       tm.mark(flush ? 2 : 1, s, true);
-      lazy_pass<T>(p, flush, s);
+      if (int rc = lazy_pass<T>(p, flush, s)) return rc;
       tm.mark(flush ? 2 : 1, s, false);
       nl += 2;
       if (flush) t0 = t + 1;
@@ -1080,7 +1194,7 @@ static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_
   p.force = 1;
   p.t = done - 1;
   p.t0 = t0;
-  lazy_pass<T>(p, true, s);
+  if (int rc = lazy_pass<T>(p, true, s)) return rc;
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
 }
@@ -1350,12 +1464,12 @@ int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long 
 }
 
 template <typename T>
-static void lazy_step_t(const DenseParams& p, bool pivcol, bool flush, cudaStream_t s) {
+static int lazy_step_t(const DenseParams& p, bool pivcol, bool flush, cudaStream_t s) {
   if (pivcol) {
     const int blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
     lazy_pivcol_kernel<T><<<blocks, 256, 0, s>>>(p);
   }
-  lazy_pass<T>(p, flush, s);
+  return lazy_pass<T>(p, flush, s);
 }
 
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
@@ -1376,12 +1490,14 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   p.t0 = t0;
   p.lazy = 1;
   p.force = force ? 1 : 0;
+  int rc;
   switch (dtype) {
-    case RPLU_F64: lazy_step_t<double>(p, pivcol, flush, s); break;
-    case RPLU_F32: lazy_step_t<float>(p, pivcol, flush, s); break;
-    case RPLU_C128: lazy_step_t<double2>(p, pivcol, flush, s); break;
+    case RPLU_F64: rc = lazy_step_t<double>(p, pivcol, flush, s); break;
+    case RPLU_F32: rc = lazy_step_t<float>(p, pivcol, flush, s); break;
+    case RPLU_C128: rc = lazy_step_t<double2>(p, pivcol, flush, s); break;
     default: set_error("unknown dtype"); return RPLU_ERR_ARG;
   }
+  if (rc) return rc;
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
 }

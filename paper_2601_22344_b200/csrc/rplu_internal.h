@@ -83,7 +83,7 @@ int dense_sweep_launch(int dtype, void* R, long long ld, long long n, long long 
                        void* U, long long ldu, double* masses, DevState* st, long long t,
                        bool update, cudaStream_t s);
 
-constexpr int kLazyMaxBlock = 12;  // longest delayed-update block
+constexpr int kLazyMaxBlock = 16;  // longest delayed-update block
 
 // Delayed-update pieces on a row block, from dense.cu: (pivcol) the pivot
 // column L[:,t] rebuilt from R^(t0) and the pending terms, then the pass
