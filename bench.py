@@ -512,7 +512,7 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": _traffic(cfg, n, flush_share if lazy_block else None),
-                     "kernel": ("lazy_pass_kernel (K3 delayed-update pass + row masses)"
+                     "kernel": ("lazy_pass4_kernel (TMA-fed delayed-update pass + row masses)"
                                 if lazy_block else
                                 "dense_sweep_kernel (K3 fused Schur update + row masses)"),
                      "algorithmic_bytes_per_launch": bytes_per_launch,

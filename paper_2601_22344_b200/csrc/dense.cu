@@ -602,6 +602,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2}], [%3], %4;\n" ::"l"(map),
+      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 template <typename T, int QC>
 struct LazyTma {
   static constexpr int TX = 64, RPT = 8, ROWS = 32, NCW = 8;  // NCW consumer warps
@@ -650,7 +664,6 @@ __global__ void __launch_bounds__(288, 1)
   const long long n = p.n, m = p.m, ld = p.ld;
   const long long nchunks = (m + CW - 1) / CW;
   const long long nblocks = (n + ROWS - 1) / ROWS;
-  T* R = reinterpret_cast<T*>(p.R);
   const T* Lt = reinterpret_cast<const T*>(p.Lt);
 
   if (warp == C::NCW) {  // producer warp: one elected lane issues two TMA loads per stage
@@ -660,11 +673,28 @@ __global__ void __launch_bounds__(288, 1)
       const uint64_t pol_r = policy_evict_first(), pol_u = policy_evict_last();
       int stage = 0;
       unsigned phase = 0;
+      long long i = 0;  // items (row block, column chunk) issued by this CTA
+      // FLUSH: the consumers write the updated tile back into its stage; the
+      // stage's previous occupant (item i - STAGES) is stored with one TMA
+      // store before the stage is refilled (rows / columns outside R are
+      // clipped by the tensor map).
+      auto store_item = [&](long long j) {
+        const long long rbj = blockIdx.x + (j / nchunks) * gridDim.x, cj = j % nchunks;
+        const V* sj = tiles + (size_t)(j % STAGES) * (ROWS + QC) * TX;
+        tma_store_2d(&tmR, (int)(cj * WORDS), (int)(rbj * ROWS), sj, pol_r);
+        bulk_commit();
+      };
       for (long long rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
-        for (long long c = 0; c < nchunks; ++c) {
+        for (long long c = 0; c < nchunks; ++c, ++i) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], (unsigned)C::STAGE);
           V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
+          if constexpr (FLUSH) {
+            if (i >= STAGES) {
+              store_item(i - STAGES);
+              bulk_wait_read_all();  // the store has read the stage
+            }
+          }
+          mbar_expect_tx(&full[stage], (unsigned)C::STAGE);
           tma_load_2d(st, &tmR, (int)(c * WORDS), (int)(rb * ROWS), &full[stage], pol_r);
           tma_load_2d(st + ROWS * TX, &tmU, (int)(c * WORDS), (int)p.t0, &full[stage], pol_u);
           if (++stage == STAGES) {
@@ -672,6 +702,13 @@ __global__ void __launch_bounds__(288, 1)
             phase ^= 1;
           }
         }
+      }
+      if constexpr (FLUSH) {
+        for (long long j = i > STAGES ? i - STAGES : 0; j < i; ++j) {
+          mbar_wait(&empty[j % STAGES], (unsigned)((j / STAGES) & 1));
+          store_item(j);
+        }
+        bulk_wait_all();
       }
     }
     return;
@@ -705,7 +742,7 @@ __global__ void __launch_bounds__(288, 1)
     for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
     for (long long c = 0; c < nchunks; ++c) {
       mbar_wait(&full[stage], phase);
-      const V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
+      V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
       const long long l = c * CW + (long long)tx * VEC;
       if (l < m) {
         V rv[RPT];
@@ -721,6 +758,11 @@ __global__ void __launch_bounds__(288, 1)
             for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
           }
         }
+        if constexpr (FLUSH) {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) st[(ty * RPT + r) * TX + tx] = rv[r];
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // visible to the TMA store
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (VEC == 1 || l + VEC <= m) {
@@ -729,16 +771,12 @@ __global__ void __launch_bounds__(288, 1)
             if (r < nr) {
 #pragma unroll
               for (int e = 0; e < VEC; ++e) acc[r] += S::mass(rv[r].v[e]);
-              if (FLUSH) *reinterpret_cast<V*>(R + (myrow0 + r) * ld + l) = rv[r];
             }
           }
         } else {  // last, partial vector of a row (m % VEC columns)
           for (int r = 0; r < RPT; ++r) {
             if (r < nr) {
-              for (int e = 0; e < VEC && l + e < m; ++e) {
-                acc[r] += S::mass(rv[r].v[e]);
-                if (FLUSH) R[(myrow0 + r) * ld + l + e] = rv[r].v[e];
-              }
+              for (int e = 0; e < VEC && l + e < m; ++e) acc[r] += S::mass(rv[r].v[e]);
             }
           }
         }
@@ -1128,17 +1166,16 @@ static int lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
   return flush ? launch_lazy_pass4_f<T, true>(p, s) : launch_lazy_pass4_f<T, false>(p, s);
 }
 
-// Default flush interval: the pass is HBM-bound up to q ~ 3 pending terms and
-// then grows ~0.12 ms per term at C3 while a flush costs a full write of R;
-// the per-step minimum on B200 is at 5 (fp64; measured 1.25 / 1.23 / 1.26 /
-// 1.38 ms for q = 1..4, 2.7 ms for a flush), overridable with
-// RPLU_LAZY_BLOCK.
-// (Applying the pending terms as single FMAs instead of the reference's
-// multiply-then-subtract was measured and gives no gain at any block: the
-// pass is not FP64-throughput bound; profiles/r01/fused_terms_experiment.txt.)
+// Default flush interval, from the measured per-q pass times of the TMA-fed
+// pass at C3 (profiles/r01/pass4_q_launches_summary.txt): a read pass is
+// HBM-bound at ~1.19 ms up to q ~ 5 pending terms, then FP64-bound at ~0.115
+// ms per term (2 FP64 operations per element and term, 76% of the FP64
+// pipe), while a flush costs ~2.9 ms; the per-step minimum is at b = 7..8
+// for fp64 (643 steps/s), 6 for fp32 and 5 for complex128
+// (profiles/r01/sweep_lazy_block_tma_*.txt).  RPLU_LAZY_BLOCK overrides.
 template <typename T>
 static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 3 : (sizeof(T) == 4 ? 4 : 5);  // fp32: 1064 steps/s at 4
+  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 8);
   int b = env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }

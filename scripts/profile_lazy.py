@@ -1,4 +1,5 @@
-"""C3 fp64 delayed-update run of 12 steps (default flush interval): for ncu of the lazy pass."""
+"""C3 delayed-update run for ncu of the lazy pass: argv[1] = f64|f32|c128,
+PROFILE_STEPS steps (default 12) at the flush interval RPLU_LAZY_BLOCK."""
 import os
 import sys
 
@@ -8,8 +9,11 @@ import torch  # noqa: E402
 import paper_2601_22344_b200 as rp  # noqa: E402
 from paper_2601_22344_b200 import gen  # noqa: E402
 
-dt = torch.float32 if (len(sys.argv) > 1 and sys.argv[1] == "f32") else torch.float64
-A = gen.c3_dense_device(0, n=32768, dtype=dt)
-rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), 12, update="lazy")
+name = sys.argv[1] if len(sys.argv) > 1 else "f64"
+dt = {"f64": torch.float64, "f32": torch.float32, "c128": torch.complex128}[name]
+n = int(os.environ.get("PROFILE_N", "32768"))
+A = gen.c3_dense_device(0, n=n, dtype=torch.float64).to(dt)
+steps = int(os.environ.get("PROFILE_STEPS", "12"))
+rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), steps, update="lazy")
 torch.cuda.synchronize()
 print("profile_lazy ok")
