@@ -433,10 +433,12 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     clocks.start()
     time.sleep(0.3)
     stats = []
-    # Small residuals run as one CUDA graph per elimination (host-launch
-    # bound otherwise); graph-recorded events cannot be timed, so for them the
-    # K3 launch durations come from a second pass of the same K runs with
-    # per-launch events (plain stream launches).  Large residuals: one pass.
+    # The timed region runs the public call as a user would (no per-launch
+    # events: small residuals run as one CUDA graph per elimination, and the
+    # event records between the ~5 launches of a pivot step would add ~4% at
+    # C3).  The per-kernel durations behind `roofline` come from a second
+    # pass of the same K runs with CUDA events around every launch on the
+    # launching stream.
     graphable = n * n <= 64 * 1024 * 1024
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -446,14 +448,13 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     ev0.record()
     for _ in range(args.steps):
         for _ in range(reps):
-            tr = one_run(time_kernels=not graphable)
+            tr = one_run()
             stats.append(tr.kernel_stats)
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
     timed_launches = sum(s["kernel_launches"] for s in stats)
-    if graphable:
-        stats = [one_run(time_kernels=True).kernel_stats for _ in range(args.steps)]
+    stats = [one_run(time_kernels=True).kernel_stats for _ in range(args.steps)]
     clk = clocks.stop()
     pivots_done = tr.steps
     value = args.steps * reps * pivots_done / (total_ms / 1e3)
@@ -518,7 +519,9 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "update": (f"delayed (read R per step, write every {lazy_block} steps)"
                                 if lazy_block else "eager (read + write R per step)"),
-                     "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src},
+                     "avg_launch_ms": avg_s * 1e3, "peak_source": peak_src,
+                     "launch_timing": (f"CUDA events around every launch on the launching "
+                                       f"stream, second pass of the same {args.steps} runs")},
         "step_breakdown_ms": {"sweep_per_pivot": sweep_ms / sweep_n,
                               "select_per_pivot": select_ms / (len(stats) * (pivots_done + 1)),
                               "total_per_pivot": total_ms / (args.steps * reps * pivots_done)},
