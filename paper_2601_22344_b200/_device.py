@@ -119,3 +119,22 @@ def matvec(t, v, adjoint=False):
         vt = vt.to(torch.float64)
     r = (tt.conj().T @ vt) if adjoint else (tt @ vt)
     return r.cpu().numpy()
+
+
+_PINNED_MIN_BYTES = 1 << 20
+
+
+def to_numpy(t):
+    """Device tensor -> numpy through page-locked host memory.
+
+    A device->pageable copy into freshly allocated numpy memory runs at
+    ~2 GB/s on the B200 boxes (measured: 121 ms for L and U at C3); a copy
+    into a block of torch's caching pinned-host allocator runs at PCIe speed
+    and the numpy result is a view of that block (kept alive by the array).
+    """
+    if not t.is_cuda or t.numel() * t.element_size() < _PINNED_MIN_BYTES:
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+

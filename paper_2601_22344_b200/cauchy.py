@@ -363,7 +363,7 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
         A = torch.stack([s[2] for s in steps_dev])
         tr.steps_device = (C, R, A)
         if host_steps:
-            Ch, Rh, Ah = C.cpu().numpy(), R.cpu().numpy(), A.cpu().numpy()
+            Ch, Rh, Ah = _device.to_numpy(C), _device.to_numpy(R), A.cpu().numpy()
             tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(len(steps_dev))]
     return tr
 
@@ -436,6 +436,6 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
     if C is not None:
         tr.steps_device = (C, R, A)
         if host_steps and k:
-            Ch, Rh, Ah = C[:k].cpu().numpy(), R[:k].cpu().numpy(), A[:k].cpu().numpy()
+            Ch, Rh, Ah = _device.to_numpy(C[:k]), _device.to_numpy(R[:k]), A[:k].cpu().numpy()
             tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(k)]
     return tr

@@ -77,7 +77,7 @@ class EliminationTrace:
     def residual(self):
         r = self._residual
         if self._host and isinstance(r, torch.Tensor):
-            r = self._residual = r.cpu().numpy()
+            r = self._residual = _device.to_numpy(r)
         return r
 
     @property
@@ -180,8 +180,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     if return_device:
         L_out, U_out = Ld, Ud
     else:
-        L_out = Lt[:k].cpu().numpy().T
-        U_out = Ud.cpu().numpy()
+        L_out = _device.to_numpy(Lt[:k]).T
+        U_out = _device.to_numpy(Ud.contiguous())
     trace = EliminationTrace(
         pivots=piv, L=L_out, U=U_out, resid_fro=resid[:k + 1].copy(), residual=R, steps=k,
         resid_trace=None, clean_early_stop=bool(out.clean_early_stop),
