@@ -58,6 +58,8 @@ extern "C" {
 #define RPLU_FLAG_LAZY 4         /* dense: force the delayed-update loop */
 #define RPLU_FLAG_EAGER 8        /* dense: force the eager (update every step) loop;
                                     default: delayed updates when R exceeds L2 */
+#define RPLU_FLAG_STEPWISE 16   /* dense: per-step launches even where the whole loop would run
+                                    as one persistent cooperative launch */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0

@@ -34,6 +34,7 @@ FLAG_TIME_KERNELS = 1
 FLAG_NO_GRAPH = 2
 FLAG_LAZY = 4
 FLAG_EAGER = 8
+FLAG_STEPWISE = 16
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -244,6 +244,10 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
   const T* R = reinterpret_cast<const T*>(p.R);
   const double* masses = p.masses;
   auto wrow = [&](long long k) { return masses[k]; };
+  // the step's two uniforms, loaded before the CDF build (latency overlap)
+  const long long uc0 = st->ucount;
+  const bool pre = p.rule == RPLU_RULE_RPLU && uc0 + 2 <= p.n_uniforms;
+  const double u1p = pre ? p.uniforms[uc0] : 0.0, u2p = pre ? p.uniforms[uc0 + 1] : 0.0;
 
   Cdf<B> cr = cdf_build<B>(wrow, n, sm);
   const double total = cr.total;
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
   __syncthreads();
   if (s_stop) return;
 
-  long long uc = st->ucount;
+  long long uc = uc0;
   long long near = 0;
   long long i = 0, j = 0;
   T a = S::zero();
@@ -283,8 +287,8 @@ __global__ void __launch_bounds__(1024) dense_select_kernel(DenseParams p) {
         if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
         return;
       }
-      const double u1 = p.uniforms[uc];
-      const double u2 = p.uniforms[uc + 1];
+      const double u1 = attempt == 0 ? u1p : p.uniforms[uc];
+      const double u2 = attempt == 0 ? u2p : p.uniforms[uc + 1];
       uc += 2;
       i = cdf_find<B>(wrow, n, cr, u1, sm);
       // near-boundary accounting for the row draw
@@ -942,6 +946,296 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Shared-memory-resident loop for small residuals (C1: 2000^2 fp64 = 32 MB =
+// 148 SMs x 216 KB): the whole elimination is ONE cooperative launch of one
+// 1024-thread CTA per SM, and each CTA keeps its contiguous block of rows of
+// R in shared memory for the whole run, so a pivot step moves no residual
+// bytes through L2 or HBM at all.  Per step:
+//   1. every CTA draws the row from the n masses (identical code and data:
+//      identical draws everywhere; CTA 0 alone writes the outputs);
+//   2. the CTA holding row i writes it to U[t,:] (an output anyway) and
+//      publishes it with a release counter; the others acquire it;
+//   3. every CTA draws the column from U[t,:] and updates its own rows in
+//      shared memory (pivot-column entries captured first), leaving the
+//      masses of R^(t+1) in a double-buffered global array;
+//   4. one grid barrier.
+// R is written back once, after the last step.  The CDF uses the same
+// 1024-thread layout as dense_select_kernel; masses are summed in a fixed
+// order (per-thread vector, warp tree, 32 warps in order).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
+  while (ld_acquire_u32(c) < target) {
+  }
+}
+// sync[0]: grid-barrier arrivals
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    wait_count(bar, target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct ResidentLayout {
+  int rows;     // rows per CTA (max)
+  size_t off_l, off_red, bytes;
+};
+template <typename T>
+__host__ __device__ inline ResidentLayout resident_layout(long long n, long long ld, int grid) {
+  ResidentLayout L;
+  L.rows = (int)((n + grid - 1) / grid);
+  const size_t rbytes = (size_t)L.rows * (size_t)ld * sizeof(T);
+  L.off_l = (rbytes + 15) & ~size_t(15);
+  L.off_red = (L.off_l + sizeof(T) * L.rows + 15) & ~size_t(15);
+  L.bytes = L.off_red + sizeof(double) * 32 * L.rows;
+  return L;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1)
+    dense_resident_kernel(DenseParams p, double* masses2, unsigned* sync, long long* trace) {
+  using S = Scalar<T>;
+  constexpr int B = 1024, VEC = S::kVec, NW = B / 32;
+  using V = VecT<T, VEC>;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ CdfSmem<B> sm;
+  __shared__ int s_stop;
+  DevState* st = p.st;
+  const bool lead = blockIdx.x == 0;
+  const unsigned G = gridDim.x;
+  const long long n = p.n, m = p.m, ld = p.ld;
+  const ResidentLayout lay = resident_layout<T>(n, ld, (int)G);
+  T* Rs = reinterpret_cast<T*>(dsm);  // [rows][ld]
+  T* lvals = reinterpret_cast<T*>(dsm + lay.off_l);
+  double* red = reinterpret_cast<double*>(dsm + lay.off_red);  // [NW][rows]
+  T* R = reinterpret_cast<T*>(p.R);
+  T* Lt = reinterpret_cast<T*>(p.Lt);
+  const long long r0 = (long long)blockIdx.x * lay.rows;
+  const int nr = (int)max(0LL, min((long long)lay.rows, n - r0));
+  double* mbuf[2] = {p.masses, masses2};
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long ldv = ld / VEC;  // 16-byte vectors per row (ld is a multiple of VEC)
+  const int tv = threadIdx.x;      // this thread's column vector (m <= 1024 * VEC)
+  const bool has_v = (long long)tv * VEC < m;
+
+  // load the block's rows (16-byte vectors)
+  for (long long k = threadIdx.x; k < (long long)nr * ldv; k += B)
+    reinterpret_cast<V*>(Rs)[k] = reinterpret_cast<const V*>(R + r0 * ld)[k];
+  __syncthreads();
+
+  // masses of the block's rows (with the update of step t when upd)
+  // The 32 lanes' partial masses of 16 rows are reduced by recursive halving
+  // (16 shuffles + 16 adds per lane instead of 16 separate warp trees); lane
+  // 2q ends with the warp's sum for row q of the chunk.
+  auto rows_pass = [&](bool upd, const V& pv, double* mout) {
+    for (int c0 = 0; c0 < nr; c0 += 16) {
+      double c[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        c[r] = 0.0;
+        if (c0 + r < nr && has_v) {
+          V x = reinterpret_cast<V*>(Rs + (long long)(c0 + r) * ld)[tv];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            if ((long long)tv * VEC + e < m) {
+              if (upd) x.v[e] = S::sub_outer(x.v[e], lvals[c0 + r], pv.v[e]);
+              c[r] += S::mass(x.v[e]);
+            }
+          }
+          if (upd) reinterpret_cast<V*>(Rs + (long long)(c0 + r) * ld)[tv] = x;
+        }
+      }
+#pragma unroll
+      for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+          const double send = up ? c[k] : c[k + h];
+          const double keep = up ? c[k + h] : c[k];
+          c[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      c[0] += __shfl_xor_sync(0xffffffffu, c[0], 1);
+      const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                    ((lane >> 1) & 1);
+      if ((lane & 1) == 0 && c0 + q < nr) red[w * lay.rows + c0 + q] = c[0];
+    }
+    __syncthreads();
+    for (int r = w; r < nr; r += NW) {  // row r: the 32 warp sums, one per lane
+      const double sv = warp_sum(red[lane * lay.rows + r]);
+      if (lane == 0) mout[r0 + r] = sv;
+    }
+  };
+
+  unsigned nbar = 0;
+  rows_pass(false, V{}, mbuf[0]);
+  grid_barrier(sync, G * (++nbar));
+
+  long long uc = 0, near = 0;
+  double fro0 = 0.0;
+  auto mark = [&](long long t, int k) {  // phase timestamps (diagnostics only)
+    if (trace && lead && threadIdx.x == 0 && t < 1024) {
+      long long v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      trace[8 * t + k] = v;
+    }
+  };
+  for (long long t = 0;; ++t) {
+    mark(t, 0);
+    const bool pre = p.rule == RPLU_RULE_RPLU && uc + 2 <= p.n_uniforms;
+    const double u1p = pre ? p.uniforms[uc] : 0.0, u2p = pre ? p.uniforms[uc + 1] : 0.0;
+    const double* masses = mbuf[t & 1];
+    auto wrow = [&](long long k) { return __ldcg(masses + k); };
+    Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+    mark(t, 4);
+    const double total = cr.total;
+    const double resid = sqrt(total);
+    if (t == 0) fro0 = resid;
+    if (threadIdx.x == 0) {
+      int stop = 0, status = kRunning;
+      if (t > 0 && p.stop_tol > 0.0 && resid <= p.stop_tol * fro0) {
+        status = kTolStop;
+        stop = 1;
+      } else if (t >= p.steps) {
+        stop = 1;
+      } else if (resid == 0.0) {
+        status = kCleanStop;
+        stop = 1;
+      }
+      if (lead) {
+        p.resid[t] = resid;
+        if (t == 0) st->fro0 = resid;
+        if (stop) {
+          st->status = status;
+          st->active = 0;
+          st->ucount = uc;
+          st->near_boundary = near;
+        }
+      }
+      s_stop = stop;
+    }
+    __syncthreads();
+    if (s_stop) break;
+
+    T* urow = reinterpret_cast<T*>(p.U) + t * p.ldu;
+    long long i = 0, j = 0;
+    T a = S::zero();
+    V pv{};
+    bool fail = false;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      double u2 = 0.0;
+      if (p.rule == RPLU_RULE_RPLU) {
+        if (uc + 2 > p.n_uniforms) {
+          if (lead && threadIdx.x == 0) {
+            st->status = kUniformsExhausted;
+            st->active = 0;
+            st->ucount = uc;
+            st->near_boundary = near;
+          }
+          fail = true;
+          break;
+        }
+        const double u1 = attempt == 0 ? u1p : p.uniforms[uc];
+        u2 = attempt == 0 ? u2p : p.uniforms[uc + 1];
+        uc += 2;
+        i = cdf_find<B>(wrow, n, cr, u1, sm);
+        if (threadIdx.x == 0) {
+          const double tol = kNearBoundaryRel * total, tg = u1 * total;
+          if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+        }
+      } else {
+        i = block_argmax<B>(wrow, n, nullptr);
+      }
+      mark(t, 5);
+      // the holder of row i publishes it as U[t,:]; the others acquire it
+      const unsigned seq = (unsigned)(2 * t + attempt + 1);
+      if (i >= r0 && i < r0 + nr) {
+        const T* src = Rs + (i - r0) * ld;
+        for (long long k = threadIdx.x; k < m; k += B) urow[k] = src[k];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          st_release_u32(sync + 1, seq);
+        }
+      } else {
+        if (threadIdx.x == 0) wait_count(sync + 1, seq);
+        __syncthreads();
+      }
+      mark(t, 6);
+      if (has_v) {  // this thread's slice of the pivot row, for the update
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          pv.v[e] = ((long long)tv * VEC + e < m) ? __ldcg(urow + (long long)tv * VEC + e) : S::zero();
+      }
+      if (p.rule == RPLU_RULE_RPLU) {
+        auto wcol = [&](long long k) { return S::weight(__ldcg(urow + k)); };
+        Cdf<B> cc = cdf_build<B>(wcol, m, sm);
+        mark(t, 7);
+        j = cdf_find<B>(wcol, m, cc, u2, sm);
+        if (threadIdx.x == 0) {
+          const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+          if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+        }
+      } else {
+        auto wabs = [&](long long k) { return S::absval(__ldcg(urow + k)); };
+        j = block_argmax<B>(wabs, m, nullptr);
+      }
+      a = __ldcg(urow + j);
+      if (!S::is_zero(a)) break;
+      if (attempt == 1 || p.rule != RPLU_RULE_RPLU) {
+        if (lead && threadIdx.x == 0) {
+          st->status = kZeroPivot;
+          st->active = 0;
+          st->err_i = i;
+          st->err_j = j;
+          st->ucount = uc;
+          st->near_boundary = near;
+        }
+        fail = true;
+        break;
+      }
+      __syncthreads();
+    }
+    if (fail) break;
+    mark(t, 1);
+    if (lead && threadIdx.x == 0) {
+      st->pi = i;
+      st->pj = j;
+      store_coef<T>(st, a);
+      p.pivots[2 * t] = i;
+      p.pivots[2 * t + 1] = j;
+      st->done = t + 1;
+    }
+    // pivot-column entries of the block's rows, before any row is written
+    const typename S::coef_t cf = S::make_coef(a);
+    if (threadIdx.x < nr) {
+      const T lv = S::scale(Rs[(long long)threadIdx.x * ld + j], cf);
+      lvals[threadIdx.x] = lv;
+      Lt[t * n + r0 + threadIdx.x] = lv;
+    }
+    __syncthreads();
+    rows_pass(true, pv, mbuf[(t + 1) & 1]);
+    mark(t, 2);
+    grid_barrier(sync, G * (++nbar));
+    mark(t, 3);
+  }
+  // the residual R^(k) back to HBM
+  __syncthreads();
+  for (long long k = threadIdx.x; k < (long long)nr * ldv; k += B)
+    reinterpret_cast<V*>(R + r0 * ld)[k] = reinterpret_cast<const V*>(Rs)[k];
+}
+
+// ---------------------------------------------------------------------------
 // host-side launchers
 
 __global__ void init_state_kernel(DevState* st) {
@@ -1236,6 +1530,83 @@ static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_
   return RPLU_OK;
 }
 
+// Shared-memory bytes the resident loop needs for this residual (0: the
+// residual does not fit in the SMs' shared memory or a row is too long).
+template <typename T>
+static size_t resident_bytes(long long n, long long m, long long ld) {
+  if (m > 1024LL * Scalar<T>::kVec || n <= 0) return 0;
+  static const size_t cap = [] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, dense_resident_kernel<T>);
+    const long long c = (long long)optin - (long long)fa.sharedSizeBytes - 1024;
+    return (size_t)(c > 0 ? c : 0);
+  }();
+  const ResidentLayout L = resident_layout<T>(n, ld, sm_count());
+  return L.bytes <= cap ? L.bytes : 0;
+}
+
+template <typename T>
+static int launch_persistent(rplu_ctx* ctx, const DenseParams& p, cudaStream_t s,
+                             cudaEvent_t* ev) {
+  auto kern = dense_resident_kernel<T>;
+  const int smem = (int)resident_bytes<T>(p.n, p.m, p.ld);
+  static int attr_smem = -1;
+  if (smem > attr_smem) {
+    RPLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_smem = smem;
+  }
+  int per_sm = 0;
+  RPLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
+  if (per_sm < 1) {
+    set_error("shared-memory-resident dense loop does not fit on an SM");
+    return RPLU_ERR_CUDA;
+  }
+  int rc;
+  if ((rc = ctx->masses2.ensure(sizeof(double) * (size_t)(p.n > 0 ? p.n : 1)))) return rc;
+  if ((rc = ctx->gbar.ensure(2 * sizeof(unsigned)))) return rc;
+  RPLU_CUDA(cudaMemsetAsync(ctx->gbar.ptr, 0, 2 * sizeof(unsigned), s));
+  DenseParams q = p;
+  double* m2 = reinterpret_cast<double*>(ctx->masses2.ptr);
+  unsigned* sync = reinterpret_cast<unsigned*>(ctx->gbar.ptr);
+  // RPLU_PERSIST_TRACE=1: CTA 0's phase timestamps of the first 1024 steps
+  // (draws / update / barrier), printed to stderr (diagnostics)
+  static const bool tracing = getenv("RPLU_PERSIST_TRACE") != nullptr;
+  long long* trace = nullptr;
+  if (tracing) {
+    RPLU_CUDA(cudaMalloc(&trace, sizeof(long long) * 8 * 1024));
+    RPLU_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 8 * 1024, s));
+  }
+  void* args[] = {&q, &m2, &sync, &trace};
+  const unsigned grid = (unsigned)sm_count();
+  if (ev[0]) RPLU_CUDA(cudaEventRecord(ev[0], s));
+  RPLU_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(1024), args,
+                                        (size_t)smem, s));
+  if (ev[1]) RPLU_CUDA(cudaEventRecord(ev[1], s));
+  if (tracing) {
+    std::vector<long long> h(8 * 1024);
+    RPLU_CUDA(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
+    RPLU_CUDA(cudaStreamSynchronize(s));
+    cudaFree(trace);
+    // 0 start, 4 row CDF built, 5 row drawn, 6 pivot row published/acquired,
+    // 7 column CDF built, 1 column drawn, 2 rows updated, 3 barrier passed
+    const int order[8] = {0, 4, 5, 6, 7, 1, 2, 3};
+    const char* names[7] = {"row cdf", "row find", "publish", "col cdf", "col find", "update", "barrier"};
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long k = 0;
+    for (; k < 1024 && h[8 * k + 3] != 0; ++k)
+      for (int q = 0; q < 7; ++q) acc[q] += (double)(h[8 * k + order[q + 1]] - h[8 * k + order[q]]);
+    if (k > 0) {
+      fprintf(stderr, "[rplu] resident loop, CTA 0, %lld steps (us/step):", k);
+      for (int q = 0; q < 7; ++q) fprintf(stderr, " %s %.2f", names[q], acc[q] / k / 1e3);
+      fprintf(stderr, "\n");
+    }
+  }
+  return RPLU_OK;
+}
+
 int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(a->stream);
   const long long n = a->n, m = a->m, steps = a->steps;
@@ -1303,6 +1674,41 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   else if (lazy_env >= 0) want = lazy_env;
   const bool lazy = a->rule != RPLU_RULE_CPLU && vec_ok && steps >= 2 &&
                     (want == 1 || (want < 0 && (double)n * m * esize > 256.0e6));
+  // Residuals that fit in the SMs' shared memory: the whole loop as one
+  // persistent cooperative launch with R resident on chip (RPLU_PERSIST=0
+  // disables, for comparisons)
+  static const int persist_env = env_int("RPLU_PERSIST", 1);
+  size_t res_bytes = 0;
+  if (!lazy && persist_env != 0 && !(a->flags & RPLU_FLAG_STEPWISE) &&
+      a->rule != RPLU_RULE_CPLU && steps >= 1 && want != 1 && vec_ok) {
+    switch (a->dtype) {
+      case RPLU_F64: res_bytes = resident_bytes<double>(n, m, a->ld); break;
+      case RPLU_F32: res_bytes = resident_bytes<float>(n, m, a->ld); break;
+      case RPLU_C128: res_bytes = resident_bytes<double2>(n, m, a->ld); break;
+    }
+  }
+  const bool persist = res_bytes > 0;
+  if (persist) {
+    cudaEvent_t pe[2] = {nullptr, nullptr};
+    if (tm.on) {
+      RPLU_CUDA(cudaEventCreate(&pe[0]));
+      RPLU_CUDA(cudaEventCreate(&pe[1]));
+    }
+    init_state_kernel<<<1, 1, 0, s>>>(st);
+    switch (a->dtype) {
+      case RPLU_F64: rc = launch_persistent<double>(ctx, p, s, pe); break;
+      case RPLU_F32: rc = launch_persistent<float>(ctx, p, s, pe); break;
+      case RPLU_C128: rc = launch_persistent<double2>(ctx, p, s, pe); break;
+      default: set_error("unknown dtype"); rc = RPLU_ERR_ARG;
+    }
+    if (rc) return rc;
+    launches = 2;
+    if (tm.on) {
+      tm.ev.push_back(pe[0]);
+      tm.ev.push_back(pe[1]);
+      tm.kind.push_back(3);  // whole loop in one launch
+    }
+  } else {
   rc = run_maybe_graph(ctx, s, graph, 0, [&](cudaStream_t q) -> int {
     init_state_kernel<<<1, 1, 0, q>>>(st);
     switch (a->dtype) {
@@ -1320,6 +1726,7 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     return RPLU_ERR_ARG;
   });
   if (rc) return rc;
+  }
 
   DevState hs;
   RPLU_CUDA(cudaMemcpyAsync(&hs, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -1351,7 +1758,11 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     for (size_t q = 0; q < tm.kind.size(); ++q) {
       float ms = 0.f;
       RPLU_CUDA(cudaEventElapsedTime(&ms, tm.ev[2 * q], tm.ev[2 * q + 1]));
-      if (tm.kind[q] >= 1) {
+      if (tm.kind[q] == 3) {  // persistent loop: K1 + every step's update
+        out->sweep_ms += ms;
+        out->sweep_launches += 1;
+        out->sweep_bytes += (double)n * m * esize * (1.0 + 2.0 * (double)done);
+      } else if (tm.kind[q] >= 1) {
         // algorithmic bytes: eager update and lazy flush read + write R,
         // a lazy pass reads it
         const double pass_bytes = (double)n * m * esize * ((lazy && tm.kind[q] == 1) ? 1 : 2);

@@ -161,6 +161,8 @@ struct CdfSmem {
   double wincl[BLOCK / 32];  // CDF value at the end of warp segment w
   long long idx;
   double lo_c, hi_c;
+  double wsel;    // weight of the selected element (when known without a reload)
+  int has_wsel;
   int owner;
 };
 
@@ -224,11 +226,15 @@ __device__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
   if (lane == 0) s.wincl[w] = run;  // segment total (temporarily)
   __syncthreads();
   if (threadIdx.x == 0) {
+    // sequential prefix over the segment totals (all loads issued first)
+    double tv[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) tv[q] = s.wincl[q];
     double e = 0.0;
+#pragma unroll
     for (int q = 0; q < W; ++q) {
-      const double st = s.wincl[q];
       s.wexcl[q] = e;
-      e = e + st;
+      e = e + tv[q];
       s.wincl[q] = e;
     }
   }
@@ -256,16 +262,20 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
                                      double target, CdfSmem<BLOCK>& s) {
   constexpr int W = BLOCK / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    int owner = -1;
-    for (int q = 0; q < W; ++q)
-      if (s.wincl[q] > target) { owner = q; break; }
-    s.owner = owner;
-    if (owner < 0) {
-      // u*total >= every partial sum: searchsorted returns n, clamp to n-1
-      s.idx = n - 1;
-      s.lo_c = c.total;
-      s.hi_c = c.total;
+  if (w == 0) {  // owner = first segment whose running sum exceeds the target
+    static_assert(W <= 32, "one lane per segment");
+    const bool gt = lane < W && s.wincl[lane] > target;
+    const unsigned hit = __ballot_sync(0xffffffffu, gt);
+    const int owner = hit ? __ffs(hit) - 1 : -1;
+    if (lane == 0) {
+      s.owner = owner;
+      s.has_wsel = 0;
+      if (owner < 0) {
+        // u*total >= every partial sum: searchsorted returns n, clamp to n-1
+        s.idx = n - 1;
+        s.lo_c = c.total;
+        s.hi_c = c.total;
+      }
     }
   }
   __syncthreads();
@@ -292,10 +302,13 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
           const int L = __ffs(hit) - 1;
           const double hc = __shfl_sync(0xffffffffu, ck, L);
           const double pc = __shfl_sync(0xffffffffu, ck, L > 0 ? L - 1 : 0);
+          const double wv = __shfl_sync(0xffffffffu, xs[u], L);
           if (lane == 0) {
             s.idx = sb + L;
             s.hi_c = hc;
             s.lo_c = L > 0 ? pc : prev;
+            s.wsel = wv;
+            s.has_wsel = 1;
           }
           done = true;
         } else {
@@ -315,7 +328,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
   __syncthreads();
   long long i = s.idx;
   // walk back over zero weights (rng.py:70-73)
-  double wi = wf(i);
+  const double wi = s.has_wsel ? s.wsel : wf(i);
   __syncthreads();
   if (!(wi > 0.0)) {
     // largest k <= i with w(k) > 0, else smallest k with w(k) > 0

@@ -145,4 +145,6 @@ struct rplu_ctx {
   rplu::DevBuf pivots;      // 2*steps int64
   rplu::DevBuf resid;       // steps+1 doubles
   rplu::DevBuf scratch[8];  // path-specific
+  rplu::DevBuf masses2;     // n doubles (persistent dense loop: double-buffered masses)
+  rplu::DevBuf gbar;        // grid-barrier counters (persistent dense loop)
 };

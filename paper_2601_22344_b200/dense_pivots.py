@@ -103,7 +103,7 @@ def _input_tensor(A, compute_dtype):
 
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
-              return_device=None, time_kernels=False, update="auto"):
+              return_device=None, time_kernels=False, update="auto", persistent=True):
     """Run pivoted elimination for up to ``steps`` pivots (dense_pivots.py:129).
 
     Stops early, with a flag, when the residual Frobenius norm falls to
@@ -119,7 +119,9 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     with CUDA events; results in ``trace.kernel_stats``), ``update``
     ("auto" | "eager" | "lazy": update the residual every step, or apply the
     pending rank-1 terms on the fly and write R every few steps — same bits,
-    half the HBM traffic; "auto" = lazy when R does not fit in L2).
+    half the HBM traffic; "auto" = lazy when R does not fit in L2),
+    ``persistent`` (False: per-step K2/K3 launches even where an L2-resident
+    residual would run the whole loop as one persistent cooperative launch).
     """
     if update not in ("auto", "eager", "lazy"):
         raise ValueError(f"unknown update mode {update!r}")
@@ -163,7 +165,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         n_uniforms=block.values.size if block else 0,
         stream=torch.cuda.current_stream(dev).cuda_stream,
         flags=((_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
-               | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]))
+               | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]
+               | (0 if persistent else _ffi.FLAG_STEPWISE)))
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)

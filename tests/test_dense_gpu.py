@@ -276,6 +276,48 @@ def test_lazy_every_flush_interval_is_bit_identical(dtype, block, cuda_device, m
     np.testing.assert_allclose(z.resid_fro, e.resid_fro, rtol=1e-13)
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.complex128])
+@pytest.mark.parametrize("rule", ["rplu", "c2plu"])
+@pytest.mark.parametrize("n,m,steps", [(2000, 2000, 100), (1001, 1153, 80), (37, 1500, 30),
+                                       (1500, 41, 41)])
+def test_persistent_loop_matches_stepwise(dtype, rule, n, m, steps, cuda_device):
+    """The one-launch persistent loop (L2-resident residuals) against the
+    per-step K2/K3 launches: same pivots, bit-identical L, U and residual."""
+    rs = np.random.default_rng(n * 7 + m)
+    A = rs.standard_normal((n, m)) @ np.diag(0.99 ** np.arange(m))
+    if dtype == torch.complex128:
+        A = A + 1j * rs.standard_normal((n, m))
+    At = torch.from_numpy(A).to("cuda", dtype)
+
+    def mk():
+        return rp.PivotRule("rplu", rp.RngState(9)) if rule == "rplu" else "c2plu"
+
+    s = rp.eliminate(At, mk(), steps, persistent=False)
+    z = rp.eliminate(At, mk(), steps, time_kernels=True)
+    vec = {torch.float64: 2, torch.float32: 4, torch.complex128: 1}[dtype]
+    if m <= 1024 * vec and n * m * At.element_size() <= 30e6:  # fits the SMs' shared memory
+        assert z.kernel_stats["kernel_launches"] <= 3  # init + one loop launch
+    assert z.pivots == s.pivots and z.steps == s.steps
+    assert torch.equal(z.L, s.L) and torch.equal(z.U, s.U)
+    assert torch.equal(z.residual, s.residual)
+    np.testing.assert_allclose(z.resid_fro, s.resid_fro, rtol=1e-13)
+    assert z.uniforms_consumed == s.uniforms_consumed
+
+
+def test_persistent_loop_stops(cuda_device):
+    A = torch.from_numpy(gen.c1_dense(2, n=600, m=512)).cuda()
+    for tol in (0.3, 0.05):
+        e = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(2)), 300, stop_tol=tol,
+                         persistent=False)
+        z = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(2)), 300, stop_tol=tol)
+        assert e.tol_stop and z.tol_stop and z.steps == e.steps and z.pivots == e.pivots
+        assert torch.equal(z.residual, e.residual)
+    B = torch.from_numpy(np.diag(np.arange(1.0, 31.0))).cuda()
+    z = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30)
+    e = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30, persistent=False)
+    assert z.pivots == e.pivots and z.clean_early_stop == e.clean_early_stop
+
+
 @pytest.mark.parametrize("rule", ["rplu", "c2plu"])
 def test_lazy_early_stops_flush_the_residual(rule, cuda_device):
     A = torch.from_numpy(gen.c1_dense(2, n=600, m=512)).cuda()
