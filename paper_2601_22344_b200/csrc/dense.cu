@@ -620,9 +620,12 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-template <typename T, int QC>
+template <typename T, int QC, int TXW = 64>
 struct LazyTma {
-  static constexpr int TX = 64, RPT = 8, ROWS = 32, NCW = 8;  // NCW consumer warps
+  // TXW threads across a (TXW x 16)-byte column chunk x (256 / TXW) groups of
+  // RPT rows: 32 rows x 1 KB (TXW = 64) or 16 rows x 2 KB (TXW = 128)
+  static constexpr int TX = TXW, RPT = 8, ROWS = (256 / TXW) * RPT, NCW = 8;  // NCW consumer warps
+  static constexpr int WPG = TX / 32;                         // warps per row group
   static constexpr int LINE = TX * 16;                        // bytes of one row per stage
   static constexpr int STAGE = (ROWS + QC) * LINE;
   static constexpr int STAGES = (196 * 1024) / STAGE > 8 ? 8 : (196 * 1024) / STAGE;
@@ -636,15 +639,16 @@ struct LazyTma {
 // complex128, 4-byte for fp32), box = 1 KB x 32 rows; tmU: the pending rows
 // U[t0 .. t0+QC) with box 1 KB x QC rows.  Out-of-range rows and columns are
 // zero-filled by the TMA unit, so every stage carries (32 + QC) KB.
-template <typename T, int VEC, bool FLUSH, int QC>
+template <typename T, int VEC, bool FLUSH, int QC, int TXW = 64>
 __global__ void __launch_bounds__(288, 1)
     lazy_pass4_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmR,
                       const __grid_constant__ CUtensorMap tmU) {
   using S = Scalar<T>;
-  using C = LazyTma<T, QC>;
+  using C = LazyTma<T, QC, TXW>;
   using V = VecT<T, VEC>;
   constexpr int TX = C::TX, RPT = C::RPT, ROWS = C::ROWS, STAGES = C::STAGES, CW = TX * VEC;
-  constexpr int WORDS = 1024 / (sizeof(T) == 4 ? 4 : 8);  // box inner extent in map words
+  constexpr int WORDS = C::LINE / (sizeof(T) == 4 ? 4 : 8);  // box inner extent in map words
+  static_assert(WORDS <= 256, "TMA box extent");
   static_assert(sizeof(V) == 16, "16-byte vectors");
   if (!p.force && !p.st->active) return;
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
@@ -736,8 +740,12 @@ __global__ void __launch_bounds__(288, 1)
     if (prev_row0 >= 0 && threadIdx.x < ROWS) {
       const double* rd = red + (buf ^ 1) * C::NCW * RPT;
       const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
-      if (prev_row0 + threadIdx.x < n)
-        p.masses[prev_row0 + threadIdx.x] = rd[(2 * g) * RPT + r] + rd[(2 * g + 1) * RPT + r];
+      if (prev_row0 + threadIdx.x < n) {
+        double sv = rd[(C::WPG * g) * RPT + r];
+#pragma unroll
+        for (int q = 1; q < C::WPG; ++q) sv += rd[(C::WPG * g + q) * RPT + r];
+        p.masses[prev_row0 + threadIdx.x] = sv;
+      }
     }
     const long long myrow0 = row0 + ty * RPT;
     const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
@@ -805,8 +813,12 @@ __global__ void __launch_bounds__(288, 1)
   if (prev_row0 >= 0 && threadIdx.x < ROWS) {
     const double* rd = red + ((k - 1) & 1) * C::NCW * RPT;
     const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
-    if (prev_row0 + threadIdx.x < n)
-      p.masses[prev_row0 + threadIdx.x] = rd[(2 * g) * RPT + r] + rd[(2 * g + 1) * RPT + r];
+    if (prev_row0 + threadIdx.x < n) {
+      double sv = rd[(C::WPG * g) * RPT + r];
+#pragma unroll
+      for (int q = 1; q < C::WPG; ++q) sv += rd[(C::WPG * g + q) * RPT + r];
+      p.masses[prev_row0 + threadIdx.x] = sv;
+    }
   }
 }
 
@@ -1369,14 +1381,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // 2-D map over a row-major (rows x cols) array of element size esize with a
 // row pitch of ld elements; box = 1 KB of columns x box_rows rows.
 static bool make_row_map(CUtensorMap* map, const void* base, int esize, long long rows,
-                         long long cols, long long ld, int box_rows) {
+                         long long cols, long long ld, int box_rows, int box_bytes = 1024) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
   const int w = esize == 4 ? 4 : 8;  // complex128 = pairs of fp64 words
   const int per = esize / w;
   const cuuint64_t dims[2] = {(cuuint64_t)(cols * per), (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)(ld * esize)};
-  const cuuint32_t box[2] = {(cuuint32_t)(1024 / w), (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)(box_bytes / w), (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, w == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
              const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1384,13 +1396,13 @@ static bool make_row_map(CUtensorMap* map, const void* base, int esize, long lon
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, bool FLUSH, int QC>
-static int launch_lazy_pass4_q(const DenseParams& p, cudaStream_t s) {
+template <typename T, bool FLUSH, int QC, int TXW>
+static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
-  using C = LazyTma<T, QC>;
+  using C = LazyTma<T, QC, TXW>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC>,
+    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
@@ -1399,13 +1411,20 @@ static int launch_lazy_pass4_q(const DenseParams& p, cudaStream_t s) {
   if (g <= 0 || p.m <= 0) return RPLU_OK;
   CUtensorMap tmR, tmU;
   const long long urows = p.t0 + QC;  // U rows 0 .. t0+QC-1 exist
-  if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, C::ROWS) ||
-      !make_row_map(&tmU, p.U, (int)sizeof(T), urows, p.m, p.ldu, QC)) {
+  if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, C::ROWS, C::LINE) ||
+      !make_row_map(&tmU, p.U, (int)sizeof(T), urows, p.m, p.ldu, QC, C::LINE)) {
     set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
     return RPLU_ERR_CUDA;
   }
-  lazy_pass4_kernel<T, VEC, FLUSH, QC><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
+  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
   return RPLU_OK;
+}
+
+// (16 rows x 2 KB stages, TXW = 128, were measured no faster than 32 rows x
+// 1 KB at C3 fp64: 623 vs 627 steps/s at b = 6)
+template <typename T, bool FLUSH, int QC>
+static int launch_lazy_pass4_q(const DenseParams& p, cudaStream_t s) {
+  return launch_lazy_pass4_w<T, FLUSH, QC, 64>(p, s);
 }
 
 template <typename T, bool FLUSH>
@@ -1465,11 +1484,13 @@ static int lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
 // HBM-bound at ~1.19 ms up to q ~ 5 pending terms, then FP64-bound at ~0.115
 // ms per term (2 FP64 operations per element and term, 76% of the FP64
 // pipe), while a flush costs ~2.9 ms; the per-step minimum is at b = 7..8
-// for fp64 (643 steps/s), 6 for fp32 and 5 for complex128
-// (profiles/r01/sweep_lazy_block_tma_*.txt).  RPLU_LAZY_BLOCK overrides.
+// for fp64 at full clocks (646 / 650 steps/s) and at b = 6 on a box whose
+// power cap held the SMs at ~1.45 GHz (627 vs 619 at 8): 7 is the default;
+// 6 for fp32 and 5 for complex128 (profiles/r01/sweep_lazy_block_tma_*.txt).
+// RPLU_LAZY_BLOCK overrides.
 template <typename T>
 static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 8);
+  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 7);
   int b = env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
