@@ -170,6 +170,10 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)
+    # host results: pin their buffers while the loop runs
+    pre = None
+    if not return_device and steps * (n + m) * src.element_size() >= (1 << 20):
+        pre = _device.PinnedPrefetch([((steps, n), src.dtype), ((steps, m), src.dtype)])
     status = c._lib.rplu_dense_run(c.handle, ctypes.byref(args), ctypes.byref(out))
     if block is not None:
         # the reference consumed exactly these draws, even when it raised
@@ -183,8 +187,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     if return_device:
         L_out, U_out = Ld, Ud
     else:
-        L_out = _device.to_numpy(Lt[:k]).T
-        U_out = _device.to_numpy(Ud.contiguous())
+        L_out = _device.copy_to_host(Lt[:k], pre.get(0) if pre else None).T
+        U_out = _device.copy_to_host(Ud, pre.get(1) if pre else None)
     trace = EliminationTrace(
         pivots=piv, L=L_out, U=U_out, resid_fro=resid[:k + 1].copy(), residual=R, steps=k,
         resid_trace=None, clean_early_stop=bool(out.clean_early_stop),
