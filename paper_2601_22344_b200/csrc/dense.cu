@@ -1484,13 +1484,14 @@ static int lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
 // HBM-bound at ~1.19 ms up to q ~ 5 pending terms, then FP64-bound at ~0.115
 // ms per term (2 FP64 operations per element and term, 76% of the FP64
 // pipe), while a flush costs ~2.9 ms; the per-step minimum is at b = 7..8
-// for fp64 at full clocks (646 / 650 steps/s) and at b = 6 on a box whose
-// power cap held the SMs at ~1.45 GHz (627 vs 619 at 8): 7 is the default;
-// 6 for fp32 and 5 for complex128 (profiles/r01/sweep_lazy_block_tma_*.txt).
+// for fp64 at full clocks (646 / 650 steps/s, 642 at 6) and at b = 6 on the
+// boxes whose power cap held the SMs at ~1.45 GHz (624-627 vs 619-622 at 7-8):
+// with b = 6 every read pass stays HBM-bound (q <= 5), so 6 is the default;
+// 6 for fp32 and 5 for complex128 (profiles/r01/sweep_lazy_block_*.txt).
 // RPLU_LAZY_BLOCK overrides.
 template <typename T>
 static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 7);
+  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 6);
   int b = env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
