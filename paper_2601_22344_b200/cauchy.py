@@ -419,6 +419,11 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
                          bound_maxes=bmax.ctypes.data_as(f64p),
                          bound_sums=bsum.ctypes.data_as(f64p))
     c = _device.ctx(dev)
+    pre = None
+    if C is not None and host_steps and rank * (n + m) * 16 >= (1 << 20):
+        # pin the host copies of the kept steps while the loop runs
+        pre = _device.PinnedPrefetch([((rank, n), torch.complex128),
+                                      ((rank, m), torch.complex128)])
     status = c._lib.rplu_cauchy_run(c.handle, ctypes.byref(args), ctypes.byref(out))
     if block is not None:
         block.commit(out.uniforms_consumed)
@@ -436,6 +441,8 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
     if C is not None:
         tr.steps_device = (C, R, A)
         if host_steps and k:
-            Ch, Rh, Ah = _device.to_numpy(C[:k]), _device.to_numpy(R[:k]), A[:k].cpu().numpy()
+            Ch = _device.copy_to_host(C[:k], pre.get(0) if pre else None)
+            Rh = _device.copy_to_host(R[:k], pre.get(1) if pre else None)
+            Ah = A[:k].cpu().numpy()
             tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(k)]
     return tr

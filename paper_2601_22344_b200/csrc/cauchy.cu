@@ -55,6 +55,13 @@ struct CauchyParams {
   // sharded path: the pivot message [(i_global, 0), x_i, G_i[0..P)] the row
   // and snapshot kernels read instead of G / x (null on one GPU)
   const double2* psrc;
+  // per-row-block arrival counters: the last split CTA of a row block sums
+  // the split partials into masses (fixed split order) -- no separate launch
+  unsigned* blk_count;
+  // max_j |r_j| of the step's pivot row as the bits of a non-negative double
+  // (atomicMax in the row kernel; read and cleared by the column select)
+  unsigned long long* rmax_bits;
+  double2* gsnap;    // G_i, B_j before the update (written by the column select)
 };
 
 // ---------------------------------------------------------------------------
@@ -135,6 +142,28 @@ __global__ void __launch_bounds__(256) cauchy_mass_kernel(CauchyParams q) {
   for (int r = 0; r < RPT; ++r) {
     long long i = row_base + threadIdx.x + (long long)r * NT;
     if (valid[r]) q.partial[(long long)blockIdx.y * q.n + i] = acc[r];
+  }
+  if (q.splits > 1 && q.blk_count) {
+    // the last of the row block's split CTAs to finish forms the masses
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      s_last = atomicAdd(&q.blk_count[blockIdx.x], 1u) == (unsigned)(q.splits - 1);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const long long i = row_base + threadIdx.x + (long long)r * NT;
+        if (valid[r]) {
+          double sv = 0.0;
+          for (int k = 0; k < q.splits; ++k) sv += __ldcg(q.partial + (long long)k * q.n + i);
+          q.masses[i] = sv;
+        }
+      }
+      if (threadIdx.x == 0) q.blk_count[blockIdx.x] = 0u;
+    }
   }
 }
 
@@ -226,6 +255,7 @@ __global__ void cauchy_row_kernel(CauchyParams q) {
     for (int l = 0; l < P; ++l) gi[l] = q.G[i * P + l];
     xi = q.x[i];
   }
+  double amax = 0.0;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < q.m;
        j += (long long)gridDim.x * blockDim.x) {
     double re = 0.0, im = 0.0;
@@ -241,6 +271,13 @@ __global__ void cauchy_row_kernel(CauchyParams q) {
     q.rbuf[j] = r;
     const double a = cabs_np(r);
     q.wbuf[j] = a * a;
+    amax = fmax(amax, a);
+  }
+  if (q.rmax_bits) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0 && amax > 0.0)
+      atomicMax(q.rmax_bits, (unsigned long long)__double_as_longlong(amax));
   }
 }
 
@@ -257,15 +294,20 @@ __global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q)
   const double* w = q.wbuf;
   auto wcol = [&](long long k) { return w[k]; };
   auto wabs = [&](long long k) { return cabs_np(q.rbuf[k]); };
-  // max |r| for the relative threshold
-  double mx = 0.0;
-  for (long long k = threadIdx.x; k < m; k += B) mx = fmax(mx, wabs(k));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
-  __syncthreads();
+  // max |r| for the relative threshold (from the row kernel's atomic max,
+  // else scanned here)
   double rmax = 0.0;
-  for (int k = 0; k < B / 32; ++k) rmax = fmax(rmax, s_max[k]);
+  if (q.rmax_bits) {
+    rmax = __longlong_as_double((long long)__ldcg(q.rmax_bits));
+  } else {
+    double mx = 0.0;
+    for (long long k = threadIdx.x; k < m; k += B) mx = fmax(mx, wabs(k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    for (int k = 0; k < B / 32; ++k) rmax = fmax(rmax, s_max[k]);
+  }
   const double thr = kPivotRelTol * rmax;
   long long j;
   long long uc = st->ucount;
@@ -330,6 +372,12 @@ __global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q)
     q.cols[t] = j;
     if (q.Aout) q.Aout[t] = a;
     st->done = t + 1;
+    if (q.rmax_bits) *q.rmax_bits = 0ull;  // for the next step's row kernel
+  }
+  if (q.gsnap && threadIdx.x < q.p) {  // G_i and B_j before the update
+    const int l = threadIdx.x;
+    q.gsnap[l] = q.psrc ? q.psrc[2 + l] : q.G[st->pi * q.p + l];
+    q.gsnap[q.p + l] = q.Bt[j * q.p + l];
   }
 }
 
@@ -402,10 +450,12 @@ __global__ void cauchy_snapshot_kernel(CauchyParams q, double2* gsnap) {
 // launch helpers
 
 static int choose_splits(long long n, long long m, int rows_per_cta, int sm_count) {
+  // latency-bound sizes: about two CTAs per SM (a whole number of CTAs per
+  // SM, so no SM runs a lone extra CTA), each with >= 64 columns
   long long row_blocks = (n + rows_per_cta - 1) / rows_per_cta;
-  long long want = 4LL * sm_count;  // CTAs for latency-bound sizes
+  long long want = 2LL * sm_count;
   long long s = (want + row_blocks - 1) / row_blocks;
-  long long max_s = (m + 255) / 256;  // at least 256 columns per split
+  long long max_s = (m + 63) / 64;
   if (s > max_s) s = max_s;
   if (s < 1) s = 1;
   if (s > 1024) s = 1024;
@@ -509,6 +559,14 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   q.st = reinterpret_cast<DevState*>(ctx->state.ptr);
   q.uniforms = reinterpret_cast<const double*>(ctx->uniforms.ptr);
   q.n_uniforms = nu;
+  // fused per-step bookkeeping: split sums in K5, row max in K6a, snapshot
+  // in the column select (no sum / snapshot launches)
+  const long long mass_blocks = (n + rows_per_cta(p) - 1) / rows_per_cta(p);
+  const size_t sync_bytes = sizeof(unsigned long long) * (size_t)(mass_blocks + 1);
+  if ((rc = ctx->csync.ensure(sync_bytes))) return rc;
+  q.rmax_bits = reinterpret_cast<unsigned long long*>(ctx->csync.ptr);
+  q.blk_count = reinterpret_cast<unsigned*>(q.rmax_bits + 1);
+  q.gsnap = gsnap;
   long long* piv = reinterpret_cast<long long*>(ctx->pivots.ptr);
   q.rows = piv;
   q.cols = piv + K + 1;
@@ -524,6 +582,7 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      (double)n * (double)m * p <= 256.0 * 1024 * 1024 && K >= 4;
   rc = run_maybe_graph(ctx, s, graph, 1, [&](cudaStream_t qs) -> int {
+    RPLU_CUDA(cudaMemsetAsync(ctx->csync.ptr, 0, sync_bytes, qs));
     cauchy_init_state<<<1, 1, 0, qs>>>(q.st);
     for (long long t = 0; t < K; ++t) {
       q.t = t;
@@ -540,17 +599,11 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
         cudaEventRecord(e1, qs);
         ev.push_back(e1);
       }
-      if (q.splits > 1) {
-        sum_partials_kernel<<<(unsigned)((n + 255) / 256), 256, 0, qs>>>(q.partial, q.splits, n,
-                                                                          q.masses);
-        ++launches;
-      }
       cauchy_select_row_kernel<<<1, 1024, 0, qs>>>(q);
       RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, qs>>>(q)));
       cauchy_select_col_kernel<<<1, 1024, 0, qs>>>(q);
-      cauchy_snapshot_kernel<<<1, 32, 0, qs>>>(q, gsnap);
       RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, qs>>>(q, gsnap)));
-      launches += 6;
+      launches += 5;
     }
     RPLU_CUDA(cudaGetLastError());
     return RPLU_OK;

@@ -1,7 +1,7 @@
 set -x
 mkdir -p gpurun_out
-timeout 600 python scripts/time_c1.py > gpurun_out/time_c1.log 2>&1; echo tc1=$?
-cat gpurun_out/time_c1.log
-RPLU_PERSIST_TRACE=1 timeout 600 python scripts/time_c1.py 2>&1 | sort | uniq -c | sort -rn | head -2
-timeout 900 python -m pytest tests/test_dense_gpu.py -x -q -k "persistent or golden or c1" > gpurun_out/pytest_dense.log 2>&1; echo pd=$?
-tail -3 gpurun_out/pytest_dense.log
+timeout 1200 python -m pytest tests/test_cauchy_gpu.py tests/test_cauchy_plan_gpu.py tests/test_distributed_gpu.py -x -q > gpurun_out/pytest_c.log 2>&1; echo pc=$?
+tail -3 gpurun_out/pytest_c.log
+timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.log 2>&1; echo b=$?
+cut -c1-400 gpurun_out/bench_c2.log
+PROFILE_NOGRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c2_launches.csv python scripts/profile_c2.py > /dev/null 2>&1; echo l=$?
