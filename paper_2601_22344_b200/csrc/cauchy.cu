@@ -177,11 +177,11 @@ __global__ void sum_partials_kernel(const double* partial, int splits, long long
 }
 
 // ---------------------------------------------------------------------------
-// K2a: row selection + stop rules.
-__global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q) {
+// K2a: row selection + stop rules (block-uniform result: the row, or -1
+// when the loop stops here).
+__device__ __forceinline__ long long cauchy_select_row_dev(const CauchyParams& q) {
   constexpr int B = 1024;
   DevState* st = q.st;
-  if (!st->active) return;
   __shared__ CdfSmem<B> sm;
   __shared__ int s_stop;
   __shared__ double s_max[B / 32];
@@ -215,13 +215,13 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
     s_stop = stop;
   }
   __syncthreads();
-  if (s_stop) return;
+  if (s_stop) return -1;
   long long i;
   long long uc = st->ucount;
   if (q.rule == RPLU_RULE_RPLU) {
     if (uc + 1 > q.n_uniforms) {
       if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
-      return;
+      return -1;
     }
     const double u1 = q.uniforms[uc];
     i = cdf_find<B>(wrow, n, cr, u1, sm);
@@ -234,14 +234,19 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
     i = block_argmax<B>(wrow, n, nullptr);
   }
   if (threadIdx.x == 0) st->pi = i;
+  return i;
+}
+
+__global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q) {
+  if (!q.st->active) return;
+  cauchy_select_row_dev(q);
 }
 
 // ---------------------------------------------------------------------------
 // K6a: pivot row r_j = (G_i . B_j) / (x_i - y_j) for all j, weights |r_j|^2.
 // numpy order: matmul then complex division (Smith).
 template <int P>
-__global__ void cauchy_row_kernel(CauchyParams q) {
-  if (!q.st->active) return;
+__device__ __forceinline__ void cauchy_row_dev(const CauchyParams& q, long long j0, long long js) {
   double2 gi[P];
   double2 xi;
   if (q.psrc) {
@@ -256,8 +261,7 @@ __global__ void cauchy_row_kernel(CauchyParams q) {
     xi = q.x[i];
   }
   double amax = 0.0;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < q.m;
-       j += (long long)gridDim.x * blockDim.x) {
+  for (long long j = j0; j < q.m; j += js) {
     double re = 0.0, im = 0.0;
 #pragma unroll
     for (int l = 0; l < P; ++l) {
@@ -281,13 +285,19 @@ __global__ void cauchy_row_kernel(CauchyParams q) {
   }
 }
 
+template <int P>
+__global__ void cauchy_row_kernel(CauchyParams q) {
+  if (!q.st->active) return;
+  cauchy_row_dev<P>(q, (long long)blockIdx.x * blockDim.x + threadIdx.x,
+                    (long long)gridDim.x * blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // K2b: column selection with the relative zero-pivot guard; captures G_i and
 // B_j (pre-update) and 1/a coefficients into the state for the update.
-__global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q) {
+__device__ __forceinline__ void cauchy_select_col_dev(const CauchyParams& q) {
   constexpr int B = 1024;
   DevState* st = q.st;
-  if (!st->active) return;
   __shared__ CdfSmem<B> sm;
   __shared__ double s_max[B / 32];
   const long long m = q.m, t = q.t;
@@ -379,6 +389,26 @@ __global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q)
     q.gsnap[l] = q.psrc ? q.psrc[2 + l] : q.G[st->pi * q.p + l];
     q.gsnap[q.p + l] = q.Bt[j * q.p + l];
   }
+}
+
+__global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q) {
+  if (!q.st->active) return;
+  cauchy_select_col_dev(q);
+}
+
+// K2a + K6a + K2b in one CTA (single-GPU loop): the row draw, the pivot row
+// generated by the same 1024 threads (m entries, O(mp) work: microseconds even
+// at m = 2^20 against a multi-second step at that size), and the column draw
+// -- two launches and two L2 round trips fewer per step than the separate
+// kernels the sharded path uses.
+template <int P>
+__global__ void __launch_bounds__(1024) cauchy_select_kernel(CauchyParams q) {
+  if (!q.st->active) return;
+  if (cauchy_select_row_dev(q) < 0) return;
+  __syncthreads();  // st->pi written by thread 0
+  cauchy_row_dev<P>(q, threadIdx.x, blockDim.x);
+  __syncthreads();  // r, |r|^2 and the row max are in place
+  cauchy_select_col_dev(q);
 }
 
 // ---------------------------------------------------------------------------
@@ -577,7 +607,6 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   std::vector<cudaEvent_t> ev;
   long long launches = 1;
   const int upd_blocks = (int)std::min<long long>((n + m + 255) / 256, 8LL * ctx->sm_count);
-  const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
   // per-step GPU time of tens of microseconds: capture the loop as one graph
   const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      (double)n * (double)m * p <= 256.0 * 1024 * 1024 && K >= 4;
@@ -599,11 +628,9 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
         cudaEventRecord(e1, qs);
         ev.push_back(e1);
       }
-      cauchy_select_row_kernel<<<1, 1024, 0, qs>>>(q);
-      RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, qs>>>(q)));
-      cauchy_select_col_kernel<<<1, 1024, 0, qs>>>(q);
+      RPLU_P_SWITCH(p, (cauchy_select_kernel<PP><<<1, 1024, 0, qs>>>(q)));
       RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, qs>>>(q, gsnap)));
-      launches += 5;
+      launches += 3;
     }
     RPLU_CUDA(cudaGetLastError());
     return RPLU_OK;
