@@ -413,7 +413,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
 
     if dist is not None:
         from paper_2601_22344_b200 import distributed as rdist
-        return rdist.bench_sharded(args, cfg, dist, rank_id, world, dev, METRIC, UNIT)
+        return rdist.bench_sharded(args, cfg, dist, rank_id, world, dev, METRIC, UNIT,
+                                   sampler_cls=ClockSampler if rank_id == 0 else None)
 
     if cfg["n"] <= 4096 and cfg.get("kind") == "c1":
         A = torch.from_numpy(gen.c1_dense(seed, n=n)).to(dev)

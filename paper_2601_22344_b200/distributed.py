@@ -25,6 +25,7 @@ CPU tests drive it with a numpy backend over gloo).
 """
 
 import ctypes
+import time
 
 import numpy as np
 import torch
@@ -406,7 +407,7 @@ def sharded_structured_eliminate(M_local, row_offset, rule, rank, stop_tol=0.0, 
     return tr
 
 
-def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
+def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit, sampler_cls=None):
     """bench.py --gpus N leg: C3 row-block sharded over N ranks (strong scaling).
 
     Every rank builds the full seeded C3 input on its GPU (input construction,
@@ -451,20 +452,26 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
     for _ in range(args.warmup):
         one()
     torch.cuda.synchronize()
+    sampler = sampler_cls(torch.cuda.current_device()) if sampler_cls is not None else None
+    if sampler is not None:
+        sampler.start()
+        time.sleep(0.3)
     dist_mod.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        tr = one(timed=not use_graph)
+        tr = one()
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if use_graph:
-        # per-update durations from a second, hook-timed (non-graph) pass
-        dist_mod.barrier()
-        for _ in range(args.steps):
-            one(timed=True)
-        torch.cuda.synchronize()
+    clk = sampler.stop() if sampler is not None else None
+    # per-update durations from a second pass of the same runs with CUDA
+    # events around every update (plain launches, no graph)
+    dist_mod.barrier()
+    for _ in range(args.steps):
+        one(timed=True)
+    torch.cuda.synchronize()
     upd = sum(sweep_ev[2 * q].elapsed_time(sweep_ev[2 * q + 1])
               for q in range(len(sweep_ev) // 2))
     nupd = len(sweep_ev) // 2
@@ -481,7 +488,8 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
     f0.record()
     trh = sharded_eliminate(host.numpy(), lo, PivotRule("rplu", _rng(seed)), k,
                             compute_dtype=tdtype)
-    Lh, Uh = trh.L.cpu(), trh.U.cpu()
+    Lh = torch.as_tensor(_device.to_numpy(trh.L.contiguous()) if torch.is_tensor(trh.L) else trh.L)
+    Uh = torch.as_tensor(_device.to_numpy(trh.U.contiguous()) if torch.is_tensor(trh.U) else trh.U)
     f1.record()
     torch.cuda.synchronize()
     ems = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
@@ -518,6 +526,9 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
+                         "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)",
+                         "launch_timing": "CUDA events around every update, second pass of the "
+                                          "same runs, max over ranks",
                          "kernel": ("shard update (post + pivot column + delayed-update pass + local total)"
                                     if b else "shard update (post + K3 sweep + local total)")
                                    + ", per rank, max over ranks",
@@ -528,6 +539,7 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit):
                     "d2h_bytes_per_step": (Lh.numel() + Uh.numel()) * esize},
             "gpu_launches": args.steps * (((6 if b else 3) * k) + 3),
             "near_boundary_draws": tr.near_boundary_draws,
+            "clocks": clk if clk is not None else {"sm_mhz": None, "reasons": ["not sampled"]},
         }
         print(json.dumps(line), flush=True)
 
