@@ -974,30 +974,6 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
 // R is written back once, after the last step.  The CDF uses the same
 // 1024-thread layout as dense_select_kernel; masses are summed in a fixed
 // order (per-thread vector, warp tree, 32 warps in order).
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
-  while (ld_acquire_u32(c) < target) {
-  }
-}
-// sync[0]: grid-barrier arrivals
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    wait_count(bar, target);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 struct ResidentLayout {
   int rows;     // rows per CTA (max)
   size_t off_l, off_red, bytes;

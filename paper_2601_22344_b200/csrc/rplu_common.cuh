@@ -383,4 +383,30 @@ __device__ long long block_argmax(const WF& wf, long long n, double* out_val) {
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Grid-wide synchronisation for the persistent (cooperative) loops.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
+  while (ld_acquire_u32(c) < target) {
+  }
+}
+// sync[0]: grid-barrier arrivals
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    wait_count(bar, target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 }  // namespace rplu

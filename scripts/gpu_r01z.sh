@@ -1,4 +1,6 @@
 set -x
 mkdir -p gpurun_out
-RPLU_FORCE_SHARDED=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29535 bench.py --gpus 1 > gpurun_out/bench_sharded1.log 2>&1; echo s=$?
-tail -3 gpurun_out/bench_sharded1.log | cut -c1-1500
+timeout 1200 python -m pytest tests/test_cauchy_gpu.py tests/test_cauchy_plan_gpu.py tests/test_distributed_gpu.py -x -q > gpurun_out/pytest_c.log 2>&1; echo pc=$?
+tail -25 gpurun_out/pytest_c.log
+timeout 600 python bench.py --config c2 > gpurun_out/bench_c2c.log 2>&1; echo b=$?
+cut -c1-1200 gpurun_out/bench_c2c.log
