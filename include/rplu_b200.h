@@ -361,6 +361,38 @@ int rplu_sample_target(rplu_ctx* ctx, const double* weights, int64_t n, double t
  * totals the shard CDF is formed from); host result. */
 int rplu_cdf_total(rplu_ctx* ctx, const double* weights, int64_t n, double* total, void* stream);
 
+
+/* ------------------------------------------------------------------------ */
+/* Downstream consumers of the pivots and the CUR core.
+ * All vectors are device complex128 ({re, im} double pairs). */
+
+/* Loewner (divided-difference) matrix, row-major no x k:
+ * out[i*k + j] = (fo[i] - fs[j]) / (zo[i] - zs[j])  (numpy-exact elementwise
+ * arithmetic).  Replaces the matrix build of rplu.rational._loewner_weights
+ * (rational.py:124-127); the weights are its smallest right singular vector. */
+int rplu_loewner_fill(rplu_ctx* ctx, const void* zo, const void* fo, int64_t no, const void* zs,
+                      const void* fs, int64_t k, void* out, void* stream);
+
+/* Barycentric evaluation r(z) = sum_j w_j f_j/(z - t_j) / sum_j w_j/(z - t_j)
+ * with the Cauchy entries generated on the fly (no nz x k matrix in HBM).
+ * mode 0 = BarycentricRational.__call__ / eval_flagged (rational.py:63-80):
+ *   |z - t_j| <= hit_tol returns f_j (last such j); near_pole[i] = 1 when
+ *   |den| < 1e3 * DBL_MIN or the quotient is not finite (and no hit).
+ * mode 1 = the AAA refit (rational.py:165-169): non-finite quotients -> 0,
+ *   near_pole unused (may be NULL). */
+int rplu_bary_eval(rplu_ctx* ctx, const void* z, int64_t nz, const void* t, const void* f,
+                   const void* w, int64_t k, double hit_tol, int32_t mode, void* out,
+                   int32_t* near_pole, void* stream);
+
+/* One modified Gram-Schmidt Arnoldi step of restarted GMRES
+ * (rplu.precond.gmres inner loop, precond.py:160-166), one cooperative
+ * launch: for t = 0..j: h[t] = <V_t, w>, w -= h[t] V_t (MGS order);
+ * h[j+1] = ||w|| (imaginary part 0); if h[j+1] > 0 and vnext != NULL,
+ * vnext = w / h[j+1].  V: (j+1) contiguous rows of n complex128 (row t =
+ * basis vector t); w updated in place; h: device complex128[j+2]. */
+int rplu_mgs_arnoldi(rplu_ctx* ctx, const void* V, int64_t n, int32_t j, void* w, void* vnext,
+                     void* h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

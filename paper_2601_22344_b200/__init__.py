@@ -13,11 +13,13 @@ __version__ = "0.1.0"
 
 from .accessors import CallableOperator, CapabilityError, DenseMatrix, MatrixAccessor, materialize
 from .cauchy import (CauchyLikeMatrix, StructuredPivotTrace, exact_row_norms,
-                     generator_schur_update, structured_eliminate)
+                     generator_schur_update, loewner_build, structured_eliminate)
 from .dense_pivots import EliminationTrace, PivotRule, eliminate
 from .lowmem_cur import (CurBuildInfo, CurFactorization, core_extend, cur_build, residual_column,
                          residual_row)
 from .operators import GaussianKernelOperator
+from .precond import GmresResult, SmwPreconditioner, device_callable, gmres, smw_build
+from .rational import BarycentricRational, SampleSet, aaa, bary_eval, cur_aaa
 from .rng import RngState, sample_index
 from .treebounds import (CoincidentPointsError, InteractionPlan, PointQuadtree, build_plan,
                          certified_upper_bounds)
@@ -25,11 +27,13 @@ from .treebounds import (CoincidentPointsError, InteractionPlan, PointQuadtree, 
 __all__ = [
     "CallableOperator", "CapabilityError", "DenseMatrix", "MatrixAccessor", "materialize",
     "CauchyLikeMatrix", "StructuredPivotTrace", "exact_row_norms", "generator_schur_update",
-    "structured_eliminate",
+    "structured_eliminate", "loewner_build",
     "EliminationTrace", "PivotRule", "eliminate",
     "CurBuildInfo", "CurFactorization", "core_extend", "cur_build", "residual_column",
     "residual_row", "GaussianKernelOperator",
     "RngState", "sample_index",
     "CoincidentPointsError", "InteractionPlan", "PointQuadtree", "build_plan",
     "certified_upper_bounds",
+    "BarycentricRational", "SampleSet", "aaa", "bary_eval", "cur_aaa",
+    "GmresResult", "SmwPreconditioner", "device_callable", "gmres", "smw_build",
 ]

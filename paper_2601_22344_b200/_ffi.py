@@ -151,6 +151,10 @@ SIGNATURES = {
     "rplu_gauss_restricted": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
+    "rplu_loewner_fill": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "rplu_bary_eval": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_i32,
+                                      c_vp, c_vp, c_vp]),
+    "rplu_mgs_arnoldi": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "rplu_shard_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_vp]),
     "rplu_shard_select": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),
     "rplu_shard_update": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),

@@ -23,8 +23,8 @@ from .accessors import CapabilityError, MatrixAccessor
 from .rng import UniformBlock
 
 __all__ = ["CauchyLikeMatrix", "StructuredPivotTrace", "generator_schur_update",
-           "exact_row_norms", "structured_eliminate", "MAX_DISPLACEMENT_RANK",
-           "PIVOT_REL_TOL"]
+           "exact_row_norms", "structured_eliminate", "loewner_build",
+           "MAX_DISPLACEMENT_RANK", "PIVOT_REL_TOL"]
 
 MAX_DISPLACEMENT_RANK = 8    # cauchy.py:30
 PIVOT_REL_TOL = 1e-14        # cauchy.py:33
@@ -226,6 +226,11 @@ class StructuredPivotTrace:
     tol_stop: bool = False
     degenerate_stop: bool = False
     near_boundary_draws: int = 0
+    #: plan path: proposals whose norm / bound test rho >= u_i was decided
+    #: within 1e-12 relative (exact-interaction leaves make u_i == rho in
+    #: exact arithmetic, so whether an acceptance uniform is drawn is a
+    #: rounding-level tie, like a draw on a CDF boundary)
+    near_tie_acceptances: int = 0
     uniforms_consumed: int = 0
     steps_device: tuple = None
     residual: object = None
@@ -320,6 +325,8 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
                     rho = float((rr.real ** 2 + rr.imag ** 2).sum())
                     tr.proposals += 1
                     ui = float(u[ii])
+                    if abs(rho - ui) <= 1e-12 * ui:
+                        tr.near_tie_acceptances += 1
                     if rho >= ui or stream.next() <= rho / ui:
                         tr.acceptances += 1
                         i, r = ii, rr
@@ -446,3 +453,42 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
             Ah = A[:k].cpu().numpy()
             tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(k)]
     return tr
+
+
+def _host_c128(a):
+    if isinstance(a, torch.Tensor):
+        return a.detach().to("cpu", torch.complex128).reshape(-1).numpy()
+    return np.asarray(a, dtype=np.complex128).ravel()
+
+
+def loewner_build(x, f_x, y, f_y, device=None):
+    """Divided-difference matrix (f_x[i] - f_y[j]) / (x[i] - y[j]) as a
+    displacement-rank-2 CauchyLikeMatrix (cauchy.py:280-306).
+
+    Generators G = [f_x/alpha, alpha], B = [alpha; -f_y/alpha] with the
+    balanced scale alpha = sqrt(max |f|) (alpha = 1 with a warning when every
+    sample is zero).  The O(n + m) scale search runs on the samples as given
+    (host arrays, as SampleSet holds them); the generators are formed on the
+    device, dividing by alpha as numpy does for a real-valued complex divisor
+    (times 1/alpha, bit for bit).
+    """
+    import warnings
+    x, y, fx, fy = (_host_c128(a) for a in (x, y, f_x, f_y))
+    if x.size != fx.size or y.size != fy.size:
+        raise ValueError("points and values must have matching lengths")
+    for arr in (fx, fy):
+        if not np.all(np.isfinite(arr.real)) or not np.all(np.isfinite(arr.imag)):
+            raise ValueError("sample values must be finite")
+    fmax = max(float(np.max(np.abs(fx), initial=0.0)), float(np.max(np.abs(fy), initial=0.0)))
+    if fmax == 0.0:
+        warnings.warn("all sample values are zero; scaling factor set to 1", stacklevel=2)
+        alpha = 1.0
+    else:
+        alpha = float(np.sqrt(fmax))
+    dev = _device.require_cuda(device)
+    inv = 1.0 / alpha
+    fxd = _c128(fx, dev)
+    fyd = _c128(fy, dev)
+    G = torch.stack([fxd * inv, torch.full_like(fxd, alpha)], dim=1).contiguous()
+    Bt = torch.stack([torch.full_like(fyd, alpha), -(fyd * inv)], dim=1).contiguous()
+    return CauchyLikeMatrix(x, y, G, None, device=dev, _bt=Bt)

@@ -107,6 +107,14 @@ int cur_downdate_impl(rplu_ctx* ctx, long long n, double* nrow, const double* g,
                       const double* chat, double l2, double floor, long long* clamped,
                       double* total, cudaStream_t s);
 
+int loewner_fill_impl(const void* zo, const void* fo, long long no, const void* zs,
+                      const void* fs, long long k, void* out, cudaStream_t s);
+int bary_eval_impl(const void* z, long long nz, const void* t, const void* f, const void* w,
+                   long long k, double hit_tol, int mode, void* out, int32_t* near_pole,
+                   cudaStream_t s);
+int mgs_arnoldi_impl(rplu_ctx* ctx, const void* V, long long n, int j, void* w, void* vnext,
+                     void* h, cudaStream_t s);
+
 static int gauss_check(const rplu_gauss_op* op) {
   if (!op || op->n < 1 || op->m < 1 || !op->P || !op->Q || !(op->h > 0.0)) {
     set_error("invalid Gaussian-kernel operator");
@@ -189,6 +197,10 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->uniforms.release();
     ctx->pivots.release();
     ctx->resid.release();
+    ctx->masses2.release();
+    ctx->gbar.release();
+    ctx->csync.release();
+    ctx->krylov.release();
     for (auto& b : ctx->scratch) b.release();
     for (auto& e : ctx->graph_exec)
       if (e) cudaGraphExecDestroy(e);
@@ -687,6 +699,46 @@ int rplu_gauss_restricted(rplu_ctx* ctx, const rplu_gauss_op* op, int32_t axis,
                                  reinterpret_cast<cudaStream_t>(stream));
   return gauss_restricted_impl(ctx, op->P, op->n, op->Q, s, w, k, c, out,
                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_loewner_fill(rplu_ctx* ctx, const void* zo, const void* fo, int64_t no, const void* zs,
+                      const void* fs, int64_t k, void* out, void* stream) {
+  if (!ctx || no < 0 || k < 0 || (no * k > 0 && (!zo || !fo || !zs || !fs || !out))) {
+    set_error("rplu_loewner_fill: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return loewner_fill_impl(zo, fo, no, zs, fs, k, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_bary_eval(rplu_ctx* ctx, const void* z, int64_t nz, const void* t, const void* f,
+                   const void* w, int64_t k, double hit_tol, int32_t mode, void* out,
+                   int32_t* near_pole, void* stream) {
+  if (!ctx || nz < 0 || k < 1 || k > (1 << 30) || (mode != 0 && mode != 1) ||
+      (nz > 0 && (!z || !t || !f || !w || !out || (mode == 0 && !near_pole)))) {
+    set_error("rplu_bary_eval: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return bary_eval_impl(z, nz, t, f, w, k, hit_tol, mode, out, near_pole,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_mgs_arnoldi(rplu_ctx* ctx, const void* V, int64_t n, int32_t j, void* w, void* vnext,
+                     void* h, void* stream) {
+  if (!ctx || n < 1 || j < 0 || !V || !w || !h) {
+    set_error("rplu_mgs_arnoldi: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  if (((uintptr_t)V | (uintptr_t)w | (uintptr_t)vnext) % 16) {
+    set_error("rplu_mgs_arnoldi: vectors must be 16-byte aligned");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return mgs_arnoldi_impl(ctx, V, n, j, w, vnext, h, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, const double* v,

@@ -148,4 +148,5 @@ struct rplu_ctx {
   rplu::DevBuf masses2;     // n doubles (persistent dense loop: double-buffered masses)
   rplu::DevBuf gbar;        // grid-barrier counters (persistent dense loop)
   rplu::DevBuf csync;       // Cauchy loop: split-arrival counters + row max slot
+  rplu::DevBuf krylov;      // MGS Arnoldi: per-CTA partials + grid barrier
 };

@@ -251,11 +251,153 @@ def c1_runs(seeds=range(30), steps=100):
         json.dump({"meta": meta(), "n": 2000, "steps": steps, "runs": out}, f)
 
 
+def _aaa_samples(name):
+    """Seeded desk-size sample sets for the rational consumers (§8(f4))."""
+    g = np.random.default_rng(len(name) * 7919)
+    if name == "tanh_line":        # real segment, a function with nearby poles
+        z = np.linspace(-1.0, 1.0, 240) + 0j
+        return z, np.tanh(6.0 * z)
+    if name == "circle_log":       # jittered unit circle, a branch point outside
+        t = np.sort(g.uniform(0.0, 2 * np.pi, 300))
+        z = np.exp(1j * t) * (1.0 + 0.01 * g.standard_normal(300))
+        return z, np.log(2.5 - z)
+    if name == "spiral_mero":      # C2-like spiral point set, a meromorphic function
+        t = g.uniform(0.0, 1.0, 360)
+        z = (0.1 + t) * np.exp(1j * 4 * np.pi * t) + 0.01 * (g.standard_normal(360)
+                                                         + 1j * g.standard_normal(360))
+        return z, np.exp(z) / (z - 1.7) + 1.0 / (z + 1.6j)
+    raise KeyError(name)
+
+
+def _cur_aaa_stable(S, tol, seed, leaf, result, trials=3):
+    """Whether the reference's cur_aaa result survives 1e-15 relative
+    perturbations of the generated rows / columns.  With exact-interaction
+    leaves the certified bound equals ||r_i||^2 in exact arithmetic, so the
+    rejection test rho >= u_i (which decides whether an acceptance uniform is
+    drawn) is a rounding-level tie and the whole stream can shift; such
+    inputs only get the fit-quality bar in the GPU test."""
+    import warnings
+    C = rplu.cauchy.CauchyLikeMatrix
+    row, col = C.row, C.column
+    g = np.random.default_rng(1)
+    try:
+        C.row = lambda self, i: row(self, i) * (1 + 1e-15 * g.standard_normal(self.shape[1]))
+        C.column = lambda self, j: col(self, j) * (1 + 1e-15 * g.standard_normal(self.shape[0]))
+        for _ in range(trials):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                rc, side = rplu.cur_aaa(S, tol=tol, rng=rplu.RngState(seed), leaf_size=leaf)
+            if side != result[0] or not np.array_equal(rc.support, result[1]):
+                return False
+        return True
+    finally:
+        C.row, C.column = row, col
+
+
+def rational_cases():
+    """aaa / cur_aaa / bary_eval / loewner_build (rational.py, cauchy.py:280-306)."""
+    import warnings
+    arrays, info = {}, []
+    for name, tol, seed in (("tanh_line", 1e-11, 3), ("circle_log", 1e-11, 5),
+                            ("spiral_mero", 1e-10, 11)):
+        z, f = _aaa_samples(name)
+        S = rplu.SampleSet(z, f)
+        arrays[name + "_z"], arrays[name + "_f"] = z, f
+        r, errs = rplu.aaa(S, tol=1e-13, max_degree=60)
+        zt = z[:-1] + 0.37 * np.diff(z)              # off-sample evaluation points
+        arrays[name + "_zt"] = zt
+        arrays[name + "_aaa_support"] = r.support
+        arrays[name + "_aaa_weights"] = r.weights
+        arrays[name + "_aaa_errors"] = errs
+        arrays[name + "_aaa_eval"] = r(zt)
+        cur = {}
+        for leaf in (None, 8):
+            tag = "_cur" if leaf is None else "_cur8"
+            rng = rplu.RngState(seed)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                rc, side = rplu.cur_aaa(S, tol=tol, rng=rng, leaf_size=leaf)
+            after = rng.uniform()
+            arrays[name + tag + "_support"] = rc.support
+            arrays[name + tag + "_weights"] = rc.weights
+            arrays[name + tag + "_eval"] = rc(zt)
+            arrays[name + tag + "_err"] = np.array([np.max(np.abs(rc(z) - f))])
+            cur[tag] = {"leaf_size": leaf, "side": side, "next_uniform": after,
+                        "support_idx": [int(np.nonzero(z == t)[0][0]) for t in rc.support],
+                        "degree": int(rc.degree),
+                        "stable": _cur_aaa_stable(S, tol, seed, leaf, (side, rc.support))}
+        # the split Loewner generators cur_aaa eliminates
+        perm = rplu.RngState(seed).permutation(z.size)
+        half = (z.size + 1) // 2
+        L = rplu.cauchy.loewner_build(z[perm[:half]], f[perm[:half]], z[perm[half:]],
+                                      f[perm[half:]])
+        arrays[name + "_loewner_G"], arrays[name + "_loewner_B"] = L.G, L.B
+        info.append({"name": name, "tol": tol, "seed": seed, "cur": cur,
+                     "aaa_support_idx": [int(np.nonzero(z == t)[0][0]) for t in r.support],
+                     "aaa_degree": int(r.degree)})
+    # bary_eval edge cases: exact support hits, a point on a pole
+    t = np.array([0.0, 1.0, 1j, -1.0 + 0.5j])
+    fv = np.array([1.0, 2.0 - 1j, 0.5j, -3.0])
+    w = np.array([1.0, -2.0, 1.5j, 0.25 - 0.25j])
+    r = rplu.BarycentricRational(t, fv, w)
+    ze = np.array([0.0, 1.0 + 1e-16, 0.3 + 0.2j, 2.0, 1j, 5.0 - 5j])
+    out, flags = r.eval_flagged(ze)
+    arrays["bary_t"], arrays["bary_f"], arrays["bary_w"] = t, fv, w
+    arrays["bary_z"], arrays["bary_out"], arrays["bary_flags"] = ze, out, flags
+    save("rational", arrays, info)
+
+
+def precond_cases():
+    """smw_build + gmres (precond.py) on a banded-plus-low-rank system."""
+    import scipy.linalg as sla
+    arrays, info = {}, []
+    for name, n, k, seed in (("band_lowrank300", 300, 20, 4), ("band_lowrank200_k8", 200, 8, 9)):
+        A = gen.planted_spectrum(n, n, 0.5, seed) * 40.0
+        main = np.full(n, 4.0)
+        off = np.full(n - 1, -1.0)
+        ab = np.zeros((3, n))
+        ab[0, 1:], ab[1, :], ab[2, :-1] = off, main, off
+
+        def b_inv(v, ab=ab):
+            return sla.solve_banded((1, 1), ab, v)
+
+        def K_apply(v, A=A, main=main, off=off):
+            out = A @ v
+            out = out + main * v
+            out[:-1] += off * v[1:]
+            out[1:] += off * v[:-1]
+            return out
+
+        rng = rplu.RngState(seed)
+        b = rng.complex_normal(n)
+        fact, _ = rplu.cur_build(rplu.DenseMatrix(A), "rplu-cur", k, rng=rplu.RngState(seed ^ 1))
+        pre = rplu.smw_build(b_inv, rplu.DenseMatrix(A), fact)
+        v = rplu.RngState(seed + 100).complex_normal(n)
+        res_pre = rplu.gmres(K_apply, b, M_inv=pre, restart=20, tol=1e-10, max_restarts=200)
+        res_plain = rplu.gmres(K_apply, b, restart=10, tol=1e-8, max_restarts=300)
+        arrays[name + "_b"], arrays[name + "_v"] = b, v   # A regenerated from gen (seeded)
+        arrays[name + "_pre_v"] = pre.apply(v)
+        arrays[name + "_x_pre"], arrays[name + "_hist_pre"] = res_pre.x, res_pre.residuals
+        arrays[name + "_x_plain"], arrays[name + "_hist_plain"] = res_plain.x, res_plain.residuals
+        info.append({"name": name, "n": n, "k": k, "seed": seed,
+                     "I": [int(i) for i in fact.row_indices],
+                     "J": [int(j) for j in fact.col_indices],
+                     "pre": {"iterations": res_pre.iterations, "converged": res_pre.converged,
+                             "stagnated": res_pre.stagnated},
+                     "plain": {"iterations": res_plain.iterations,
+                               "converged": res_plain.converged,
+                               "stagnated": res_plain.stagnated}})
+    save("precond", arrays, info)
+
+
 if __name__ == "__main__":
-    sample_index_cases()
-    dense_cases()
-    cauchy_cases()
-    cauchy_plan_cases()
-    cur_cases()
+    if "--consumers" not in sys.argv:
+        sample_index_cases()
+        dense_cases()
+        cauchy_cases()
+        cauchy_plan_cases()
+        cur_cases()
+    rational_cases()
+    precond_cases()
     if "--c1" in sys.argv:
         c1_runs()

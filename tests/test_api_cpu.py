@@ -60,3 +60,16 @@ def test_uniform_block_accepts_reference_like_rng():
 def test_no_cpu_fallback_without_gpu():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         rp.eliminate(np.eye(4), rp.PivotRule("rplu", rp.RngState(0)), 2)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_consumers_have_no_cpu_fallback():
+    S = rp.SampleSet(np.arange(6) + 0j, np.exp(np.arange(6) + 0j))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rp.aaa(S)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rp.cur_aaa(S, rng=rp.RngState(0))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rp.gmres(np.eye(3), np.ones(3))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rp.BarycentricRational([0.0, 1.0], [1.0, 2.0], [1.0, 1.0])

@@ -172,3 +172,68 @@ def test_cur_oracle_matches_reference(case):
                                atol=1e-12 * case["total_sq_norms"][0])
     if gen_ is not None:
         assert float(gen_.random()) == case["next_uniform"]
+
+
+# ---------------------------------------------------------------------------
+# §8(f4) consumers: AAA / barycentric evaluation / Loewner generators, SMW + GMRES
+
+def _rational():
+    return load_golden("rational")
+
+
+@pytest.mark.parametrize("name", ["tanh_line", "circle_log", "spiral_mero"])
+def test_oracle_aaa_matches_reference(name):
+    info, arr = _rational()
+    case = next(c for c in info["cases"] if c["name"] == name)
+    z, f = arr[name + "_z"], arr[name + "_f"]
+    sup, w, errs = oracle.consumers.aaa(z, f, tol=1e-13, max_degree=60)
+    assert sup == case["aaa_support_idx"]
+    np.testing.assert_allclose(errs, arr[name + "_aaa_errors"], rtol=1e-6, atol=1e-15)
+    vals, _ = oracle.consumers.bary_eval_flagged(z[sup], f[sup], w, arr[name + "_zt"])
+    np.testing.assert_allclose(vals, arr[name + "_aaa_eval"], rtol=0,
+                               atol=1e-10 * np.abs(f).max())
+
+
+@pytest.mark.parametrize("name", ["tanh_line", "circle_log", "spiral_mero"])
+def test_oracle_loewner_generators_match_reference(name):
+    info, arr = _rational()
+    case = next(c for c in info["cases"] if c["name"] == name)
+    z, f = arr[name + "_z"], arr[name + "_f"]
+    perm = oracle.uniform_stream(case["seed"]).permutation(z.size)
+    h = (z.size + 1) // 2
+    G, B = oracle.consumers.loewner_generators(z[perm[:h]], f[perm[:h]], z[perm[h:]],
+                                                f[perm[h:]])
+    np.testing.assert_array_equal(G, arr[name + "_loewner_G"])
+    np.testing.assert_array_equal(B, arr[name + "_loewner_B"])
+
+
+def test_oracle_bary_eval_edge_cases_match_reference():
+    _, arr = _rational()
+    vals, flags = oracle.consumers.bary_eval_flagged(arr["bary_t"], arr["bary_f"], arr["bary_w"],
+                                                     arr["bary_z"])
+    fin = np.isfinite(arr["bary_out"])
+    np.testing.assert_allclose(vals[fin], arr["bary_out"][fin], rtol=1e-13)
+    np.testing.assert_array_equal(flags, arr["bary_flags"])
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_oracle_smw_gmres_match_reference(idx):
+    from consumer_cases import band_system
+    info, arr = load_golden("precond")
+    case = info["cases"][idx]
+    name, n = case["name"], case["n"]
+    A, _, b_inv, K_apply, _ = band_system(n, case["seed"])
+    pre = oracle.consumers.smw_apply_factory(b_inv, A, case["I"], case["J"])
+    np.testing.assert_allclose(pre(arr[name + "_v"]), arr[name + "_pre_v"], rtol=1e-10,
+                               atol=1e-12 * np.abs(arr[name + "_pre_v"]).max())
+    b = arr[name + "_b"]
+    x, hist, iters, conv, stag = oracle.consumers.gmres_mgs(K_apply, b, M=pre, restart=20,
+                                                            tol=1e-10, max_restarts=200)
+    assert (iters, conv, stag) == (case["pre"]["iterations"], case["pre"]["converged"],
+                                   case["pre"]["stagnated"])
+    np.testing.assert_allclose(x, arr[name + "_x_pre"], rtol=1e-8, atol=1e-10)
+    x, hist, iters, conv, stag = oracle.consumers.gmres_mgs(K_apply, b, restart=10, tol=1e-8,
+                                                            max_restarts=300)
+    assert (iters, conv) == (case["plain"]["iterations"], case["plain"]["converged"])
+    np.testing.assert_allclose(hist, arr[name + "_hist_plain"], rtol=1e-6)
+    np.testing.assert_allclose(x, arr[name + "_x_plain"], rtol=1e-7, atol=1e-9)
