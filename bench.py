@@ -46,6 +46,13 @@ CONFIGS = {
     "c5": dict(desc="C5 matrix-free Gaussian kernel fp64 2e6 x 2e6 (BASELINE configs[4]); bench "
                     "step = `rank` pivot steps of the rank-1024 cur_build",
                n=2_000_000, rank=2, dtype="f64", seed=0, kind="cur"),
+    # §8(f4) consumers (not BASELINE configs: supplementary measurement lines)
+    "gmres": dict(desc="SURVEY 8(f4) restarted GMRES: one 20-step MGS Arnoldi cycle on n=2^24 "
+                       "complex128 (stencil operator); bench step = one restart cycle",
+                  n=1 << 24, rank=20, dtype="c128", seed=0, kind="gmres"),
+    "bary": dict(desc="SURVEY 8(f4) barycentric evaluation: degree-256 rational at 2^24 points "
+                      "(+ one cur_aaa fit on 20000 samples); bench step = one evaluation",
+                 n=1 << 24, rank=256, dtype="c128", seed=0, kind="bary"),
 }
 METRIC = "RPLU pivot steps/sec at rank k; dense Schur step HBM GB/s vs B200 peak"
 UNIT = "pivot steps/s"
@@ -332,6 +339,7 @@ def run_cur_arm(args, cfg):
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gemv = []
+    launches0 = _ffi.kernel_launch_count()
     ev0.record()
     for _ in range(args.steps):
         fact, info = rp.cur_build(op, "rplu-cur", rank, rng=rp.RngState(seed), time_gemv=True)
@@ -339,6 +347,7 @@ def run_cur_arm(args, cfg):
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
+    launches = _ffi.kernel_launch_count() - launches0
     clk = clocks.stop()
     k = fact.rank
     value = args.steps * k / (total_ms / 1e3)
@@ -387,11 +396,188 @@ def run_cur_arm(args, cfg):
                                    f"applies per step; CPU: {model}"},
         "e2e": {"value": k / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 48 * n,
                 "d2h_bytes_per_step": Wh.nbytes + 8 * n},
-        "gpu_launches": None,
+        "gpu_launches": launches,
         "near_boundary_draws": info.near_boundary_draws,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def _supp_line(args, cfg, metric, unit, value, total_ms, roofline, cpu, e2e, launches, clk,
+               extra=None):
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (seeded)",
+            "config": {"workload": cfg["desc"], "n": cfg["n"], "seed": cfg["seed"],
+                       "l2": "inputs larger than L2"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk}
+    line.update(extra or {})
+    print(json.dumps(line), flush=True)
+
+
+def run_gmres_arm(args, cfg):
+    """One restart cycle of GMRES (20 MGS Arnoldi steps) at n = 2^24: the
+    Krylov basis (21 x 256 MB) streams from HBM; the MGS kernel is timed
+    per launch in a second pass against its algorithmic bytes
+    (112 + 64 j) * 16 n / 16 ... see DESIGN.md §3."""
+    import ctypes
+
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _device, _ffi
+    torch.cuda.set_device(0)
+    n, steps_per = cfg["n"], cfg["rank"]
+    g = torch.Generator(device="cuda").manual_seed(cfg["seed"])
+    b = torch.complex(torch.randn(n, generator=g, device="cuda", dtype=torch.float64),
+                      torch.randn(n, generator=g, device="cuda", dtype=torch.float64))
+
+    @rp.device_callable
+    def K(x):     # shifted 1-D Laplacian stencil (the user's operator)
+        y = 4.0 * x
+        y[1:] -= x[:-1]
+        y[:-1] -= x[1:]
+        return y
+
+    def cycle(bb):
+        return rp.gmres(K, bb, restart=steps_per, tol=1e-300, max_restarts=1)
+    for _ in range(args.warmup):
+        cycle(b)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _ffi.kernel_launch_count()
+    e0.record()
+    for _ in range(args.steps):
+        res = cycle(b)
+    e1.record()
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    launches = _ffi.kernel_launch_count() - launches0
+    clk = clocks.stop()
+    value = args.steps * res.iterations / (total_ms / 1e3)
+    # second pass: the MGS kernel alone, per launch, on the same basis shape
+    V = torch.zeros((steps_per + 1, n), dtype=torch.complex128, device="cuda")
+    V[0] = b / torch.linalg.vector_norm(b)
+    h = torch.zeros(steps_per + 2, dtype=torch.complex128, device="cuda")
+    c = _device.ctx(torch.device("cuda", 0))
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ms, byts = [], []
+    for j in range(steps_per):
+        w = K(V[j]).contiguous()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        _ffi.check(c._lib.rplu_mgs_arnoldi(c.handle, V.data_ptr(), n, j, w.data_ptr(),
+                                           V[j + 1].data_ptr(), h.data_ptr(), st))
+        a1.record()
+        torch.cuda.synchronize()
+        ms.append(a0.elapsed_time(a1))
+        byts.append((112 + 64 * j) * n)
+    peak, peak_src = _peaks()
+    achieved = sum(byts) / (sum(ms) / 1e3) / 1e9
+    # e2e: host rhs in, host solution out (one cycle)
+    bh = b.cpu().numpy()
+    e0.record()
+    resh = rp.gmres(K, bh, restart=steps_per, tol=1e-300, max_restarts=1)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    # CPU baseline: the oracle's MGS GMRES cycle on a 2^20 sample, scaled to n
+    ns = 1 << 20
+    bs = bh[:ns]
+    Kh = lambda x: 4.0 * x - np.concatenate([[0], x[:-1]]) - np.concatenate([x[1:], [0]])  # noqa
+    t0 = time.perf_counter()
+    oracle.consumers.gmres_mgs(Kh, bs, restart=steps_per, tol=1e-300, max_restarts=1)
+    dt = (time.perf_counter() - t0) * n / ns
+    model, _ = _cpu_info()
+    _supp_line(args, cfg, "GMRES Arnoldi steps/s (MGS, restart 20)", "Arnoldi steps/s", value,
+               total_ms,
+               {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "mgs_arnoldi_kernel (one cooperative launch per Arnoldi step)",
+                "algorithmic_bytes_per_cycle": float(sum(byts)),
+                "avg_launch_ms": sum(ms) / len(ms), "peak_source": peak_src},
+               {"value": steps_per / dt, "unit": "Arnoldi steps/s", "cores": 1, "kind": "port",
+                "sample": f"oracle gmres_mgs cycle on {ns} of {n} unknowns "
+                          f"({dt * ns / n:.2f}s), scaled linearly; CPU: {model}"},
+               {"value": resh.iterations / (e2e_ms / 1e3), "unit": "Arnoldi steps/s",
+                "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n},
+               launches, clk)
+
+
+def run_bary_arm(args, cfg):
+    """Barycentric evaluation kernel (generated Cauchy entries, FP64 pipe)
+    at 2^24 points, degree 256; plus one cur_aaa fit as the e2e call."""
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _ffi
+    torch.cuda.set_device(0)
+    n, k, seed = cfg["n"], cfg["rank"], cfg["seed"]
+    g = np.random.default_rng(seed)
+    t = np.exp(2j * np.pi * g.uniform(size=k)) * 1.2
+    f = np.exp(t)
+    w = g.standard_normal(k) + 1j * g.standard_normal(k)
+    r = rp.BarycentricRational(t, f, w)
+    zd = torch.complex(torch.rand(n, device="cuda", dtype=torch.float64) * 2 - 1,
+                       torch.rand(n, device="cuda", dtype=torch.float64) * 2 - 1)
+    for _ in range(args.warmup):
+        r.eval_dev(zd)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        r.eval_dev(zd)
+    e1.record()
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    per_ms = total_ms / args.steps
+    flops = 22.0 * n * k     # 2 sub, |d|^2 (2), reciprocal (1), 2 mul, 2 complex MACs (8+8)... /pair
+    achieved = flops / (per_ms / 1e3) / 1e12
+    peak = _ffi.fp64_peak_tflops(0)
+    # e2e: cur_aaa on 20000 spiral samples (host samples in, host rational out)
+    m = 20000
+    tt = g.uniform(size=m)
+    zs = (0.1 + tt) * np.exp(1j * 4 * np.pi * tt) + 0.01 * (g.standard_normal(m)
+                                                          + 1j * g.standard_normal(m))
+    S = rp.SampleSet(zs, np.exp(zs) / (zs - 1.7))
+    e0.record()
+    ra, side = rp.cur_aaa(S, tol=1e-10, rng=rp.RngState(seed), leaf_size=16)
+    sup = ra.support
+    e1.record()
+    torch.cuda.synchronize()
+    fit_ms = e0.elapsed_time(e1)
+    # CPU: oracle evaluation on a 2^14-point sample, scaled
+    ns = 1 << 14
+    zh = zd[:ns].cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.consumers.bary_eval_flagged(t, f, w, zh)
+    dt = (time.perf_counter() - t0) * n / ns
+    model, _ = _cpu_info()
+    _supp_line(args, cfg, "barycentric evaluations/s (degree 256, 2^24 points)", "evaluations/s",
+               1e3 / per_ms, total_ms,
+               {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "bary_eval_kernel (generated Cauchy entries, two RHS)",
+                "algorithmic_flops_per_launch": flops, "avg_launch_ms": per_ms,
+                "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)",
+                "note": "22 flop per (z, t_j) pair, the reciprocal counted as one"},
+               {"value": 1.0 / dt, "unit": "evaluations/s", "cores": 1, "kind": "port",
+                "sample": f"oracle bary_eval_flagged on {ns} of {n} points, scaled; CPU: {model}"},
+               {"value": 1e3 / fit_ms, "unit": "cur_aaa fits/s (20000 samples)",
+                "h2d_bytes_per_step": 32 * m, "d2h_bytes_per_step": 16 * len(sup) * 3},
+               args.steps, clk, {"cur_aaa": {"degree": int(ra.degree), "side": side,
+                                             "ms": fit_ms}})
 
 
 def run_b200_arm(args, cfg, dist, rank_id, world):
@@ -400,6 +586,10 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
         return run_cauchy_arm(args, cfg)
     if cfg.get("kind") == "cur":
         return run_cur_arm(args, cfg)
+    if cfg.get("kind") == "gmres":
+        return run_gmres_arm(args, cfg)
+    if cfg.get("kind") == "bary":
+        return run_bary_arm(args, cfg)
 
     import paper_2601_22344_b200 as rp
     from paper_2601_22344_b200 import gen

@@ -69,6 +69,11 @@ extern "C" {
 typedef struct rplu_ctx rplu_ctx;
 
 int rplu_abi_version(void);
+/* Kernels launched so far (process-wide) by the standalone primitives
+ * (rplu_gauss_*, rplu_cur_downdate, rplu_sample_index, rplu_loewner_fill,
+ * rplu_bary_eval, rplu_mgs_arnoldi); the loop drivers report their own
+ * counts in their out structs. */
+int64_t rplu_kernel_launch_count(void);
 const char* rplu_last_error(void);
 
 /* Create a context bound to CUDA device `device` (workspace is grown lazily). */

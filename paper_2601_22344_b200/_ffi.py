@@ -151,6 +151,7 @@ SIGNATURES = {
     "rplu_gauss_restricted": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
+    "rplu_kernel_launch_count": (c_i64, []),
     "rplu_loewner_fill": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "rplu_bary_eval": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_i32,
                                       c_vp, c_vp, c_vp]),
@@ -171,6 +172,11 @@ SIGNATURES = {
     "rplu_cauchy_shard_finish": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs),
                                                 ctypes.POINTER(CauchyOut)]),
 }
+
+
+def kernel_launch_count():
+    """Process-wide count of kernels launched by the standalone primitives."""
+    return int(load_library().rplu_kernel_launch_count())
 
 
 def fp64_peak_tflops(device=0):

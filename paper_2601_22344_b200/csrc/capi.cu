@@ -8,6 +8,11 @@
 
 #include "rplu_internal.h"
 
+#include <atomic>
+namespace rplu {
+static std::atomic<long long> g_launches{0};
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace rplu
 namespace rplu {
 
 static thread_local std::string g_last_error;
@@ -163,6 +168,8 @@ using namespace rplu;
 extern "C" {
 
 int rplu_abi_version(void) { return RPLU_B200_ABI_VERSION; }
+
+int64_t rplu_kernel_launch_count(void) { return g_launches.load(); }
 
 const char* rplu_last_error(void) { return g_last_error.c_str(); }
 

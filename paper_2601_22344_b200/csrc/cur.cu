@@ -15,6 +15,7 @@
 // complex128 vectors carry zero imaginary parts throughout.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -24,15 +25,21 @@
 
 namespace rplu {
 
-// exp(x) for x <= 0 (the kernel's exponent), table-driven: x = (32n + j)
-// ln2/32 + r with |r| <= ln2/64, exp(x) = 2^n * 2^(j/32) * p(r), p the
-// degree-6 Taylor polynomial (truncation < 4e-18 relative).  2^(j/32) comes
-// from a 32-entry table held one entry per lane (fetched with a warp
-// shuffle: no shared-memory bank conflicts), 2^n is added to the table
-// value's exponent field with integer ops, and k = 32n + j is read from the
-// low word of the round-to-nearest shifter sum — so an entry costs 19 FP64
-// pipe operations including the distance and the accumulate.  Accuracy
-// ~1 ulp.  Below -708 the result is 0 (entries < 1e-307).
+// exp(-d2) for d2 >= 0 (the kernel's exponent), table-driven.  With
+// y = -d2 * 32/ln2, k = round(y) = 32 n + j (0 <= j < 32) and s = y - k
+// (|s| <= 1/2, formed as fma(-K, d2, -k): one rounding, so the Cody-Waite
+// hi/lo reduction of a separately rounded y is not needed),
+//   exp(-d2) = 2^n * 2^(j/32) * p(s),   p(s) = sum_{i<=6} (s ln2/32)^i / i!
+// (truncation < 4e-18 relative).  2^(j/32) comes from a 32-entry table held
+// one entry per lane (fetched with a warp shuffle: no shared-memory bank
+// conflicts), 2^n is added to the table value's exponent field with integer
+// ops, k is read from the low word of the round-to-nearest shifter sum, and
+// the underflow cut (exp(-d2) < 1e-307 -> 0) is an integer compare on k —
+// so an entry costs 17 FP64-pipe operations including the distance and the
+// accumulate (the hi/lo reduction and the FP64 compare of the previous
+// variant cost 19).  A 64-entry table with a degree-5 polynomial saves one
+// more DFMA but needs two 64-bit shuffles per entry and measured 2% slower
+// (DESIGN.md §10).  Relative error ~ 1 ulp + d2 * 2^-53 (the rounding of K d2).
 // Every lane of the warp must call it (warp-synchronous shuffle).
 __constant__ double kExp2Tab[32] = {
     1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
@@ -44,35 +51,38 @@ __constant__ double kExp2Tab[32] = {
     1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,
     1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002};
 
-__device__ __forceinline__ double exp2tab_lane() { return kExp2Tab[threadIdx.x & 31]; }
+using ExpTab = double;  // this lane's 2^(lane/32)
 
-__device__ __forceinline__ double exp_nonpos(double x, double tlane) {
+__device__ __forceinline__ ExpTab exp2tab_lane() { return kExp2Tab[threadIdx.x & 31]; }
+
+__device__ __forceinline__ double exp_neg(double d2, ExpTab tab) {
   const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest
-  const double sft = fma(x, 46.16624130844683, shifter);   // x * 32/ln2
+  const double K = 46.16624130844683;          // 32 / ln2
+  const double sft = fma(d2, -K, shifter);
   const double kd = sft - shifter;
   const int k = __double2loint(sft);
-  double r = fma(kd, -0.02166084938653512, x);             // ln2/32 (hi)
-  r = fma(kd, -5.9631716539705866e-12, r);                 // ln2/32 (lo)
-  double p = 1.3888888888888889e-03;                       // 1/720
-  p = fma(p, r, 8.3333333333333333e-03);                   // 1/120
-  p = fma(p, r, 4.1666666666666667e-02);                   // 1/24
-  p = fma(p, r, 1.6666666666666667e-01);                   // 1/6
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const double t = __shfl_sync(0xffffffffu, tlane, k & 31);
+  const double s = fma(d2, -K, -kd);           // y - k, |s| <= 1/2
+  double p = 1.4345655584131932e-13;           // L^6/720, L = ln2/32
+  p = fma(p, s, 3.9737099845494154e-11);       // L^5/120
+  p = fma(p, s, 9.172562701824643e-09);        // L^4/24
+  p = fma(p, s, 1.6938509724371819e-06);       // L^3/6
+  p = fma(p, s, 0.00023459619820224677);       // L^2/2
+  p = fma(p, s, 0.02166084939249829);          // L
+  p = fma(p, s, 1.0);
+  const double t = __shfl_sync(0xffffffffu, tab, k & 31);
   const double ts = __hiloint2double(__double2hiint(t) + ((k >> 5) << 20), __double2loint(t));
-  return x < -708.0 ? 0.0 : p * ts;
+  const double e = p * ts;
+  return k < -32700 ? 0.0 : e;                 // k < -32*1021.9: below 1e-307
 }
 
 // Entry from coordinates prescaled by sc = 1/(sqrt(2) h) (done once per
 // point as it is loaded into registers / shared memory), so the exponent
-// -|p-q|^2/(2h^2) is just -|p'-q'|^2: 18 FP64-pipe operations per entry.
+// -|p-q|^2/(2h^2) is just -|p'-q'|^2.
 __device__ __forceinline__ double gauss_entry(double px, double py, double pz, double qx,
-                                              double qy, double qz, double tlane) {
+                                              double qy, double qz, ExpTab tab) {
   const double dx = px - qx, dy = py - qy, dz = pz - qz;
   const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  return exp_nonpos(-d2, tlane);
+  return exp_neg(d2, tab);
 }
 
 // ---------------------------------------------------------------------------
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const doubl
   const long long cols_per = (op.m + splits - 1) / splits;
   const long long j0 = (long long)blockIdx.y * cols_per;
   const long long j1 = min(op.m, j0 + cols_per);
-  const double tl = exp2tab_lane();
+  const ExpTab tl = exp2tab_lane();
   double px[RPT], py[RPT], pz[RPT], acc[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -140,7 +150,7 @@ __global__ void reduce_splits_kernel(const double* partial, int splits, long lon
 __global__ void gauss_line_kernel(const double* __restrict__ pts, long long count,
                                   const double* __restrict__ base, double c, double* out) {
   const double bx = c * base[0], by = c * base[1], bz = c * base[2];
-  const double tl = exp2tab_lane();
+  const ExpTab tl = exp2tab_lane();
   const long long stride = (long long)gridDim.x * blockDim.x;
   // warp-uniform trip count (the exp's table shuffle needs every lane)
   for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < count; k0 += stride) {
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(256) gauss_restricted_kernel(
     ss[s * 4 + 3] = w[s];
   }
   __syncthreads();
-  const double tl = exp2tab_lane();
+  const ExpTab tl = exp2tab_lane();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < count; t0 += stride) {
     const long long t = t0 + threadIdx.x;
@@ -232,23 +242,44 @@ static int gemv_splits(long long n, long long m, int rows_per_cta, int sms) {
   return (int)std::min(s, 1024LL);
 }
 
+template <int RPT>
+static void gemv_launch(const GaussOp& op, const double* v, double* part, int splits, bool square,
+                        cudaStream_t s) {
+  constexpr int TJ = 256;
+  dim3 grid((unsigned)((op.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)splits);
+  if (square) gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits);
+  else gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits);
+}
+
+// rows per thread of K7 (RPLU_GEMV_RPT experiment override: 1, 2 or 4)
+static int gemv_rpt() {
+  static int v = [] {
+    const char* e = getenv("RPLU_GEMV_RPT");
+    int r = e ? atoi(e) : 4;   // measured at n = m = 1e6: 1 -> 1417 ms, 2 -> 1347, 4 -> 1336
+    return (r == 1 || r == 2) ? r : 4;
+  }();
+  return v;
+}
+
 int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
                     cudaStream_t s, float* ms) {
-  constexpr int RPT = 2, TJ = 256;
-  const int splits = gemv_splits(op.n, op.m, 256 * RPT, ctx->sm_count);
+  const int rpt = gemv_rpt();
+  const int splits = gemv_splits(op.n, op.m, 256 * rpt, ctx->sm_count);
   int rc;
   if ((rc = ctx->scratch[4].ensure(sizeof(double) * (size_t)splits * op.n))) return rc;
   double* part = reinterpret_cast<double*>(ctx->scratch[4].ptr);
-  dim3 grid((unsigned)((op.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)splits);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ms) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  if (square) gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits);
-  else gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits);
+  count_launches(1);
+  if (rpt == 1) gemv_launch<1>(op, v, part, splits, square, s);
+  else if (rpt == 2) gemv_launch<2>(op, v, part, splits, square, s);
+  else gemv_launch<4>(op, v, part, splits, square, s);
   if (ms) cudaEventRecord(e1, s);
+  count_launches(1);
   reduce_splits_kernel<<<(unsigned)((op.n + 255) / 256), 256, 0, s>>>(part, splits, op.n, out);
   RPLU_CUDA(cudaGetLastError());
   if (ms) {
@@ -263,6 +294,7 @@ int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* o
 int gauss_line_impl(const double* pts, long long count, const double* base, double c, double* out,
                     cudaStream_t s) {
   const int blocks = (int)std::min<long long>((count + 255) / 256, 4096);
+  count_launches(1);
   gauss_line_kernel<<<blocks, 256, 0, s>>>(pts, count, base, c, out);
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
@@ -281,6 +313,7 @@ int gauss_restricted_impl(rplu_ctx* ctx, const double* targets, long long count,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   const int blocks = (int)std::min<long long>((count + 255) / 256, 16LL * ctx->sm_count);
+  count_launches(1);
   gauss_restricted_kernel<<<blocks, 256, smem, s>>>(targets, count, selpts, sel, w, k, c, out);
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
@@ -295,6 +328,7 @@ int cur_downdate_impl(rplu_ctx* ctx, long long n, double* nrow, const double* g,
     return rc;
   double* ps = reinterpret_cast<double*>(ctx->scratch[5].ptr);
   long long* pc = reinterpret_cast<long long*>(ps + blocks);
+  count_launches(1);
   cur_downdate_kernel<<<blocks, 256, 0, s>>>(n, nrow, g, v, chat, l2, floor, ps, pc);
   RPLU_CUDA(cudaGetLastError());
   std::vector<double> hs(blocks);

@@ -1868,6 +1868,7 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int
   int rc;
   if ((rc = ctx->scratch[7].ensure(sizeof(SampleOut)))) return rc;
   SampleOut* d = reinterpret_cast<SampleOut*>(ctx->scratch[7].ptr);
+  count_launches(1);
   sample_index_kernel<<<1, 1024, 0, s>>>(w, n, u, mode, d);
   RPLU_CUDA(cudaGetLastError());
   SampleOut h;

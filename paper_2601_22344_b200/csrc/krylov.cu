@@ -131,6 +131,7 @@ int mgs_arnoldi_impl(rplu_ctx* ctx, const void* V, long long n, int j, void* w, 
   double2* vn = (double2*)vnext;
   double2* hp = (double2*)h;
   void* args[] = {&Vp, &n, &j, &wp, &vn, &hp, &part, &bar};
+  count_launches(1);
   RPLU_CUDA(cudaLaunchCooperativeKernel((const void*)mgs_arnoldi_kernel, dim3(grid),
                                         dim3(kMgsThreads), args, 0, s));
   return 0;

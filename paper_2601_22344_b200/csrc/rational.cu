@@ -18,8 +18,11 @@
 //                      non-finite quotients become 0 (:168).
 // Support sets are small (degree <= a few hundred) and evaluation sets large:
 // one thread per evaluation point, the support staged through shared memory
-// in tiles, FP64-pipe bound (≈ 8 DFMA-pipe ops + one Smith reciprocal per
-// (z, t_j) pair).
+// in tiles, FP64-pipe bound: per (z, t_j) pair 2 sub + |d|^2 (2) + one IEEE
+// reciprocal + 2 mul + two complex MACs (8 FMA).  The entries are
+// conj(d)/|d|^2 (Smith division only where |d|^2 would leave the normal
+// range); the sums are order-dependent anyway (the reference's are BLAS
+// zgemv), so parity is to rounding, not bits.
 #include <cuda_runtime.h>
 #include <float.h>
 #include <stdint.h>
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(256) bary_eval_kernel(const double2* __restric
   const double2 zi = i < nz ? z[i] : make_double2(0.0, 0.0);
   double2 num = make_double2(0.0, 0.0), den = make_double2(0.0, 0.0);
   int hit = -1;
+  const double hit2 = hit_tol * hit_tol * (1.0 + 1e-12);
   for (int j0 = 0; j0 < k; j0 += kBaryTile) {
     const int cnt = min(kBaryTile, k - j0);
     __syncthreads();
@@ -76,9 +80,18 @@ __global__ void __launch_bounds__(256) bary_eval_kernel(const double2* __restric
     }
     __syncthreads();
     for (int c = 0; c < cnt; ++c) {
-      const double2 d = make_double2(__dsub_rn(zi.x, st[c].x), __dsub_rn(zi.y, st[c].y));
-      if (mode == 0 && hypot(d.x, d.y) <= hit_tol) hit = j0 + c;
-      const double2 cj = cdiv_np(make_double2(1.0, 0.0), d);  // 1.0 / (z - t_j)
+      const double dx = zi.x - st[c].x, dy = zi.y - st[c].y;
+      const double d2 = fma(dx, dx, dy * dy);
+      // exact-hit test |z - t_j| <= tol (np.abs = hypot): cheap prefilter on
+      // |d|^2, hypot only for the candidates
+      if (mode == 0 && d2 <= hit2 && hypot(dx, dy) <= hit_tol) hit = j0 + c;
+      double2 cj;
+      if (d2 > 1e-290 && d2 < 1e290) {  // 1/(z - t) = conj(d) / |d|^2
+        const double r = __drcp_rn(d2);
+        cj = make_double2(dx * r, -dy * r);
+      } else {                            // over/underflow-safe Smith division
+        cj = cdiv_np(make_double2(1.0, 0.0), make_double2(dx, dy));
+      }
       num = cmac(num, cj, swf[c]);
       den = cmac(den, cj, sw[c]);
     }
@@ -105,6 +118,7 @@ int loewner_fill_impl(const void* zo, const void* fo, long long no, const void* 
   const long long total = no * k;
   if (total == 0) return 0;
   const long long blocks = std::min<long long>((total + 255) / 256, 148LL * 16);
+  count_launches(1);
   loewner_fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(
       (const double2*)zo, (const double2*)fo, no, (const double2*)zs, (const double2*)fs, k,
       (double2*)out);
@@ -117,6 +131,7 @@ int bary_eval_impl(const void* z, long long nz, const void* t, const void* f, co
                    cudaStream_t s) {
   if (nz == 0) return 0;
   const long long blocks = (nz + 255) / 256;
+  count_launches(1);
   bary_eval_kernel<<<(unsigned)blocks, 256, 0, s>>>(
       (const double2*)z, nz, (const double2*)t, (const double2*)f, (const double2*)w, (int)k,
       hit_tol, mode, (double2*)out, near_pole);

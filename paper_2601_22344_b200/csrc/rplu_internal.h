@@ -103,6 +103,11 @@ int cauchy_shard_finish_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, rpl
 int cauchy_shard_active_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, int* active);
 
 void set_error(const std::string& msg);
+
+// Process-wide count of kernels launched by the standalone primitives
+// (Gaussian-kernel, sample-index, consumer kernels) for bench.py's
+// gpu_launches claim; the pivot-loop drivers report theirs in *_out.
+void count_launches(long long k);
 int cuda_fail(cudaError_t e, const char* where);
 
 #define RPLU_CUDA(call)                                        \

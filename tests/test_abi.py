@@ -17,7 +17,7 @@ def _declared_functions():
     for h in glob.glob(os.path.join(REPO, "include", "*.h")):
         src = open(h).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-        for m in re.finditer(r"^\s*(?:int|const char\*|void)\s+(rplu_\w+)\s*\(", src, flags=re.M):
+        for m in re.finditer(r"^\s*(?:int|int64_t|const char\*|void)\s+(rplu_\w+)\s*\(", src, flags=re.M):
             names.add(m.group(1))
     return sorted(names)
 
