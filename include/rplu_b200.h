@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RPLU_B200_ABI_VERSION 1
+#define RPLU_B200_ABI_VERSION 2
 
 /* status codes (negative = error class; mapped to Python exceptions) */
 #define RPLU_OK 0
@@ -283,7 +283,7 @@ int rplu_cauchy_shard_finish(rplu_ctx* ctx, const rplu_cauchy_shard_args* a,
 typedef struct rplu_tree_plan {
   int64_t n, m;            /* target / source point counts */
   int32_t p;               /* displacement rank */
-  int32_t reserved;
+  int32_t n_levels;        /* internal-node levels (ABI 2) */
   int64_t n_tleaves;       /* target leaves */
   const int64_t* tperm;    /* [n] target points grouped by leaf */
   const int64_t* tstart;   /* [n_tleaves+1] */
@@ -295,8 +295,11 @@ typedef struct rplu_tree_plan {
   int64_t n_snodes, n_sleaves;
   const int64_t* spts;     /* [m] source points grouped by source leaf */
   const int64_t* sstart;   /* [n_sleaves+1] */
-  const int64_t* bstart;   /* [n_snodes+1] source leaves below each node */
-  const int64_t* bleaf;
+  const int64_t* cstart;   /* [n_snodes+1] children of each source node (CSR) */
+  const int64_t* cidx;
+  const int64_t* leaf_node;  /* [n_sleaves] node id of each source leaf */
+  const int64_t* lvl_nodes;  /* internal nodes grouped by level, deepest first */
+  const int64_t* lvl_start;  /* HOST array [n_levels+1]: level slices of lvl_nodes */
 } rplu_tree_plan;
 
 int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,

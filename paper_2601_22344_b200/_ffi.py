@@ -115,11 +115,12 @@ CAUCHY_MSG_DOUBLES = 20   # RPLU_CAUCHY_MSG_DOUBLES
 
 class TreePlan(ctypes.Structure):
     _fields_ = [
-        ("n", c_i64), ("m", c_i64), ("p", c_i32), ("reserved", c_i32), ("n_tleaves", c_i64),
+        ("n", c_i64), ("m", c_i64), ("p", c_i32), ("n_levels", c_i32), ("n_tleaves", c_i64),
         ("tperm", c_vp), ("tstart", c_vp), ("agg_start", c_vp), ("agg_node", c_vp),
         ("agg_alpha", c_vp), ("ex_start", c_vp), ("ex_leaf", c_vp),
         ("n_snodes", c_i64), ("n_sleaves", c_i64), ("spts", c_vp), ("sstart", c_vp),
-        ("bstart", c_vp), ("bleaf", c_vp),
+        ("cstart", c_vp), ("cidx", c_vp), ("leaf_node", c_vp), ("lvl_nodes", c_vp),
+        ("lvl_start", c_vp),
     ]
 
 

@@ -181,8 +181,10 @@ def tree_bounds_device(plan, M):
         agg_start=dp.agg_start.data_ptr(), agg_node=dp.agg_node.data_ptr(),
         agg_alpha=dp.agg_alpha.data_ptr(), ex_start=dp.ex_start.data_ptr(),
         ex_leaf=dp.ex_leaf.data_ptr(), n_snodes=dp.n_snodes, n_sleaves=dp.n_sleaves,
-        spts=dp.spts.data_ptr(), sstart=dp.sstart.data_ptr(), bstart=dp.bstart.data_ptr(),
-        bleaf=dp.bleaf.data_ptr())
+        spts=dp.spts.data_ptr(), sstart=dp.sstart.data_ptr(), cstart=dp.cstart.data_ptr(),
+        cidx=dp.cidx.data_ptr(), leaf_node=dp.leaf_node.data_ptr(),
+        lvl_nodes=dp.lvl_nodes.data_ptr(), lvl_start=dp.lvl_start.ctypes.data,
+        n_levels=dp.n_levels)
     c = _device.ctx(M.device)
     _ffi.check(c._lib.rplu_tree_bounds(c.handle, ctypes.byref(s), M.x.data_ptr(), M.y.data_ptr(),
                                        M.G.data_ptr(), M.Bt.data_ptr(), out.data_ptr(),

@@ -768,7 +768,8 @@ int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, c
                      const void* G, const void* Bt, double* u, void* stream) {
   if (!ctx || !plan || !x || !y || !G || !Bt || !u || plan->n < 1 || plan->m < 1 ||
       plan->p < 1 || plan->p > 8 || plan->n_tleaves < 1 || plan->n_snodes < 1 ||
-      plan->n_sleaves < 1) {
+      plan->n_sleaves < 1 || !plan->cstart || !plan->leaf_node || plan->n_levels < 0 ||
+      (plan->n_levels > 0 && (!plan->lvl_nodes || !plan->lvl_start))) {
     set_error("rplu_tree_bounds: bad argument");
     return RPLU_ERR_ARG;
   }

@@ -7,10 +7,11 @@
 //       + sum_{s in E_leaf(i)} sum_{j in s} |g_i . B_:,j|^2 / |x_i - y_j|^2
 //
 // Gram matrices: one warp per source leaf (lanes over the p^2 entries), then
-// one warp per node summing the leaves below it.  Bounds: one CTA per target
-// leaf, one thread per target point, the node Grams read through L1/L2
-// (broadcast: every thread of the CTA uses the same H_s).  Work per step is
-// O((n+m)|A| p^2) instead of the exact norms' O(n m p).
+// one warp per node summing the leaves below it.  Bounds: one warp per target
+// leaf folds the leaf's aggregated interactions into one p x p matrix, then
+// evaluates one quadratic form per target point.  Work per step is
+// O(m p^2 + |leaves| |A| p^2 + n p^2 + exact pairs) instead of the exact
+// norms' O(n m p).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,9 +29,8 @@ struct TreeParams {
   const double* agg_alpha;
   const long long *ex_start, *ex_leaf;
   const long long *spts, *sstart;
-  const long long *bstart, *bleaf;
+  const long long *cstart, *cidx, *leaf_node;
   const double2 *x, *y, *G, *Bt;
-  double2* Hleaf;  // n_sleaves x p x p
   double2* Hnode;  // n_snodes x p x p
   double* u;       // n
 };
@@ -59,58 +59,80 @@ __global__ void tree_gram_leaf_kernel(TreeParams q) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int e = lane + 32 * h;
-    if (e < P * P) q.Hleaf[leaf * P * P + e] = acc[h];
+    if (e < P * P) q.Hnode[q.leaf_node[leaf] * P * P + e] = acc[h];
   }
 }
 
+// Internal node Grams bottom-up, one launch per tree level (deepest first):
+// one warp per node, lanes over the P*P entries, H_node = sum of its
+// children's H in child order (the reference's _gram_bottom_up,
+// treebounds.py:196-210).  O(n_snodes p^2) in ~depth short launches.  (A
+// warp — or CTA — per node summing every leaf below it made the root, ~60k
+// leaves at C4, a serial 1-7 ms chain.)
 template <int P>
-__global__ void tree_gram_node_kernel(TreeParams q) {
-  const long long node = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256) tree_gram_level_kernel(TreeParams q,
+                                                              const long long* __restrict__ nodes,
+                                                              long long count) {
+  const long long w = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (node >= q.n_snodes) return;
-  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-  for (long long k = q.bstart[node]; k < q.bstart[node + 1]; ++k) {
-    const long long lf = q.bleaf[k];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int e = lane + 32 * h;
-      if (e < P * P) {
-        const double2 v = q.Hleaf[lf * P * P + e];
-        acc[h].x += v.x;
-        acc[h].y += v.y;
-      }
+  if (w >= count) return;
+  const long long node = nodes[w];
+  const long long c0 = q.cstart[node], c1 = q.cstart[node + 1];
+  for (int e = lane; e < P * P; e += 32) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long c = c0; c < c1; ++c) {
+      const double2 v = q.Hnode[q.cidx[c] * P * P + e];
+      acc.x += v.x;
+      acc.y += v.y;
     }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int e = lane + 32 * h;
-    if (e < P * P) q.Hnode[node * P * P + e] = acc[h];
+    q.Hnode[node * P * P + e] = acc;
   }
 }
 
+// One warp per target leaf.  The aggregated part is linear in the Grams, so
+// the warp first folds the leaf's interaction list into one p x p matrix
+// M = sum_(s,alpha) alpha H_s in shared memory (lanes over the p^2 entries;
+// ~34 nodes per leaf at C4), then each lane evaluates Re(g_i M g_i^H) for its
+// target points: O(p^2) per point instead of O(|A| p^2).  The exact part
+// sums |g_i . B_:,j|^2 / |x_i - y_j|^2 over the leaf's exact source leaves.
+constexpr int kTreeWarps = 4;
+
 template <int P>
-__global__ void __launch_bounds__(64) tree_bounds_kernel(TreeParams q) {
-  const long long leaf = blockIdx.x;
+__global__ void __launch_bounds__(32 * kTreeWarps) tree_bounds_kernel(TreeParams q) {
+  __shared__ double2 Ms[kTreeWarps][P * P];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long leaf = (long long)blockIdx.x * kTreeWarps + wid;
+  if (leaf >= q.n_tleaves) return;  // warp-uniform
   const long long a0 = q.agg_start[leaf], a1 = q.agg_start[leaf + 1];
   const long long e0 = q.ex_start[leaf], e1 = q.ex_start[leaf + 1];
-  for (long long k = q.tstart[leaf] + threadIdx.x; k < q.tstart[leaf + 1]; k += blockDim.x) {
+  for (int c = lane; c < P * P; c += 32) {
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (long long e = a0; e < a1; ++e) {
+      const double al = q.agg_alpha[e];
+      const double2 v = q.Hnode[q.agg_node[e] * P * P + c];
+      acc.x = fma(al, v.x, acc.x);
+      acc.y = fma(al, v.y, acc.y);
+    }
+    Ms[wid][c] = acc;
+  }
+  __syncwarp();
+  const double2* M = Ms[wid];
+  for (long long k = q.tstart[leaf] + lane; k < q.tstart[leaf + 1]; k += 32) {
     const long long i = q.tperm[k];
     double2 g[P];
 #pragma unroll
     for (int l = 0; l < P; ++l) g[l] = q.G[i * P + l];
     const double2 xi = q.x[i];
     double acc = 0.0;
-    for (long long e = a0; e < a1; ++e) {  // aggregated: alpha * Re(g H g^H)
-      const double2* H = q.Hnode + q.agg_node[e] * P * P;
-      double val = 0.0;
+    if (a1 > a0) {  // aggregated: Re(g M g^H)
 #pragma unroll
       for (int a = 0; a < P; ++a) {
         double2 t = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < P; ++b) t = cfma_conj(t, H[a * P + b], g[b]);  // (H conj(g))_a
-        val = fma(g[a].x, t.x, fma(-g[a].y, t.y, val));                 // Re(g_a t_a)
+        for (int b = 0; b < P; ++b) t = cfma_conj(t, M[a * P + b], g[b]);  // (M conj(g))_a
+        acc = fma(g[a].x, t.x, fma(-g[a].y, t.y, acc));                  // Re(g_a t_a)
       }
-      acc = fma(q.agg_alpha[e], val, acc);
     }
     for (long long e = e0; e < e1; ++e) {  // exact: sum over the source leaf's points
       const long long lf = q.ex_leaf[e];
@@ -163,8 +185,9 @@ int tree_bounds_impl(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, c
   q.ex_leaf = reinterpret_cast<const long long*>(plan->ex_leaf);
   q.spts = reinterpret_cast<const long long*>(plan->spts);
   q.sstart = reinterpret_cast<const long long*>(plan->sstart);
-  q.bstart = reinterpret_cast<const long long*>(plan->bstart);
-  q.bleaf = reinterpret_cast<const long long*>(plan->bleaf);
+  q.cstart = reinterpret_cast<const long long*>(plan->cstart);
+  q.cidx = reinterpret_cast<const long long*>(plan->cidx);
+  q.leaf_node = reinterpret_cast<const long long*>(plan->leaf_node);
   q.x = reinterpret_cast<const double2*>(x);
   q.y = reinterpret_cast<const double2*>(y);
   q.G = reinterpret_cast<const double2*>(G);
@@ -172,14 +195,19 @@ int tree_bounds_impl(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, c
   q.u = u;
   const size_t pp = (size_t)q.p * q.p;
   int rc;
-  if ((rc = ctx->scratch[6].ensure(sizeof(double2) * pp * (size_t)(q.n_sleaves + q.n_snodes))))
-    return rc;
-  q.Hleaf = reinterpret_cast<double2*>(ctx->scratch[6].ptr);
-  q.Hnode = q.Hleaf + pp * q.n_sleaves;
-  const unsigned gl = (unsigned)((q.n_sleaves + 7) / 8), gn = (unsigned)((q.n_snodes + 7) / 8);
+  if ((rc = ctx->scratch[6].ensure(sizeof(double2) * pp * (size_t)q.n_snodes))) return rc;
+  q.Hnode = reinterpret_cast<double2*>(ctx->scratch[6].ptr);
+  const unsigned gl = (unsigned)((q.n_sleaves + 7) / 8);
   RPLU_TREE_P_SWITCH(q.p, (tree_gram_leaf_kernel<PP><<<gl, 256, 0, s>>>(q)));
-  RPLU_TREE_P_SWITCH(q.p, (tree_gram_node_kernel<PP><<<gn, 256, 0, s>>>(q)));
-  RPLU_TREE_P_SWITCH(q.p, (tree_bounds_kernel<PP><<<(unsigned)q.n_tleaves, 64, 0, s>>>(q)));
+  const long long* lvl_nodes = reinterpret_cast<const long long*>(plan->lvl_nodes);
+  for (int l = 0; l < plan->n_levels; ++l) {
+    const long long b0 = plan->lvl_start[l], cnt = plan->lvl_start[l + 1] - b0;
+    if (cnt <= 0) continue;
+    const unsigned gb = (unsigned)((cnt + 7) / 8);
+    RPLU_TREE_P_SWITCH(q.p, (tree_gram_level_kernel<PP><<<gb, 256, 0, s>>>(q, lvl_nodes + b0, cnt)));
+  }
+  RPLU_TREE_P_SWITCH(q.p, (tree_bounds_kernel<PP><<<(unsigned)((q.n_tleaves + kTreeWarps - 1) / kTreeWarps),
+                                                       32 * kTreeWarps, 0, s>>>(q)));
   RPLU_CUDA(cudaGetLastError());
   return RPLU_OK;
 }

@@ -194,17 +194,22 @@ class _DevicePlan:
         for leaf in src.leaves:
             spts.extend(int(i) for i in src.node_points[leaf])
             sstart.append(len(spts))
-        below = [[] for _ in range(src.n_nodes)]
-        for leaf in src.leaves:
-            k = leaf
-            while k != -1:
-                below[k].append(sleaf_index[leaf])
-                k = src.parent[k]
-        bstart, bleaf = [0], []
+        # children CSR and the internal nodes grouped by depth, deepest first
+        # (node Grams are summed bottom-up from their children, one launch
+        # per level, as the reference's _gram_bottom_up, treebounds.py:196-210)
+        cstart, cidx = [0], []
         for k in range(src.n_nodes):
-            bleaf.extend(below[k])
-            bstart.append(len(bleaf))
-
+            cidx.extend(src.children[k])
+            cstart.append(len(cidx))
+        depth = [0] * src.n_nodes
+        for k in range(1, src.n_nodes):          # parents precede children
+            depth[k] = depth[src.parent[k]] + 1
+        internal = [k for k in range(src.n_nodes) if src.children[k]]
+        levels = sorted(set(depth[k] for k in internal), reverse=True)
+        lvl_nodes, lvl_start = [], [0]
+        for d in levels:
+            lvl_nodes.extend(k for k in internal if depth[k] == d)
+            lvl_start.append(len(lvl_nodes))
         def i64(a):
             return torch.tensor(np.asarray(a, dtype=np.int64), device=device)
 
@@ -217,7 +222,11 @@ class _DevicePlan:
         self.ex_leaf = i64([sleaf_index[s] for s in ex_leaf] if ex_leaf else [0])
         self.n_snodes, self.n_sleaves = src.n_nodes, len(src.leaves)
         self.spts, self.sstart = i64(spts), i64(sstart)
-        self.bstart, self.bleaf = i64(bstart), i64(bleaf)
+        self.cstart, self.cidx = i64(cstart), i64(cidx if cidx else [0])
+        self.leaf_node = i64(list(src.leaves))
+        self.lvl_nodes = i64(lvl_nodes if lvl_nodes else [0])
+        self.lvl_start = np.asarray(lvl_start, dtype=np.int64)   # host
+        self.n_levels = len(levels)
         self.max_leaf = max(int(np.diff(tstart).max()), int(np.diff(sstart).max()))
 
 

@@ -32,7 +32,7 @@ def test_library_exports_all_declared_symbols():
     lib = _ffi.load_library()
     for name in _declared_functions():
         assert hasattr(lib, name), f"{name} declared in include/ but not exported"
-    assert lib.rplu_abi_version() == 1
+    assert lib.rplu_abi_version() == 2
 
 
 def test_ffi_signatures_cover_header():
