@@ -15,3 +15,4 @@ running the reference itself in the build container
 
 from .rplu_oracle import *  # noqa: F401,F403
 from . import consumers_oracle as consumers  # noqa: F401,E402  (§8(f4) consumers)
+from . import plan_oracle as plan  # noqa: F401,E402  (§8(f1) certified bounds)

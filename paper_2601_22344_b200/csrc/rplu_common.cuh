@@ -248,7 +248,8 @@ __device__ Cdf<BLOCK> cdf_build(const WF& wf, long long n, CdfSmem<BLOCK>& s) {
 // near-boundary accounting.
 template <int BLOCK, typename WF>
 __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>& c,
-                                     double target, CdfSmem<BLOCK>& s);
+                                     double target, CdfSmem<BLOCK>& s, double cbase = 0.0,
+                                     bool walk_back = true);
 
 template <int BLOCK, typename WF>
 __device__ __forceinline__ long long cdf_find(const WF& wf, long long n, const Cdf<BLOCK>& c,
@@ -257,14 +258,19 @@ __device__ __forceinline__ long long cdf_find(const WF& wf, long long n, const C
 }
 
 // Same search against an absolute target in [0, total] (sharded draws).
+// `cbase` offsets every CDF value of this block (c_k = base + (excl_w + ...)):
+// the chunked large-n draw runs the search on its owner chunk with base = the
+// chunk's exclusive prefix (cbase = 0 adds nothing: identical results).
+// walk_back = false leaves a zero-weight selection to the caller.
 template <int BLOCK, typename WF>
 __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>& c,
-                                     double target, CdfSmem<BLOCK>& s) {
+                                     double target, CdfSmem<BLOCK>& s, double cbase,
+                                     bool walk_back) {
   constexpr int W = BLOCK / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (w == 0) {  // owner = first segment whose running sum exceeds the target
     static_assert(W <= 32, "one lane per segment");
-    const bool gt = lane < W && s.wincl[lane] > target;
+    const bool gt = lane < W && cbase + s.wincl[lane] > target;
     const unsigned hit = __ballot_sync(0xffffffffu, gt);
     const int owner = hit ? __ffs(hit) - 1 : -1;
     if (lane == 0) {
@@ -273,8 +279,8 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
       if (owner < 0) {
         // u*total >= every partial sum: searchsorted returns n, clamp to n-1
         s.idx = n - 1;
-        s.lo_c = c.total;
-        s.hi_c = c.total;
+        s.lo_c = cbase + c.total;
+        s.hi_c = cbase + c.total;
       }
     }
   }
@@ -282,7 +288,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
   if (w == s.owner) {
     const long long lo = min((long long)w * c.seg, n), hi = min(lo + c.seg, n);
     const double ex = s.wexcl[w];
-    double run = 0.0, prev = ex;
+    double run = 0.0, prev = cbase + ex;
     bool done = false;
     for (long long base = lo; base < hi && !done; base += 32 * kCdfUnroll) {
       double xs[kCdfUnroll];
@@ -296,7 +302,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
         const long long sb = base + 32 * u;
         if (done || sb >= hi) break;
         const double p = warp_incl_scan(xs[u]);
-        const double ck = ex + (run + p);
+        const double ck = cbase + (ex + (run + p));
         const unsigned hit = __ballot_sync(0xffffffffu, (sb + lane < hi) && ck > target);
         if (hit) {
           const int L = __ffs(hit) - 1;
@@ -313,7 +319,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
           done = true;
         } else {
           run += __shfl_sync(0xffffffffu, p, 31);
-          prev = ex + run;
+          prev = cbase + (ex + run);
         }
       }
     }
@@ -322,7 +328,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
       // the interval up to incl_w
       s.idx = hi - 1;
       s.lo_c = prev;
-      s.hi_c = s.wincl[w];
+      s.hi_c = cbase + s.wincl[w];
     }
   }
   __syncthreads();
@@ -330,7 +336,7 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
   // walk back over zero weights (rng.py:70-73)
   const double wi = s.has_wsel ? s.wsel : wf(i);
   __syncthreads();
-  if (!(wi > 0.0)) {
+  if (walk_back && !(wi > 0.0)) {
     // largest k <= i with w(k) > 0, else smallest k with w(k) > 0
     long long best_lo = -1, best_any = n;
     for (long long k = threadIdx.x; k < n; k += BLOCK) {

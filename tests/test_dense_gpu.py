@@ -80,6 +80,46 @@ def test_sample_index_boundaries(cuda_device):
         assert abs(rp.sample_index(big, u) - oracle.sample_index(big, u)) <= 1
 
 
+def test_sample_index_chunked_large_n(cuda_device):
+    """n >= 131072 uses the two-level (chunked) CDF: same semantics as the
+    reference's sample_index (first running sum > u*total, clamp, zero
+    walk-back), draws equal to the oracle's except within 1e-12 of a CDF
+    boundary; zero runs across chunk boundaries, leading zero chunks and a
+    zero tail exercise the walk-back and the clamp."""
+    g = np.random.default_rng(3)
+    n = 5 * 32768 + 123
+    cases = []
+    w = g.random(n)
+    cases.append(w)
+    w = g.random(n)
+    w[: 2 * 32768 + 7] = 0.0                  # leading zero chunks
+    cases.append(w)
+    w = g.random(n)
+    w[32768 - 50: 2 * 32768 + 50] = 0.0       # zero run across two chunk boundaries
+    w[-1000:] = 0.0                           # zero tail (clamp + walk-back)
+    cases.append(w)
+    w = np.zeros(n)
+    w[[5, 40000, 150000]] = [1.0, 2.0, 3.0]   # sparse
+    cases.append(w)
+    us = list(g.random(40)) + [0.0, 1.0 - 2 ** -53, 0.5]
+    for w in cases:
+        tot = float(np.sum(w))
+        for u in us:
+            got = rp.sample_index(w, u)
+            want = oracle.sample_index(w, u)
+            if got != want:
+                c = np.cumsum(w)
+                lo = c[min(got, want)]
+                assert abs(lo - u * c[-1]) <= 1e-12 * tot, (u, got, want)
+            assert w[got] > 0.0
+    with pytest.raises(ValueError):
+        bad = g.random(n)
+        bad[100000] = -1.0
+        rp.sample_index(bad, 0.3)
+    with pytest.raises(ValueError):
+        rp.sample_index(np.zeros(n), 0.3)
+
+
 def test_sample_target_and_cdf_total(cuda_device):
     """The owner-shard draw against an absolute target and the per-shard CDF
     totals (rplu_sample_target / rplu_cdf_total) keep sample_index's

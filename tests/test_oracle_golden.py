@@ -237,3 +237,14 @@ def test_oracle_smw_gmres_match_reference(idx):
     assert (iters, conv) == (case["plain"]["iterations"], case["plain"]["converged"])
     np.testing.assert_allclose(hist, arr[name + "_hist_plain"], rtol=1e-6)
     np.testing.assert_allclose(x, arr[name + "_x_plain"], rtol=1e-7, atol=1e-9)
+
+
+def test_oracle_certified_bounds_match_reference():
+    from paper_2601_22344_b200 import treebounds as tb
+    info, arr = load_golden("cauchy_plan")
+    for case in info["cases"]:
+        name = case["name"]
+        x, y = arr[name + "_x"], arr[name + "_y"]
+        plan = tb.build_plan(x, y, nu=case["nu"], leaf_size=case["leaf_size"])
+        u = oracle.plan.certified_upper_bounds(plan, arr[name + "_G"], arr[name + "_B"])
+        np.testing.assert_allclose(u, arr[name + "_u0"], rtol=1e-13)
