@@ -46,6 +46,10 @@ CONFIGS = {
     "c5": dict(desc="C5 matrix-free Gaussian kernel fp64 2e6 x 2e6 (BASELINE configs[4]); bench "
                     "step = `rank` pivot steps of the rank-1024 cur_build",
                n=2_000_000, rank=2, dtype="f64", seed=0, kind="cur"),
+    "c4plan": dict(desc="C4 Cauchy-like c128 2^20 x 2^20 p=4 rank 256 (BASELINE configs[3]) "
+                        "through the certified-bound plan path (build_plan + rejection "
+                        "sampling), as every in-package Cauchy caller runs it",
+                   n=1 << 20, rank=256, dtype="c128", seed=0, kind="cauchy_plan", p=4),
     # §8(f4) consumers (not BASELINE configs: supplementary measurement lines)
     "gmres": dict(desc="SURVEY 8(f4) restarted GMRES: one 20-step MGS Arnoldi cycle on n=2^24 "
                        "complex128 (stencil operator); bench step = one restart cycle",
@@ -580,12 +584,117 @@ def run_bary_arm(args, cfg):
                                              "ms": fit_ms}})
 
 
+def run_cauchy_plan_arm(args, cfg):
+    """C4 through the plan path: one bench step = one full rank-256
+    structured_eliminate(plan=...) on the resident generators (the plan is
+    built once, untimed, like the generators)."""
+    import warnings
+
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _ffi, gen
+    torch.cuda.set_device(0)
+    n, rank, seed, p = cfg["n"], cfg["rank"], cfg["seed"], cfg["p"]
+    x, y, G, B = gen.c4_cauchy_like(seed, n=n, p=p)
+    t0 = time.perf_counter()
+    plan = rp.build_plan(x, y, nu=5.0)
+    plan_s = time.perf_counter() - t0
+    M = rp.CauchyLikeMatrix(x, y, G, B, check_points=False)
+    warnings.simplefilter("ignore")
+    for _ in range(args.warmup):
+        rp.structured_eliminate(M, "rplu", rank, plan=plan, rng=rp.RngState(seed),
+                                host_steps=False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _ffi.kernel_launch_count()
+    e0.record()
+    for _ in range(args.steps):
+        tr = rp.structured_eliminate(M, "rplu", rank, plan=plan, rng=rp.RngState(seed),
+                                     host_steps=False)
+    e1.record()
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    launches = _ffi.kernel_launch_count() - l0
+    clk = clocks.stop()
+    k = tr.rank
+    value = args.steps * k / (total_ms / 1e3)
+    # second pass: the certified-bound kernels alone (the step's FP64 work)
+    from paper_2601_22344_b200.cauchy import tree_bounds_device
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(10):
+        tree_bounds_device(plan, M)
+    a1.record()
+    torch.cuda.synchronize()
+    bounds_ms = a0.elapsed_time(a1) / 10
+    tt, st = plan.target_tree, plan.source_tree
+    n_agg = sum(len(plan.aggregated[l]) for l in tt.leaves)
+    # algorithmic FP64 work of one bound evaluation: source Grams 8 p^2 flop
+    # per source point, leaf folds 2 p^2 per aggregated entry, the quadratic
+    # form 8 p^2 per target point
+    flops = 8.0 * p * p * n + 2.0 * p * p * n_agg + 8.0 * p * p * n
+    peak = _ffi.fp64_peak_tflops(0)
+    # e2e: host generators in (public call incl. the host plan build), host
+    # index lists out
+    e0.record()
+    Mh = rp.CauchyLikeMatrix(x, y, G, B, check_points=False)
+    planh = rp.build_plan(x, y, nu=5.0)
+    trh = rp.structured_eliminate(Mh, "rplu", rank, plan=planh, rng=rp.RngState(seed),
+                                  host_steps=False)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    # CPU: the oracle's restatement of the reference's certified bounds (the
+    # reference's plan step is this per-leaf loop plus O(n + m) row work)
+    t0 = time.perf_counter()
+    oracle.plan.certified_upper_bounds(plan, G, B)
+    cpu_s = time.perf_counter() - t0
+    model, _ = _cpu_info()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded BASELINE construction)",
+        "config": {"workload": cfg["desc"], "n": n, "m": n, "p": p, "rank": rank, "seed": seed,
+                   "step": f"one structured_eliminate(plan=...) run of {rank} pivot steps",
+                   "plan_build_s": plan_s, "l2": "generated entries; generators only in HBM"},
+        "roofline": {"bound": "latency", "achieved": flops / (bounds_ms / 1e3) / 1e12,
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / (bounds_ms / 1e3) / 1e12 / peak, "traffic": None,
+                     "kernel": "tree Gram + bounds kernels (certified row-norm bounds per step)",
+                     "algorithmic_flops_per_launch": flops, "avg_launch_ms": bounds_ms,
+                     "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)",
+                     "note": "the plan step is latency bound (draws, host acceptance test); "
+                             "bounds are %.0f%% of it" % (100 * bounds_ms * k * args.steps
+                                                          / total_ms)},
+        "cpu_baseline": {"value": 1.0 / cpu_s, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"one certified-bound evaluation at full size ({cpu_s:.1f}s, "
+                                   f"the reference's per-step cost before its O(n+m) row work);"
+                                   f" CPU: {model}"},
+        "e2e": {"value": k / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * (2 + 2 * p) * n,
+                "d2h_bytes_per_step": 16 * k},
+        "gpu_launches": launches,
+        "near_boundary_draws": tr.near_boundary_draws,
+        "proposals": tr.proposals, "acceptances": tr.acceptances,
+        "near_tie_acceptances": tr.near_tie_acceptances,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200_arm(args, cfg, dist, rank_id, world):
     import torch
     if cfg.get("kind") == "cauchy":
         return run_cauchy_arm(args, cfg)
     if cfg.get("kind") == "cur":
         return run_cur_arm(args, cfg)
+    if cfg.get("kind") == "cauchy_plan":
+        return run_cauchy_plan_arm(args, cfg)
     if cfg.get("kind") == "gmres":
         return run_gmres_arm(args, cfg)
     if cfg.get("kind") == "bary":

@@ -292,7 +292,7 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
     """
     import warnings
 
-    from .rng import sample_index
+    from .rng import sample_index as _si
     tgt, src = plan.target_tree, plan.source_tree
     if tgt.points.size != M.shape[0] or src.points.size != M.shape[1]:
         raise ValueError("generator dimensions do not match the plan's points")
@@ -301,6 +301,11 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
     cap = int(REJECTION_CAP_FACTOR * max(nu, 1.0))
     stream = _UniformCursor(rng if rule == "rplu" else None, max(8, (2 * cap + 3) * rank))
     tr = StructuredPivotTrace(residual=cur)
+
+    def sample_index(w, u):
+        i, near = _si(w, u, return_near=True)
+        tr.near_boundary_draws += int(near)
+        return i
     u0_max = None
     steps_dev = []
     try:

@@ -73,11 +73,13 @@ class UniformBlock:
             self._gen.random(int(consumed))
 
 
-def sample_index(weights, u):
+def sample_index(weights, u, *, return_near=False):
     """Index with probability proportional to nonnegative weights (rng.py:50-74).
 
     Runs the same device CDF code the pivot loops use.  Raises ValueError on
-    empty, negative or all-zero weights, as the reference does.
+    empty, negative or all-zero weights, as the reference does.  With
+    ``return_near`` also reports whether the draw fell within 1e-12 relative
+    of a CDF boundary.
     """
     import torch
 
@@ -100,4 +102,6 @@ def sample_index(weights, u):
     _ffi.check(c._lib.rplu_sample_index(c.handle, ctypes.c_void_p(w.data_ptr()), w.numel(),
                                         float(u), ctypes.byref(idx), ctypes.byref(near),
                                         _device.stream_handle(w.device)))
+    if return_near:
+        return int(idx.value), bool(near.value)
     return int(idx.value)
