@@ -16,6 +16,7 @@
 // memory tile of (y_j, B_j) (column side), so a step is FP64-pipe bound.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -110,8 +111,13 @@ __global__ void __launch_bounds__(256) cauchy_mass_kernel(CauchyParams q) {
     for (int c = threadIdx.x; c < TJ; c += NT) {
       if (c < cnt) {
         sy[c] = q.y[jt + c];
+        if constexpr (P == 1) {
+          const double2 bj = q.Bt[jt + c];
+          sb[c] = make_double2(fma(bj.x, bj.x, bj.y * bj.y), 0.0);
+        } else {
 #pragma unroll
-        for (int l = 0; l < P; ++l) sb[c * P + l] = q.Bt[(jt + c) * P + l];
+          for (int l = 0; l < P; ++l) sb[c * P + l] = q.Bt[(jt + c) * P + l];
+        }
       }
     }
     __syncthreads();
@@ -123,24 +129,32 @@ __global__ void __launch_bounds__(256) cauchy_mass_kernel(CauchyParams q) {
       for (int l = 0; l < P; ++l) b[l] = sb[c * P + l];
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        double re = 0.0, im = 0.0;
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-          re = fma(g[r][l].x, b[l].x, re);
-          re = fma(-g[r][l].y, b[l].y, re);
-          im = fma(g[r][l].x, b[l].y, im);
-          im = fma(g[r][l].y, b[l].x, im);
-        }
         const double dr = xr[r].x - yj.x, di = xr[r].y - yj.y;
-        const double num = fma(re, re, im * im);
         const double den = fma(dr, dr, di * di);
-        acc[r] = fma(num, rcp_nr(den), acc[r]);
+        if constexpr (P == 1) {
+          // displacement rank 1: |g_i b_j|^2 = |g_i|^2 |b_j|^2, so the
+          // column weight |b_j|^2 (staged in sb[c].x) is accumulated here
+          // and |g_i|^2 applied once per row: 9 FP64 ops per entry, not 15
+          acc[r] = fma(b[0].x, rcp_nr(den), acc[r]);
+        } else {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            re = fma(g[r][l].x, b[l].x, re);
+            re = fma(-g[r][l].y, b[l].y, re);
+            im = fma(g[r][l].x, b[l].y, im);
+            im = fma(g[r][l].y, b[l].x, im);
+          }
+          const double num = fma(re, re, im * im);
+          acc[r] = fma(num, rcp_nr(den), acc[r]);
+        }
       }
     }
   }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     long long i = row_base + threadIdx.x + (long long)r * NT;
+    if constexpr (P == 1) acc[r] *= fma(g[r][0].x, g[r][0].x, g[r][0].y * g[r][0].y);
     if (valid[r]) q.partial[(long long)blockIdx.y * q.n + i] = acc[r];
   }
   if (q.splits > 1 && q.blk_count) {
@@ -482,10 +496,20 @@ __global__ void cauchy_snapshot_kernel(CauchyParams q, double2* gsnap) {
 static int choose_splits(long long n, long long m, int rows_per_cta, int sm_count) {
   // latency-bound sizes: about two CTAs per SM (a whole number of CTAs per
   // SM, so no SM runs a lone extra CTA), each with >= 64 columns
+  static const int per_sm = [] {  // RPLU_CAUCHY_CTAS_PER_SM experiment override
+    const char* e = getenv("RPLU_CAUCHY_CTAS_PER_SM");
+    const int v = e ? atoi(e) : 2;
+    return v >= 1 && v <= 8 ? v : 2;
+  }();
+  static const int min_cols = [] {
+    const char* e = getenv("RPLU_CAUCHY_MIN_COLS");
+    const int v = e ? atoi(e) : 64;
+    return v >= 8 && v <= 4096 ? v : 64;
+  }();
   long long row_blocks = (n + rows_per_cta - 1) / rows_per_cta;
-  long long want = 2LL * sm_count;
+  long long want = (long long)per_sm * sm_count;
   long long s = (want + row_blocks - 1) / row_blocks;
-  long long max_s = (m + 63) / 64;
+  long long max_s = (m + min_cols - 1) / min_cols;
   if (s > max_s) s = max_s;
   if (s < 1) s = 1;
   if (s > 1024) s = 1024;
