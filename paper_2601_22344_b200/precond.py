@@ -257,7 +257,9 @@ def gmres(K, b, M_inv=None, restart=20, tol=1e-10, max_restarts=200, x0=None, de
     history = []
     best_x, best_res = x.clone(), np.inf
     total_iters = 0
-    V = torch.zeros((restart + 1, n), dtype=torch.complex128, device=dev)
+    # every basis row is written before it is read (row j+1 by the Arnoldi
+    # kernel, or zeroed below when H[j+1, j] == 0), so no fill pass is needed
+    V = torch.empty((restart + 1, n), dtype=torch.complex128, device=dev)
     hcol = torch.zeros(restart + 2, dtype=torch.complex128, device=dev)
 
     for _ in range(max_restarts):
@@ -266,7 +268,6 @@ def gmres(K, b, M_inv=None, restart=20, tol=1e-10, max_restarts=200, x0=None, de
         if beta / bnorm <= tol:
             return GmresResult(out(x), np.array(history), total_iters, True)
         cycle_start = beta / bnorm
-        V.zero_()
         H = np.zeros((restart + 1, restart), dtype=np.complex128)
         cs = np.zeros(restart, dtype=np.complex128)
         sn = np.zeros(restart, dtype=np.complex128)
@@ -279,6 +280,8 @@ def gmres(K, b, M_inv=None, restart=20, tol=1e-10, max_restarts=200, x0=None, de
             _ffi.check(c._lib.rplu_mgs_arnoldi(c.handle, V.data_ptr(), n, j, w.data_ptr(),
                                                V[j + 1].data_ptr(), hcol.data_ptr(), stream))
             H[:j + 2, j] = hcol[:j + 2].cpu().numpy()
+            if not H[j + 1, j].real > 0:     # lucky breakdown: the reference's V[:, j+1] stays 0
+                V[j + 1].zero_()
             for t in range(j):
                 tmp = cs[t] * H[t, j] + sn[t] * H[t + 1, j]
                 H[t + 1, j] = -np.conj(sn[t]) * H[t, j] + np.conj(cs[t]) * H[t + 1, j]
