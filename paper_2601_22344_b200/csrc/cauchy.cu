@@ -79,9 +79,8 @@ __device__ __forceinline__ double rcp_nr(double d) {
 
 // ---------------------------------------------------------------------------
 // K5: partial[s][i] = sum_{j in split s} |G_i . B_j|^2 / |x_i - y_j|^2
-template <int P, int RPT, int TJ>
-__global__ void __launch_bounds__(256) cauchy_mass_kernel(CauchyParams q) {
-  constexpr int NT = 256;
+template <int P, int RPT, int TJ, int NT>
+__global__ void __launch_bounds__(NT) cauchy_mass_kernel(CauchyParams q) {
   if (q.st && !q.st->active) return;
   __shared__ double2 sy[TJ];
   __shared__ double2 sb[TJ * P];
@@ -516,12 +515,31 @@ static int choose_splits(long long n, long long m, int rows_per_cta, int sm_coun
   return (int)s;
 }
 
+// K5 CTA shape: rows_per_cta(p) rows per CTA either as 256 threads x 2 rows
+// (ILP: compute-bound sizes, C4 1956 ms vs 2022 ms) or 512 threads x 1 row
+// (TLP: latency-bound sizes, C2 22.4 us vs 26.0 us per launch).  The per-row
+// summation order is the same in both (bit-identical masses).
+// RPLU_CAUCHY_MASS_TLP=0/1 forces either.
+static bool mass_tlp(long long n, long long m) {
+  static const int v = [] {
+    const char* e = getenv("RPLU_CAUCHY_MASS_TLP");
+    return e ? atoi(e) : -1;
+  }();
+  if (v == 0 || v == 1) return v == 1;
+  return (double)n * (double)m <= 268435456.0;  // 2^28 entries
+}
+
 template <int P>
 static void launch_mass(CauchyParams& q, cudaStream_t s) {
-  constexpr int RPT = (P <= 4) ? 2 : 1;
   constexpr int TJ = 128;
+  if (P <= 4 && mass_tlp(q.n, q.m)) {
+    dim3 grid((unsigned)((q.n + 511) / 512), (unsigned)q.splits);
+    cauchy_mass_kernel<P, 1, TJ, 512><<<grid, 512, 0, s>>>(q);
+    return;
+  }
+  constexpr int RPT = (P <= 4) ? 2 : 1;
   dim3 grid((unsigned)((q.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)q.splits);
-  cauchy_mass_kernel<P, RPT, TJ><<<grid, 256, 0, s>>>(q);
+  cauchy_mass_kernel<P, RPT, TJ, 256><<<grid, 256, 0, s>>>(q);
 }
 
 #define RPLU_P_SWITCH(p, CALL)      \
