@@ -305,6 +305,30 @@ typedef struct rplu_tree_plan {
 int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
                      const void* G, const void* Bt, double* u, void* stream);
 
+/* Host-native interaction-plan build (no GPU needed), replacing the Python
+ * quadtrees and dual traversal of rplu.treebounds.build_plan
+ * (treebounds.py:47-104, :141-180) with identical results.  x: n complex
+ * points (re, im pairs), y: m.  On coincident target / source points returns
+ * RPLU_ERR_ARG with coincident[0] = target index, coincident[1] = source
+ * index (CoincidentPointsError in the Python layer). */
+typedef struct rplu_plan_host rplu_plan_host;
+int rplu_plan_build(const double* x, int64_t n, const double* y, int64_t m, double nu,
+                    int64_t leaf_size, int64_t* coincident, rplu_plan_host** out);
+/* counts[8]: target nodes, target leaves, target child links, source nodes,
+ * source leaves, source child links, aggregated entries, exact entries */
+int rplu_plan_counts(const rplu_plan_host* h, int64_t* counts);
+/* which = 0 target tree, 1 source tree: node boxes (x0, y0, size), parent,
+ * children CSR (cstart[nodes+1], cidx), leaves in traversal order and their
+ * points (lpstart[leaves+1], lpidx) */
+int rplu_plan_tree(const rplu_plan_host* h, int32_t which, double* x0, double* y0, double* size,
+                   int64_t* parent, int64_t* cstart, int64_t* cidx, int64_t* leaves,
+                   int64_t* lpstart, int64_t* lpidx);
+/* per target leaf (target-leaf order): aggregated (source node, alpha) and
+ * exact (source node) lists as CSR */
+int rplu_plan_lists(const rplu_plan_host* h, int64_t* agg_start, int64_t* agg_node,
+                    double* agg_alpha, int64_t* ex_start, int64_t* ex_node);
+int rplu_plan_free(rplu_plan_host* h);
+
 /* exact_row_norms (cauchy.py:129-137): u_i = sum_j |G_i.B_:,j / (x_i-y_j)|^2
  * into the device array `out` (n doubles). */
 int rplu_cauchy_row_norms(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,

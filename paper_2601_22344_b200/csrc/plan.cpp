@@ -1,0 +1,264 @@
+// Host-native interaction-plan build for the certified-bound plan path
+// (reference rplu.treebounds, pkg/src/rplu/treebounds.py):
+// square-box quadtrees over the target points x and the source points y
+// (:47-104) and the dual traversal that fills each target leaf's aggregated
+// (source node, 1/d_min^2) and exact (source leaf) lists (Alg C.1,
+// build_plan :141-180).
+//
+// The plan depends only on the point sets and is built once per call on the
+// host, as in the reference; a Python loop over ~2e6 box pairs took 3.1 s at
+// C4 size (2^20 points per side).  The arithmetic is the reference's: the
+// same box corners, edge padding, quadrant order (NW, NE, SW, SE, empty
+// children skipped, depth-first with a stack), first-maximum max() and no
+// FMA contraction (built with -ffp-contract=off), so the plans are identical
+// (tests/test_treebounds_cpu.py checks them against the reference's and the
+// Python restatement).
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/rplu_b200.h"
+
+namespace rplu {
+void set_error(const std::string& msg);
+}
+
+namespace {
+
+struct Tree {
+  std::vector<double> x0, y0, size;
+  std::vector<int64_t> parent;
+  std::vector<std::vector<int64_t>> children, pts;
+  std::vector<int64_t> leaves;
+};
+
+// Python's max(): the first maximal argument wins (strict >)
+inline double pymax(double a, double b) { return b > a ? b : a; }
+inline double pymax3(double a, double b, double c) { return pymax(pymax(a, b), c); }
+
+void build_tree(const double* p, int64_t n, int64_t leaf_size, Tree& t) {
+  double ox = p[0], oy = p[1], mx = p[0], my = p[1];
+  for (int64_t i = 1; i < n; ++i) {
+    ox = std::min(ox, p[2 * i]);
+    oy = std::min(oy, p[2 * i + 1]);
+    mx = std::max(mx, p[2 * i]);
+    my = std::max(my, p[2 * i + 1]);
+  }
+  double edge = pymax3(mx - ox, my - oy, 1e-300);
+  edge *= 1.0 + 1e-12;
+  t.x0 = {ox};
+  t.y0 = {oy};
+  t.size = {edge};
+  t.parent = {-1};
+  t.children.assign(1, {});
+  t.pts.assign(1, {});
+  t.pts[0].resize(n);
+  for (int64_t i = 0; i < n; ++i) t.pts[0][i] = i;
+  std::vector<int64_t> todo = {0};
+  while (!todo.empty()) {
+    const int64_t k = todo.back();
+    todo.pop_back();
+    std::vector<int64_t>& idx = t.pts[k];
+    bool same = true;
+    const double rx = p[2 * idx[0]], ry = p[2 * idx[0] + 1];
+    if ((int64_t)idx.size() > leaf_size) {
+      for (int64_t i : idx)
+        if (!(p[2 * i] == rx && p[2 * i + 1] == ry)) { same = false; break; }
+    }
+    if ((int64_t)idx.size() <= leaf_size || same) {
+      t.leaves.push_back(k);
+      continue;
+    }
+    const double h = t.size[k] / 2.0;
+    const double cx = t.x0[k] + h, cy = t.y0[k] + h;
+    std::vector<int64_t> quad[4];  // NW, NE, SW, SE
+    for (int64_t i : idx) {
+      const bool east = p[2 * i] >= cx, north = p[2 * i + 1] >= cy;
+      quad[north ? (east ? 1 : 0) : (east ? 3 : 2)].push_back(i);
+    }
+    const double bx[4] = {t.x0[k], cx, t.x0[k], cx};
+    const double by[4] = {cy, cy, t.y0[k], t.y0[k]};
+    std::vector<int64_t> kids;
+    for (int q = 0; q < 4; ++q) {
+      if (quad[q].empty()) continue;
+      const int64_t c = (int64_t)t.x0.size();
+      t.x0.push_back(bx[q]);
+      t.y0.push_back(by[q]);
+      t.size.push_back(h);
+      t.parent.push_back(k);
+      t.children.emplace_back();
+      t.pts.push_back(std::move(quad[q]));
+      kids.push_back(c);
+      todo.push_back(c);
+    }
+    t.children[k] = kids;
+    std::vector<int64_t>().swap(t.pts[k]);
+  }
+}
+
+// (d_min^2, d_max^2) between square ia of tree a and square ib of tree b
+inline void box_dist2(const Tree& a, int64_t ia, const Tree& b, int64_t ib, double& dmin2,
+                      double& dmax2) {
+  const double ax0 = a.x0[ia], ay0 = a.y0[ia], asz = a.size[ia];
+  const double bx0 = b.x0[ib], by0 = b.y0[ib], bsz = b.size[ib];
+  const double ax1 = ax0 + asz, ay1 = ay0 + asz, bx1 = bx0 + bsz, by1 = by0 + bsz;
+  const double dx = pymax3(0.0, bx0 - ax1, ax0 - bx1);
+  const double dy = pymax3(0.0, by0 - ay1, ay0 - by1);
+  const double ex = pymax(bx1 - ax0, ax1 - bx0);
+  const double ey = pymax(by1 - ay0, ay1 - by0);
+  const double dxx = dx * dx, dyy = dy * dy, exx = ex * ex, eyy = ey * ey;
+  dmin2 = dxx + dyy;
+  dmax2 = exx + eyy;
+}
+
+}  // namespace
+
+struct rplu_plan_host {
+  Tree tgt, src;
+  std::vector<int64_t> agg_start, agg_node, ex_start, ex_node;
+  std::vector<double> agg_alpha;
+};
+
+extern "C" {
+
+int rplu_plan_build(const double* x, int64_t n, const double* y, int64_t m, double nu,
+                    int64_t leaf_size, int64_t* coincident, rplu_plan_host** out) {
+  if (!out || !x || !y || n < 1 || m < 1) {
+    rplu::set_error("rplu_plan_build: bad argument (empty point set?)");
+    return RPLU_ERR_ARG;
+  }
+  *out = nullptr;
+  if (!(nu >= 1.0)) { rplu::set_error("nu must be >= 1"); return RPLU_ERR_ARG; }
+  if (leaf_size < 1) { rplu::set_error("leaf size must be >= 1"); return RPLU_ERR_ARG; }
+  rplu_plan_host* h = new rplu_plan_host();
+  build_tree(x, n, leaf_size, h->tgt);
+  build_tree(y, m, leaf_size, h->src);
+  const Tree& tgt = h->tgt;
+  const Tree& src = h->src;
+  // target leaves below every target node (leaf order)
+  std::vector<std::vector<int64_t>> under(tgt.x0.size());
+  for (int64_t leaf : tgt.leaves)
+    for (int64_t k = leaf; k != -1; k = tgt.parent[k]) under[k].push_back(leaf);
+  std::vector<int64_t> slot(tgt.x0.size(), -1);
+  for (size_t q = 0; q < tgt.leaves.size(); ++q) slot[tgt.leaves[q]] = (int64_t)q;
+  std::vector<std::vector<std::pair<int64_t, double>>> agg(tgt.leaves.size());
+  std::vector<std::vector<int64_t>> exact(tgt.leaves.size());
+  std::vector<std::pair<int64_t, int64_t>> todo = {{0, 0}};
+  while (!todo.empty()) {
+    const auto st = todo.back();
+    todo.pop_back();
+    const int64_t s = st.first, t = st.second;
+    double dmin2, dmax2;
+    box_dist2(src, s, tgt, t, dmin2, dmax2);
+    if (dmin2 > 0.0 && dmax2 <= nu * dmin2) {
+      for (int64_t leaf : under[t]) {
+        double lmin2, lmax2;
+        box_dist2(src, s, tgt, leaf, lmin2, lmax2);
+        agg[slot[leaf]].push_back({s, 1.0 / lmin2});
+      }
+      continue;
+    }
+    const bool s_leaf = src.children[s].empty(), t_leaf = tgt.children[t].empty();
+    if (s_leaf && t_leaf) {
+      if (dmin2 == 0.0) {  // coincident target / source points (treebounds.py:183-194)
+        for (int64_t a : tgt.pts[t])
+          for (int64_t b : src.pts[s])
+            if (x[2 * a] == y[2 * b] && x[2 * a + 1] == y[2 * b + 1]) {
+              if (coincident) { coincident[0] = a; coincident[1] = b; }
+              rplu::set_error("coincident target / source points");
+              delete h;
+              return RPLU_ERR_ARG;
+            }
+      }
+      exact[slot[t]].push_back(s);
+      continue;
+    }
+    if ((tgt.size[t] >= src.size[s] && !t_leaf) || s_leaf) {
+      for (int64_t c : tgt.children[t]) todo.push_back({s, c});
+    } else {
+      for (int64_t c : src.children[s]) todo.push_back({c, t});
+    }
+  }
+  h->agg_start.push_back(0);
+  h->ex_start.push_back(0);
+  for (size_t q = 0; q < tgt.leaves.size(); ++q) {
+    for (const auto& e : agg[q]) {
+      h->agg_node.push_back(e.first);
+      h->agg_alpha.push_back(e.second);
+    }
+    h->agg_start.push_back((int64_t)h->agg_node.size());
+    h->ex_node.insert(h->ex_node.end(), exact[q].begin(), exact[q].end());
+    h->ex_start.push_back((int64_t)h->ex_node.size());
+  }
+  *out = h;
+  return RPLU_OK;
+}
+
+int rplu_plan_counts(const rplu_plan_host* h, int64_t* counts) {
+  if (!h || !counts) { rplu::set_error("rplu_plan_counts: NULL argument"); return RPLU_ERR_ARG; }
+  const Tree* tr[2] = {&h->tgt, &h->src};
+  for (int w = 0; w < 2; ++w) {
+    int64_t nc = 0;
+    for (const auto& c : tr[w]->children) nc += (int64_t)c.size();
+    counts[3 * w + 0] = (int64_t)tr[w]->x0.size();
+    counts[3 * w + 1] = (int64_t)tr[w]->leaves.size();
+    counts[3 * w + 2] = nc;
+  }
+  counts[6] = (int64_t)h->agg_node.size();
+  counts[7] = (int64_t)h->ex_node.size();
+  return RPLU_OK;
+}
+
+int rplu_plan_tree(const rplu_plan_host* h, int32_t which, double* x0, double* y0, double* size,
+                   int64_t* parent, int64_t* cstart, int64_t* cidx, int64_t* leaves,
+                   int64_t* lpstart, int64_t* lpidx) {
+  if (!h || (which != 0 && which != 1) || !x0 || !y0 || !size || !parent || !cstart || !cidx ||
+      !leaves || !lpstart || !lpidx) {
+    rplu::set_error("rplu_plan_tree: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  const Tree& t = which == 0 ? h->tgt : h->src;
+  const size_t nn = t.x0.size();
+  std::copy(t.x0.begin(), t.x0.end(), x0);
+  std::copy(t.y0.begin(), t.y0.end(), y0);
+  std::copy(t.size.begin(), t.size.end(), size);
+  std::copy(t.parent.begin(), t.parent.end(), parent);
+  int64_t c = 0;
+  for (size_t k = 0; k < nn; ++k) {
+    cstart[k] = c;
+    for (int64_t ch : t.children[k]) cidx[c++] = ch;
+  }
+  cstart[nn] = c;
+  int64_t p = 0;
+  for (size_t q = 0; q < t.leaves.size(); ++q) {
+    leaves[q] = t.leaves[q];
+    lpstart[q] = p;
+    for (int64_t i : t.pts[t.leaves[q]]) lpidx[p++] = i;
+  }
+  lpstart[t.leaves.size()] = p;
+  return RPLU_OK;
+}
+
+int rplu_plan_lists(const rplu_plan_host* h, int64_t* agg_start, int64_t* agg_node,
+                    double* agg_alpha, int64_t* ex_start, int64_t* ex_node) {
+  if (!h || !agg_start || !agg_node || !agg_alpha || !ex_start || !ex_node) {
+    rplu::set_error("rplu_plan_lists: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  std::copy(h->agg_start.begin(), h->agg_start.end(), agg_start);
+  std::copy(h->agg_node.begin(), h->agg_node.end(), agg_node);
+  std::copy(h->agg_alpha.begin(), h->agg_alpha.end(), agg_alpha);
+  std::copy(h->ex_start.begin(), h->ex_start.end(), ex_start);
+  std::copy(h->ex_node.begin(), h->ex_node.end(), ex_node);
+  return RPLU_OK;
+}
+
+int rplu_plan_free(rplu_plan_host* h) {
+  delete h;
+  return RPLU_OK;
+}
+
+}  // extern "C"
