@@ -305,6 +305,22 @@ typedef struct rplu_tree_plan {
 int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, const void* y,
                      const void* G, const void* Bt, double* u, void* stream);
 
+/* Plan-path step primitives (structured_eliminate with a plan,
+ * cauchy.py:207-277), driven by the host rejection loop:
+ *   rplu_cauchy_plan_row: pivot row r = (G_i . B)/(x_i - y) into rbuf[m]
+ *     (complex128) and |r|^2 into wbuf[m] (numpy-exact arithmetic); out3 =
+ *     {sum_j |r_j|^2, max_j |r_j|, bounds[i] (0 if bounds is NULL)} on the
+ *     host (synchronous);
+ *   rplu_cauchy_plan_update: with a = rbuf[j], G -= (c/a) G_i and
+ *     B_:,l -= B_:,j (r_l/a) in place (c = column j); optional Cout[n] = c
+ *     and Rout[m] = r (kept steps).  Asynchronous on `stream`. */
+int rplu_cauchy_plan_row(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                         const void* y, void* G, void* Bt, int64_t i, void* rbuf, double* wbuf,
+                         const double* bounds, double* out3, void* stream);
+int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                            const void* y, void* G, void* Bt, int64_t i, int64_t j,
+                            const void* rbuf, void* Cout, void* Rout, void* stream);
+
 /* Host-native interaction-plan build (no GPU needed), replacing the Python
  * quadtrees and dual traversal of rplu.treebounds.build_plan
  * (treebounds.py:47-104, :141-180) with identical results.  x: n complex

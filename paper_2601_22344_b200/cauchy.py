@@ -307,11 +307,30 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
         tr.near_boundary_draws += int(near)
         return i
     u0_max = None
-    steps_dev = []
+    p = cur.displacement_rank
+    dev = cur.device
+    c = _device.ctx(dev)
+    stream_h = _device.stream_handle(dev)
+    rbuf = torch.empty(m, dtype=torch.complex128, device=dev)
+    wbuf = torch.empty(m, dtype=torch.float64, device=dev)
+    C = torch.empty((rank, n), dtype=torch.complex128, device=dev) if keep_steps else None
+    R = torch.empty((rank, m), dtype=torch.complex128, device=dev) if keep_steps else None
+    A_steps = []
+    out3 = np.zeros(3)
+    last_rmax = [0.0]
+
+    def row(i, u):
+        """pivot row i into rbuf / wbuf; returns (||r||^2, max|r|, u_i)"""
+        _ffi.check(c._lib.rplu_cauchy_plan_row(
+            c.handle, p, n, m, cur.x.data_ptr(), cur.y.data_ptr(), cur.G.data_ptr(),
+            cur.Bt.data_ptr(), int(i), rbuf.data_ptr(), wbuf.data_ptr(),
+            u.data_ptr() if u is not None else None, out3.ctypes.data, stream_h))
+        last_rmax[0] = float(out3[1])
+        return float(out3[0]), float(out3[1]), float(out3[2])
     try:
         for _ in range(rank):
             u = tree_bounds_device(plan, cur)
-            umax, usum = float(u.max()), float(u.sum())
+            umax, usum = torch.stack([u.max(), u.sum()]).tolist()   # one host sync
             tr.bound_maxes.append(umax)
             tr.bound_sums.append(usum)
             u0_max = umax if u0_max is None else u0_max
@@ -323,20 +342,18 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
                 break
             if rule == "c2plu":
                 i = int(torch.argmax(u))
-                r = _row_dev(cur, i)
+                row(i, None)
             else:
-                i = r = None
+                i = None
                 for _p in range(cap):
                     ii = sample_index(u, stream.next())
-                    rr = _row_dev(cur, ii)
-                    rho = float((rr.real ** 2 + rr.imag ** 2).sum())
+                    rho, _, ui = row(ii, u)
                     tr.proposals += 1
-                    ui = float(u[ii])
                     if abs(rho - ui) <= 1e-12 * ui:
                         tr.near_tie_acceptances += 1
                     if rho >= ui or stream.next() <= rho / ui:
                         tr.acceptances += 1
-                        i, r = ii, rr
+                        i = ii
                         break
                 if i is None:
                     tr.exact_fallbacks += 1
@@ -344,41 +361,44 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
                                   "used exact row norms (possible bound violation)",
                                   stacklevel=3)
                     i = sample_index(exact_row_norms_device(cur), stream.next())
-                    r = _row_dev(cur, i)
-            ra = r.abs()
+                    row(i, None)
+            rmax = last_rmax[0]
             if rule == "c2plu":
-                j = int(torch.argmax(ra))
+                j = int(torch.argmax(wbuf))
             else:
-                j = sample_index(ra ** 2, stream.next())
-            thr = PIVOT_REL_TOL * float(ra.max())
-            a = r[j]
-            if float(a.abs()) <= thr:
+                j = sample_index(wbuf, stream.next())
+            thr = PIVOT_REL_TOL * rmax
+            a = complex(rbuf[j].item())
+            if abs(a) <= thr:
                 if rule == "c2plu":
                     raise ZeroDivisionError(f"pivot ({i}, {j}) is numerically zero")
-                j = sample_index(ra ** 2, stream.next())
-                a = r[j]
-                if float(a.abs()) <= thr:
+                j = sample_index(wbuf, stream.next())
+                a = complex(rbuf[j].item())
+                if abs(a) <= thr:
                     raise ZeroDivisionError(
                         f"pivot ({i}, {j}) is numerically zero after resampling")
-            c = _column_dev(cur, j)
-            gi, bj = cur.G[i].clone(), cur.Bt[j].clone()
-            cur.G -= torch.outer(c / a, gi)
-            cur.Bt -= torch.outer(r / a, bj)
+            t = len(tr.row_indices)
+            cbuf = C[t] if keep_steps else None
+            rout = R[t] if keep_steps else None
+            _ffi.check(c._lib.rplu_cauchy_plan_update(
+                c.handle, p, n, m, cur.x.data_ptr(), cur.y.data_ptr(), cur.G.data_ptr(),
+                cur.Bt.data_ptr(), int(i), int(j), rbuf.data_ptr(),
+                cbuf.data_ptr() if cbuf is not None else None,
+                rout.data_ptr() if rout is not None else None, stream_h))
             tr.row_indices.append(int(i))
             tr.col_indices.append(int(j))
             if keep_steps:
-                steps_dev.append((c, r, a))
+                A_steps.append(a)
     finally:
         stream.commit()
     tr.uniforms_consumed = stream.used
-    if keep_steps and steps_dev:
-        C = torch.stack([s[0] for s in steps_dev])
-        R = torch.stack([s[1] for s in steps_dev])
-        A = torch.stack([s[2] for s in steps_dev])
-        tr.steps_device = (C, R, A)
+    k = len(tr.row_indices)
+    if keep_steps and k:
+        A = torch.tensor(A_steps, dtype=torch.complex128, device=dev)
+        tr.steps_device = (C[:k], R[:k], A)
         if host_steps:
-            Ch, Rh, Ah = _device.to_numpy(C), _device.to_numpy(R), A.cpu().numpy()
-            tr.steps = [(Ch[t], Rh[t], complex(Ah[t])) for t in range(len(steps_dev))]
+            Ch, Rh = _device.to_numpy(C[:k]), _device.to_numpy(R[:k])
+            tr.steps = [(Ch[t], Rh[t], A_steps[t]) for t in range(k)]
     return tr
 
 

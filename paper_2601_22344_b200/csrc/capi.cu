@@ -120,6 +120,13 @@ int bary_eval_impl(const void* z, long long nz, const void* t, const void* f, co
 int mgs_arnoldi_impl(rplu_ctx* ctx, const void* V, long long n, int j, void* w, void* vnext,
                      void* h, cudaStream_t s);
 
+int cauchy_plan_row_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                         const void* y, void* G, void* Bt, long long i, void* rbuf, double* wbuf,
+                         const double* bounds, double* host3, cudaStream_t s);
+int cauchy_plan_update_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                            const void* y, void* G, void* Bt, long long i, long long j, void* rbuf,
+                            void* Cout, void* Rout, cudaStream_t s);
+
 static int gauss_check(const rplu_gauss_op* op) {
   if (!op || op->n < 1 || op->m < 1 || !op->P || !op->Q || !(op->h > 0.0)) {
     set_error("invalid Gaussian-kernel operator");
@@ -776,6 +783,34 @@ int rplu_tree_bounds(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, c
   DeviceGuard g(ctx->device);
   if (g.rc) return g.rc;
   return tree_bounds_impl(ctx, plan, x, y, G, Bt, u, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_cauchy_plan_row(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                         const void* y, void* G, void* Bt, int64_t i, void* rbuf, double* wbuf,
+                         const double* bounds, double* out3, void* stream) {
+  if (!ctx || p < 1 || p > 8 || n < 1 || m < 1 || !x || !y || !G || !Bt || !rbuf || !wbuf ||
+      !out3 || i < 0 || i >= n) {
+    set_error("rplu_cauchy_plan_row: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_plan_row_impl(ctx, p, n, m, x, y, G, Bt, i, rbuf, wbuf, bounds, out3,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                            const void* y, void* G, void* Bt, int64_t i, int64_t j,
+                            const void* rbuf, void* Cout, void* Rout, void* stream) {
+  if (!ctx || p < 1 || p > 8 || n < 1 || m < 1 || !x || !y || !G || !Bt || !rbuf || i < 0 ||
+      i >= n || j < 0 || j >= m) {
+    set_error("rplu_cauchy_plan_update: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_plan_update_impl(ctx, p, n, m, x, y, G, Bt, i, j, const_cast<void*>(rbuf), Cout,
+                                 Rout, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {

@@ -18,6 +18,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <string.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -556,6 +558,109 @@ static void launch_mass(CauchyParams& q, cudaStream_t s) {
   }
 
 static int rows_per_cta(int p) { return 256 * ((p <= 4) ? 2 : 1); }
+
+// ---------------------------------------------------------------------------
+// Plan-path step primitives (structured_eliminate with certified bounds,
+// cauchy.py:207-277): the proposal's pivot row and the generator update run
+// in the exact-norm loop's K6 kernels (numpy-exact Smith division and
+// complex products), driven by the host rejection loop.
+
+// st <- (pi, pj, Smith coefficients of a = r_j), snapshot G_i, B_j
+__global__ void cauchy_plan_pivot_kernel(CauchyParams q, long long i, long long j,
+                                         double2* gsnap) {
+  DevState* st = q.st;
+  if (threadIdx.x == 0) {
+    st->active = 1;
+    st->status = kRunning;
+    st->pi = i;
+    st->pj = j;
+    const double2 a = q.rbuf[j];
+    st->a_re = a.x;
+    st->a_im = a.y;
+    const CDivCoef cf = cdiv_coef(a);
+    st->rat = cf.rat;
+    st->scl = cf.scl;
+    st->branch = cf.branch;
+  }
+  const int l = threadIdx.x;
+  if (l < q.p) {
+    gsnap[l] = q.G[i * q.p + l];
+    gsnap[q.p + l] = q.Bt[j * q.p + l];
+  }
+}
+
+__global__ void cauchy_plan_init_kernel(DevState* st, long long i, unsigned long long* rmax_bits) {
+  st->active = 1;
+  st->status = kRunning;
+  st->pi = i;
+  *rmax_bits = 0ull;
+}
+
+static int plan_params(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                       const void* y, void* G, void* Bt, void* rbuf, double* wbuf,
+                       CauchyParams& q, double2*& gsnap) {
+  q = CauchyParams{};
+  q.n = n;
+  q.m = m;
+  q.p = p;
+  q.x = reinterpret_cast<const double2*>(x);
+  q.y = reinterpret_cast<const double2*>(y);
+  q.G = reinterpret_cast<double2*>(G);
+  q.Bt = reinterpret_cast<double2*>(Bt);
+  q.rbuf = reinterpret_cast<double2*>(rbuf);
+  q.wbuf = wbuf;
+  int rc;
+  if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
+  q.st = reinterpret_cast<DevState*>(ctx->state.ptr);
+  if ((rc = ctx->csync.ensure(256))) return rc;
+  q.rmax_bits = reinterpret_cast<unsigned long long*>(ctx->csync.ptr);
+  gsnap = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctx->csync.ptr) + 16);
+  return RPLU_OK;
+}
+
+int cauchy_plan_row_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                         const void* y, void* G, void* Bt, long long i, void* rbuf, double* wbuf,
+                         const double* bounds, double* host3, cudaStream_t s) {
+  CauchyParams q;
+  double2* gsnap;
+  int rc;
+  if ((rc = plan_params(ctx, p, n, m, x, y, G, Bt, rbuf, wbuf, q, gsnap))) return rc;
+  cauchy_plan_init_kernel<<<1, 1, 0, s>>>(q.st, i, q.rmax_bits);
+  const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
+  count_launches(2);
+  RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, s>>>(q)));
+  RPLU_CUDA(cudaGetLastError());
+  unsigned long long rbits = 0;
+  double bi = 0.0;
+  RPLU_CUDA(cudaMemcpyAsync(&rbits, q.rmax_bits, sizeof(rbits), cudaMemcpyDeviceToHost, s));
+  if (bounds) RPLU_CUDA(cudaMemcpyAsync(&bi, bounds + i, sizeof(double), cudaMemcpyDeviceToHost, s));
+  double rho = 0.0;  // sum of |r_j|^2 in the draw code's (deterministic) order
+  if ((rc = sample_index_impl(ctx, wbuf, m, 0.0, 2, nullptr, nullptr, &rho, s))) return rc;
+  host3[0] = rho;
+  double rmax = 0.0;
+  memcpy(&rmax, &rbits, sizeof(rmax));
+  host3[1] = rmax;
+  host3[2] = bi;
+  return RPLU_OK;
+}
+
+int cauchy_plan_update_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                            const void* y, void* G, void* Bt, long long i, long long j, void* rbuf,
+                            void* Cout, void* Rout, cudaStream_t s) {
+  CauchyParams q;
+  double2* gsnap;
+  int rc;
+  if ((rc = plan_params(ctx, p, n, m, x, y, G, Bt, rbuf, nullptr, q, gsnap))) return rc;
+  q.Cout = reinterpret_cast<double2*>(Cout);
+  q.Rout = reinterpret_cast<double2*>(Rout);
+  q.t = 0;
+  const int upd_blocks = (int)std::min<long long>((n + m + 255) / 256, 8LL * ctx->sm_count);
+  count_launches(2);
+  cauchy_plan_pivot_kernel<<<1, 32, 0, s>>>(q, i, j, gsnap);
+  RPLU_P_SWITCH(p, (cauchy_update_kernel<PP><<<upd_blocks, 256, 0, s>>>(q, gsnap)));
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
 
 int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x, const void* y,
                       const void* G, const void* Bt, double* out, cudaStream_t s) {

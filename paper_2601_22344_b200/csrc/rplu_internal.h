@@ -108,6 +108,10 @@ void set_error(const std::string& msg);
 // (Gaussian-kernel, sample-index, consumer kernels) for bench.py's
 // gpu_launches claim; the pivot-loop drivers report theirs in *_out.
 void count_launches(long long k);
+
+// standalone draw (dense.cu): mode 0 u*total, 1 absolute target, 2 total only
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
+                      long long* idx, int* near, double* total, cudaStream_t s);
 int cuda_fail(cudaError_t e, const char* where);
 
 #define RPLU_CUDA(call)                                        \
