@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "rplu_common.cuh"
 #include "rplu_internal.h"
 
@@ -42,24 +44,49 @@ __device__ __forceinline__ double2 cfma_conj(double2 acc, double2 a, double2 b) 
   return acc;
 }
 
+// Leaf Grams: one warp per source leaf.  For p^2 <= 16 the warp splits into
+// 32 / p^2 groups of p^2 lanes (one entry per lane); group g sums the leaf's
+// points g, g + NG, ... and the group sums are added in group order through
+// shuffles (deterministic), so every lane is busy and NG point loads are in
+// flight per iteration.
 template <int P>
 __global__ void tree_gram_leaf_kernel(TreeParams q) {
   const long long leaf = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (leaf >= q.n_sleaves) return;
-  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-  for (long long k = q.sstart[leaf]; k < q.sstart[leaf + 1]; ++k) {
-    const long long j = q.spts[k];
+  constexpr int E = P * P;
+  const long long k0 = q.sstart[leaf], k1 = q.sstart[leaf + 1];
+  if constexpr (E <= 16) {
+    constexpr int NG = 32 / E;
+    const int e = lane % E, g = lane / E;
+    double2 acc = make_double2(0, 0);
+    if (g < NG)
+      for (long long k = k0 + g; k < k1; k += NG) {
+        const long long j = q.spts[k];
+        acc = cfma_conj(acc, q.Bt[j * P + e / P], q.Bt[j * P + e % P]);
+      }
+#pragma unroll
+    for (int h = 1; h < NG; ++h) {
+      const double ax = __shfl_sync(0xffffffffu, acc.x, e + E * h);
+      const double ay = __shfl_sync(0xffffffffu, acc.y, e + E * h);
+      if (g == 0) { acc.x += ax; acc.y += ay; }
+    }
+    if (g == 0) q.Hnode[q.leaf_node[leaf] * E + e] = acc;
+  } else {
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for (long long k = k0; k < k1; ++k) {
+      const long long j = q.spts[k];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        if (e < E) acc[h] = cfma_conj(acc[h], q.Bt[j * P + e / P], q.Bt[j * P + e % P]);
+      }
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = lane + 32 * h;
-      if (e < P * P) acc[h] = cfma_conj(acc[h], q.Bt[j * P + e / P], q.Bt[j * P + e % P]);
+      if (e < E) q.Hnode[q.leaf_node[leaf] * E + e] = acc[h];
     }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int e = lane + 32 * h;
-    if (e < P * P) q.Hnode[q.leaf_node[leaf] * P * P + e] = acc[h];
   }
 }
 
@@ -89,6 +116,41 @@ __global__ void __launch_bounds__(256) tree_gram_level_kernel(TreeParams q,
   }
 }
 
+// All internal levels in one cooperative launch: warps stride over the
+// level's nodes, one grid barrier between levels (the per-level launches
+// cost ~15 x 5 us at C4 size).
+constexpr int kMaxLevels = 62;
+struct LevelTable {
+  long long start[kMaxLevels + 1];
+  int n;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) tree_gram_levels_kernel(TreeParams q,
+                                                               const long long* __restrict__ nodes,
+                                                               LevelTable lt, unsigned* bar) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * 8;
+  unsigned nb = 0;
+  for (int l = 0; l < lt.n; ++l) {
+    for (long long w = lt.start[l] + w0; w < lt.start[l + 1]; w += nw) {
+      const long long node = nodes[w];
+      const long long c0 = q.cstart[node], c1 = q.cstart[node + 1];
+      for (int e = lane; e < P * P; e += 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (long long c = c0; c < c1; ++c) {
+          const double2 v = __ldcg(q.Hnode + q.cidx[c] * P * P + e);  // written this launch
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        q.Hnode[node * P * P + e] = acc;
+      }
+    }
+    if (l + 1 < lt.n) grid_barrier(bar, gridDim.x * (++nb));
+  }
+}
+
 // One warp per target leaf.  The aggregated part is linear in the Grams, so
 // the warp first folds the leaf's interaction list into one p x p matrix
 // M = sum_(s,alpha) alpha H_s in shared memory (lanes over the p^2 entries;
@@ -105,16 +167,40 @@ __global__ void __launch_bounds__(32 * kTreeWarps) tree_bounds_kernel(TreeParams
   if (leaf >= q.n_tleaves) return;  // warp-uniform
   const long long a0 = q.agg_start[leaf], a1 = q.agg_start[leaf + 1];
   const long long e0 = q.ex_start[leaf], e1 = q.ex_start[leaf + 1];
-  for (int c = lane; c < P * P; c += 32) {
+  constexpr int E = P * P;
+  if constexpr (E <= 16) {
+    // 32 / E lane groups split the interaction list (more loads in flight),
+    // group sums added in group order (deterministic)
+    constexpr int NG = 32 / E;
+    const int c = lane % E, g = lane / E;
     double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (long long e = a0; e < a1; ++e) {
-      const double al = q.agg_alpha[e];
-      const double2 v = q.Hnode[q.agg_node[e] * P * P + c];
-      acc.x = fma(al, v.x, acc.x);
-      acc.y = fma(al, v.y, acc.y);
+    if (g < NG)
+#pragma unroll 2
+      for (long long e = a0 + g; e < a1; e += NG) {
+        const double al = __ldg(q.agg_alpha + e);
+        const double2 v = q.Hnode[__ldg(q.agg_node + e) * E + c];
+        acc.x = fma(al, v.x, acc.x);
+        acc.y = fma(al, v.y, acc.y);
+      }
+#pragma unroll
+    for (int h = 1; h < NG; ++h) {
+      const double ax = __shfl_sync(0xffffffffu, acc.x, c + E * h);
+      const double ay = __shfl_sync(0xffffffffu, acc.y, c + E * h);
+      if (g == 0) { acc.x += ax; acc.y += ay; }
     }
-    Ms[wid][c] = acc;
+    if (g == 0) Ms[wid][c] = acc;
+  } else {
+    for (int c = lane; c < E; c += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+      for (long long e = a0; e < a1; ++e) {
+        const double al = q.agg_alpha[e];
+        const double2 v = q.Hnode[q.agg_node[e] * E + c];
+        acc.x = fma(al, v.x, acc.x);
+        acc.y = fma(al, v.y, acc.y);
+      }
+      Ms[wid][c] = acc;
+    }
   }
   __syncwarp();
   const double2* M = Ms[wid];
@@ -200,7 +286,25 @@ int tree_bounds_impl(rplu_ctx* ctx, const rplu_tree_plan* plan, const void* x, c
   const unsigned gl = (unsigned)((q.n_sleaves + 7) / 8);
   RPLU_TREE_P_SWITCH(q.p, (tree_gram_leaf_kernel<PP><<<gl, 256, 0, s>>>(q)));
   const long long* lvl_nodes = reinterpret_cast<const long long*>(plan->lvl_nodes);
-  for (int l = 0; l < plan->n_levels; ++l) {
+  if (plan->n_levels > 0 && plan->n_levels <= kMaxLevels) {
+    LevelTable lt;
+    lt.n = plan->n_levels;
+    for (int l = 0; l <= lt.n; ++l) lt.start[l] = plan->lvl_start[l];
+    if ((rc = ctx->gbar.ensure(64))) return rc;
+    unsigned* bar = reinterpret_cast<unsigned*>(ctx->gbar.ptr);
+    RPLU_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), s));
+    int per_sm = 1;
+    RPLU_TREE_P_SWITCH(q.p, (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                &per_sm, tree_gram_levels_kernel<PP>, 256, 0)));
+    per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+    long long most = 0;
+    for (int l = 0; l < lt.n; ++l) most = std::max(most, lt.start[l + 1] - lt.start[l]);
+    int grid = (int)std::min<long long>((most + 7) / 8, (long long)ctx->sm_count * per_sm);
+    grid = grid < 1 ? 1 : grid;
+    void* args[] = {&q, &lvl_nodes, &lt, &bar};
+    RPLU_TREE_P_SWITCH(q.p, (cudaLaunchCooperativeKernel((const void*)tree_gram_levels_kernel<PP>,
+                                                         dim3(grid), dim3(256), args, 0, s)));
+  } else for (int l = 0; l < plan->n_levels; ++l) {
     const long long b0 = plan->lvl_start[l], cnt = plan->lvl_start[l + 1] - b0;
     if (cnt <= 0) continue;
     const unsigned gb = (unsigned)((cnt + 7) / 8);
