@@ -531,12 +531,25 @@ static bool mass_tlp(long long n, long long m) {
   return (double)n * (double)m <= 268435456.0;  // 2^28 entries
 }
 
+// threads (= rows) per CTA of the TLP shape (RPLU_CAUCHY_TLP_NT: 512 / 768 / 1024)
+static int tlp_nt() {
+  static const int v = [] {
+    const char* e = getenv("RPLU_CAUCHY_TLP_NT");
+    const int x = e ? atoi(e) : 512;
+    return (x == 768 || x == 1024) ? x : 512;
+  }();
+  return v;
+}
+
 template <int P>
 static void launch_mass(CauchyParams& q, cudaStream_t s) {
   constexpr int TJ = 128;
   if (P <= 4 && mass_tlp(q.n, q.m)) {
-    dim3 grid((unsigned)((q.n + 511) / 512), (unsigned)q.splits);
-    cauchy_mass_kernel<P, 1, TJ, 512><<<grid, 512, 0, s>>>(q);
+    const int nt = tlp_nt();
+    dim3 grid((unsigned)((q.n + nt - 1) / nt), (unsigned)q.splits);
+    if (nt == 1024) cauchy_mass_kernel<P, 1, TJ, 1024><<<grid, 1024, 0, s>>>(q);
+    else if (nt == 768) cauchy_mass_kernel<P, 1, TJ, 768><<<grid, 768, 0, s>>>(q);
+    else cauchy_mass_kernel<P, 1, TJ, 512><<<grid, 512, 0, s>>>(q);
     return;
   }
   constexpr int RPT = (P <= 4) ? 2 : 1;
@@ -557,7 +570,10 @@ static void launch_mass(CauchyParams& q, cudaStream_t s) {
     default: break;                 \
   }
 
-static int rows_per_cta(int p) { return 256 * ((p <= 4) ? 2 : 1); }
+static int rows_per_cta(int p, long long n, long long m) {
+  if (p <= 4 && mass_tlp(n, m)) return tlp_nt();
+  return 256 * ((p <= 4) ? 2 : 1);
+}
 
 // ---------------------------------------------------------------------------
 // Plan-path step primitives (structured_eliminate with certified bounds,
@@ -672,7 +688,7 @@ int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void
   q.y = reinterpret_cast<const double2*>(y);
   q.G = reinterpret_cast<double2*>(const_cast<void*>(G));
   q.Bt = reinterpret_cast<double2*>(const_cast<void*>(Bt));
-  q.splits = choose_splits(n, m, rows_per_cta(p), ctx->sm_count);
+  q.splits = choose_splits(n, m, rows_per_cta(p, n, m), ctx->sm_count);
   int rc;
   if ((rc = ctx->scratch[0].ensure(sizeof(double) * (size_t)q.splits * n))) return rc;
   q.partial = reinterpret_cast<double*>(ctx->scratch[0].ptr);
@@ -709,7 +725,7 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   q.y = reinterpret_cast<const double2*>(a->y);
   q.G = reinterpret_cast<double2*>(a->G);
   q.Bt = reinterpret_cast<double2*>(a->Bt);
-  q.splits = choose_splits(n, m, rows_per_cta(p), ctx->sm_count);
+  q.splits = choose_splits(n, m, rows_per_cta(p, n, m), ctx->sm_count);
   q.stop_tol = a->stop_tol;
   q.rule = a->rule;
   if ((rc = ctx->scratch[0].ensure(sizeof(double) * (size_t)q.splits * n))) return rc;
@@ -738,7 +754,7 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   q.n_uniforms = nu;
   // fused per-step bookkeeping: split sums in K5, row max in K6a, snapshot
   // in the column select (no sum / snapshot launches)
-  const long long mass_blocks = (n + rows_per_cta(p) - 1) / rows_per_cta(p);
+  const long long mass_blocks = (n + rows_per_cta(p, n, m) - 1) / rows_per_cta(p, n, m);
   const size_t sync_bytes = sizeof(unsigned long long) * (size_t)(mass_blocks + 1);
   if ((rc = ctx->csync.ensure(sync_bytes))) return rc;
   q.rmax_bits = reinterpret_cast<unsigned long long*>(ctx->csync.ptr);
@@ -995,7 +1011,7 @@ int cauchy_shard_setup(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, CauchySha
   q.y = reinterpret_cast<const double2*>(a->y);
   q.G = reinterpret_cast<double2*>(a->G);
   q.Bt = reinterpret_cast<double2*>(a->Bt);
-  q.splits = n > 0 ? choose_splits(n, m, rows_per_cta(a->p), ctx->sm_count) : 1;
+  q.splits = n > 0 ? choose_splits(n, m, rows_per_cta(a->p, n, m), ctx->sm_count) : 1;
   q.stop_tol = a->stop_tol;
   q.rule = a->rule;
   int rc;
