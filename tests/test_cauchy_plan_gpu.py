@@ -76,3 +76,49 @@ def test_plan_bounds_certify_after_updates(cuda_device):
     assert np.all(u[live] >= exact[live] * (1 - 1e-10))
     assert np.all(u[live] <= 5.0 * exact[live] * (1 + 1e-10))
     assert tr.acceptances == len(tr.row_indices)
+
+
+def test_plan_step_primitives_match_generator_formulas(cuda_device):
+    """rplu_cauchy_plan_row / rplu_cauchy_plan_update (the plan path's fused
+    K6 kernels) against the reference's row / column / generator-update
+    formulas (cauchy.py:82-86, :247-250) evaluated in numpy."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_22344_b200 import _device, _ffi
+    x, y, G, B = gen.c4_cauchy_like(7, n=300, m=260, p=3)
+    M = rp.CauchyLikeMatrix(x, y, G, B)
+    n, m, p = 300, 260, 3
+    dev = M.device
+    c = _device.ctx(dev)
+    st = _device.stream_handle(dev)
+    rbuf = torch.empty(m, dtype=torch.complex128, device=dev)
+    wbuf = torch.empty(m, dtype=torch.float64, device=dev)
+    u = torch.rand(n, dtype=torch.float64, device=dev)
+    out3 = np.zeros(3)
+    i, j = 17, 41
+    _ffi.check(c._lib.rplu_cauchy_plan_row(c.handle, p, n, m, M.x.data_ptr(), M.y.data_ptr(),
+                                           M.G.data_ptr(), M.Bt.data_ptr(), i, rbuf.data_ptr(),
+                                           wbuf.data_ptr(), u.data_ptr(), out3.ctypes.data, st))
+    r = (G[i, :] @ B) / (x[i] - y)
+    np.testing.assert_allclose(rbuf.cpu().numpy(), r, rtol=1e-13)
+    np.testing.assert_allclose(wbuf.cpu().numpy(), np.abs(r) ** 2, rtol=1e-13)
+    assert abs(out3[0] - np.sum(np.abs(r) ** 2)) <= 1e-13 * out3[0]
+    assert out3[1] == np.max(np.abs(r)) and out3[2] == float(u[i])
+    C = torch.empty(n, dtype=torch.complex128, device=dev)
+    R = torch.empty(m, dtype=torch.complex128, device=dev)
+    _ffi.check(c._lib.rplu_cauchy_plan_update(c.handle, p, n, m, M.x.data_ptr(), M.y.data_ptr(),
+                                              M.G.data_ptr(), M.Bt.data_ptr(), i, j,
+                                              rbuf.data_ptr(), C.data_ptr(), R.data_ptr(), st))
+    a = r[j]
+    col = (G @ B[:, j]) / (x - y[j])
+    G1 = G - np.outer(col / a, G[i, :])
+    B1 = B - np.outer(B[:, j], r / a)
+    np.testing.assert_allclose(C.cpu().numpy(), col, rtol=1e-13)
+    np.testing.assert_allclose(R.cpu().numpy(), r, rtol=1e-13)
+    np.testing.assert_allclose(M.G.cpu().numpy(), G1, rtol=1e-12, atol=1e-14 * np.abs(G1).max())
+    np.testing.assert_allclose(M.B.cpu().numpy(), B1, rtol=1e-12, atol=1e-14 * np.abs(B1).max())
+    # after the update, row i and column j of the residual are (numerically) zero
+    Mn = rp.CauchyLikeMatrix(x, y, M.G.cpu().numpy(), M.B.cpu().numpy(), check_points=False)
+    assert np.abs(Mn.row(i)).max() <= 1e-12 * np.abs(r).max()

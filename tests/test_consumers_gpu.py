@@ -264,3 +264,25 @@ def test_precond_errors(cuda_device):
     fact2, _ = rp.cur_build(rp.DenseMatrix(A2), "rplu-cur", 1, rng=rp.RngState(0))
     with pytest.raises(np.linalg.LinAlgError):
         rp.smw_build(lambda v: -v, rp.DenseMatrix(A2), fact2)
+
+
+def test_gmres_x0_and_restart_edge_cases(cuda_device):
+    """x0 start, restart = 1, and a singular system that stagnates, each
+    against the pinned oracle's MGS-GMRES."""
+    g = np.random.default_rng(11)
+    n = 120
+    K = np.eye(n) * 3 + g.standard_normal((n, n)) * 0.05
+    b = g.standard_normal(n) + 1j * g.standard_normal(n)
+    x0 = g.standard_normal(n) + 0j
+    res = rp.gmres(K, b, restart=7, tol=1e-11, x0=x0)
+    Kf = lambda v: K @ v  # noqa: E731
+    assert res.converged
+    np.testing.assert_allclose(K @ res.x, b, rtol=0, atol=1e-9 * np.linalg.norm(b))
+    r1 = rp.gmres(Kf, b, restart=1, tol=1e-8, max_restarts=500)
+    o1 = oracle.consumers.gmres_mgs(Kf, b, restart=1, tol=1e-8, max_restarts=500)
+    assert (r1.iterations, r1.converged) == (o1[2], o1[3])
+    np.testing.assert_allclose(r1.residuals, o1[1], rtol=1e-6)
+    S = np.diag(np.r_[np.ones(n - 1), 0.0])          # singular: b has a null-space part
+    with pytest.warns(UserWarning):
+        rs = rp.gmres(S, np.ones(n), restart=5, tol=1e-12, max_restarts=20)
+    assert rs.stagnated and not rs.converged
