@@ -194,11 +194,7 @@ __global__ void sum_partials_kernel(const double* partial, int splits, long long
 // ---------------------------------------------------------------------------
 // K2a: row selection + stop rules (block-uniform result: the row, or -1
 // when the loop stops here).
-// uc_pre >= 0: the caller prefetched st->ucount and the step's first uniform
-// (loads issued before the CDF build instead of after it)
-__device__ __forceinline__ long long cauchy_select_row_dev(const CauchyParams& q,
-                                                         long long uc_pre = -1,
-                                                         double u1_pre = 0.0) {
+__device__ __forceinline__ long long cauchy_select_row_dev(const CauchyParams& q) {
   constexpr int B = 1024;
   DevState* st = q.st;
   __shared__ CdfSmem<B> sm;
@@ -236,13 +232,13 @@ __device__ __forceinline__ long long cauchy_select_row_dev(const CauchyParams& q
   __syncthreads();
   if (s_stop) return -1;
   long long i;
-  long long uc = uc_pre >= 0 ? uc_pre : st->ucount;
+  long long uc = st->ucount;
   if (q.rule == RPLU_RULE_RPLU) {
     if (uc + 1 > q.n_uniforms) {
       if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
       return -1;
     }
-    const double u1 = uc_pre >= 0 ? u1_pre : q.uniforms[uc];
+    const double u1 = q.uniforms[uc];
     i = cdf_find<B>(wrow, n, cr, u1, sm);
     if (threadIdx.x == 0) {
       const double tol = kNearBoundaryRel * cr.total, tg = u1 * cr.total;
@@ -265,8 +261,7 @@ __global__ void __launch_bounds__(1024) cauchy_select_row_kernel(CauchyParams q)
 // K6a: pivot row r_j = (G_i . B_j) / (x_i - y_j) for all j, weights |r_j|^2.
 // numpy order: matmul then complex division (Smith).
 template <int P>
-__device__ __forceinline__ void cauchy_row_dev(const CauchyParams& q, long long j0, long long js,
-                                               long long pi_pre = -1) {
+__device__ __forceinline__ void cauchy_row_dev(const CauchyParams& q, long long j0, long long js) {
   double2 gi[P];
   double2 xi;
   if (q.psrc) {
@@ -275,7 +270,7 @@ __device__ __forceinline__ void cauchy_row_dev(const CauchyParams& q, long long 
     xi = q.psrc[1];
     if (blockIdx.x == 0 && threadIdx.x == 0) q.st->pi = (long long)q.psrc[0].x;
   } else {
-    const long long i = pi_pre >= 0 ? pi_pre : q.st->pi;
+    const long long i = q.st->pi;
 #pragma unroll
     for (int l = 0; l < P; ++l) gi[l] = q.G[i * P + l];
     xi = q.x[i];
@@ -315,11 +310,7 @@ __global__ void cauchy_row_kernel(CauchyParams q) {
 // ---------------------------------------------------------------------------
 // K2b: column selection with the relative zero-pivot guard; captures G_i and
 // B_j (pre-update) and 1/a coefficients into the state for the update.
-// uc_pre >= 0: prefetched stream position and the two possible column
-// uniforms (draw, one resample)
-__device__ __forceinline__ void cauchy_select_col_dev(const CauchyParams& q,
-                                                      long long uc_pre = -1,
-                                                      double u2a = 0.0, double u2b = 0.0) {
+__device__ __forceinline__ void cauchy_select_col_dev(const CauchyParams& q) {
   constexpr int B = 1024;
   DevState* st = q.st;
   __shared__ CdfSmem<B> sm;
@@ -344,8 +335,7 @@ __device__ __forceinline__ void cauchy_select_col_dev(const CauchyParams& q,
   }
   const double thr = kPivotRelTol * rmax;
   long long j;
-  long long uc = uc_pre >= 0 ? uc_pre : st->ucount;
-  const long long uc_first = uc;
+  long long uc = st->ucount;
   long long near = 0;
   if (q.rule == RPLU_RULE_RPLU) {
     Cdf<B> cc = cdf_build<B>(wcol, m, sm);
@@ -355,7 +345,7 @@ __device__ __forceinline__ void cauchy_select_col_dev(const CauchyParams& q,
         if (threadIdx.x == 0) { st->status = kUniformsExhausted; st->active = 0; }
         return;
       }
-      const double u2 = uc_pre < 0 ? q.uniforms[uc] : (uc == uc_first ? u2a : u2b);
+      const double u2 = q.uniforms[uc];
       uc += 1;
       j = cdf_find<B>(wcol, m, cc, u2, sm);
       if (threadIdx.x == 0) {
@@ -429,18 +419,11 @@ __global__ void __launch_bounds__(1024) cauchy_select_col_kernel(CauchyParams q)
 template <int P>
 __global__ void __launch_bounds__(1024) cauchy_select_kernel(CauchyParams q) {
   if (!q.st->active) return;
-  // prefetch the stream position and the row uniform (hidden behind the CDF)
-  const long long uc0 = q.st->ucount;
-  const bool rnd = q.rule == RPLU_RULE_RPLU;
-  const double u1 = (rnd && uc0 < q.n_uniforms) ? q.uniforms[uc0] : 0.0;
-  const double u2a = (rnd && uc0 + 1 < q.n_uniforms) ? q.uniforms[uc0 + 1] : 0.0;
-  const double u2b = (rnd && uc0 + 2 < q.n_uniforms) ? q.uniforms[uc0 + 2] : 0.0;
-  const long long i = cauchy_select_row_dev(q, uc0, u1);
-  if (i < 0) return;
+  if (cauchy_select_row_dev(q) < 0) return;
   __syncthreads();  // st->pi written by thread 0
-  cauchy_row_dev<P>(q, threadIdx.x, blockDim.x, i);
+  cauchy_row_dev<P>(q, threadIdx.x, blockDim.x);
   __syncthreads();  // r, |r|^2 and the row max are in place
-  cauchy_select_col_dev(q, rnd ? uc0 + 1 : -1, u2a, u2b);
+  cauchy_select_col_dev(q);
 }
 
 // ---------------------------------------------------------------------------
