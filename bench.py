@@ -786,6 +786,10 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     A_host = host_t.numpy()
     torch.cuda.synchronize()
     e2e_runs = max(1, min(args.steps, 3))
+    # one untimed call first, as for `value` (host-buffer path: pinned staging
+    # buffers and the graph of the new residual address are set up once)
+    rp.eliminate(A_host, rp.PivotRule("rplu", rp.RngState(seed)), rank, compute_dtype=tdtype)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(e2e_runs):
