@@ -785,7 +785,10 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     host_t.copy_(A)
     A_host = host_t.numpy()
     torch.cuda.synchronize()
-    e2e_runs = max(1, min(args.steps, 3))
+    # small configs: `reps` eliminations per timed step as for `value`, so a
+    # one-off host allocation (a fresh pinned block while the previous
+    # trace is still held) does not dominate a ~10 ms region
+    e2e_runs = max(1, min(args.steps, 3)) * reps
     # one untimed call first, as for `value` (host-buffer path: pinned staging
     # buffers and the graph of the new residual address are set up once)
     rp.eliminate(A_host, rp.PivotRule("rplu", rp.RngState(seed)), rank, compute_dtype=tdtype)
