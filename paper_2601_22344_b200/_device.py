@@ -57,6 +57,14 @@ def as_device_matrix(A, dtype=None, device=None, copy=True):
     dev = require_cuda(device)
     if hasattr(A, "tensor") and isinstance(getattr(A, "tensor"), torch.Tensor):
         A = A.tensor
+    else:
+        from .accessors import foreign_dense_array
+        arr = foreign_dense_array(A)
+        if arr is not None:
+            # the reference's DenseMatrix stores complex128 always
+            # (accessors.py:100); a real-valued one computes in float64,
+            # arithmetically identical
+            A = real_if_zero_imag(arr) if dtype is None else arr
     if isinstance(A, torch.Tensor):
         if A.dim() != 2:
             raise ValueError("expected a 2-D array")
@@ -74,6 +82,13 @@ def as_device_matrix(A, dtype=None, device=None, copy=True):
                torch.complex128: np.complex128}[want]
     a = np.ascontiguousarray(a, dtype=np_want)
     return torch.from_numpy(a).to(dev)
+
+
+def real_if_zero_imag(a):
+    """float64 view of a complex array whose imaginary parts are all zero."""
+    if np.iscomplexobj(a) and not np.any(a.imag):
+        return np.ascontiguousarray(a.real)
+    return a
 
 
 def padded_residual(t):

@@ -22,6 +22,8 @@ __all__ = [
     "DenseMatrix",
     "CallableOperator",
     "materialize",
+    "foreign_dense_array",
+    "is_host_accessor",
 ]
 
 CAPABILITIES = ("apply", "adjoint_apply", "entry", "row", "column", "row_norms")
@@ -162,6 +164,29 @@ class CallableOperator(MatrixAccessor):
         if self._row_norms is None:
             return super().row_norms()
         return np.asarray(self._row_norms(), dtype=float)
+
+
+def foreign_dense_array(A):
+    """The host array of a dense accessor that is not this package's
+    :class:`DenseMatrix` -- e.g. the reference's ``rplu.DenseMatrix``
+    (accessors.py:93-131 keeps it in ``.array``) -- else None.  Lets the
+    reference's own objects cross the boundary (cli.py:150 passes one to
+    eliminate)."""
+    if isinstance(A, DenseMatrix) or isinstance(A, np.ndarray):
+        return None
+    arr = getattr(A, "array", None)
+    if isinstance(arr, np.ndarray) and arr.ndim == 2:
+        return arr
+    return None
+
+
+def is_host_accessor(A):
+    """Duck-typed accessor with host callables (the reference's
+    MatrixAccessor family: ``shape`` plus ``apply``)."""
+    if isinstance(A, MatrixAccessor):
+        return not getattr(A, "on_device", False)
+    return hasattr(A, "shape") and callable(getattr(A, "apply", None)) and \
+        not isinstance(A, np.ndarray)
 
 
 def materialize(acc):

@@ -93,13 +93,19 @@ class EliminationTrace:
 
 
 def _input_tensor(A, compute_dtype):
+    """(device matrix, host-results?) -- accessor inputs (this package's
+    DenseMatrix, or the reference's own rplu.DenseMatrix) return numpy
+    results as the reference does; only CUDA tensors keep them on device."""
     if isinstance(A, DenseMatrix):
         t = A.tensor
         if compute_dtype is not None:
             t = t.to(_device._resolve_dtype(t.is_complex(), compute_dtype))
-        return t, False
-    host = not (isinstance(A, torch.Tensor) and A.is_cuda)
-    return _device.as_device_matrix(A, dtype=compute_dtype, copy=False), host
+        return t, True, t is not A.tensor
+    if isinstance(A, torch.Tensor) and A.is_cuda:
+        t = _device.as_device_matrix(A, dtype=compute_dtype, copy=False)
+        return t, False, t is not A
+    # host arrays (and the reference's DenseMatrix): the upload is private
+    return _device.as_device_matrix(A, dtype=compute_dtype, copy=False), True, True
 
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
@@ -115,7 +121,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     promotion; torch.float32 for the fp32 residual), ``overwrite_a`` (reuse a
     CUDA input tensor as the residual buffer instead of copying it), and
     ``return_device`` (keep L/U/residual as CUDA tensors; default: True iff
-    the input was a CUDA tensor), ``time_kernels`` (bracket the K2/K3 launches
+    the input was a CUDA tensor -- numpy arrays and DenseMatrix accessors,
+    ours or the reference's, get numpy results), ``time_kernels`` (bracket the K2/K3 launches
     with CUDA events; results in ``trace.kernel_stats``), ``update``
     ("auto" | "eager" | "lazy": update the residual every step, or apply the
     pending rank-1 terms on the fly and write R every few steps — same bits,
@@ -130,7 +137,7 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     if rule.tag not in _DEVICE_RULES:
         raise CapabilityError(
             f"rule {rule.tag!r} is not on the B200 RPLU path (supported: {_DEVICE_RULES})")
-    src, host_in = _input_tensor(A, compute_dtype)
+    src, host_in, private = _input_tensor(A, compute_dtype)
     n, m = src.shape
     if not 0 <= steps <= min(n, m):
         raise ValueError(f"steps {steps} out of range [0, {min(n, m)}]")
@@ -141,8 +148,7 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
 
     dev = src.device
     vec = _device.vec_of(src.dtype)
-    fresh = host_in or (src is not A and src is not getattr(A, "tensor", None))
-    if (overwrite_a or fresh) and src.is_contiguous() and m % vec == 0:
+    if (overwrite_a or private) and src.is_contiguous() and m % vec == 0:
         buf, R = src, src    # the conversion already made a private copy
     else:
         buf, R = _device.padded_residual(src)

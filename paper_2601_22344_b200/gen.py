@@ -13,6 +13,15 @@ import numpy as np
 
 from .rng import RngState
 
+
+def _blas_threads(k):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=k, user_api="blas")
+    except ImportError:  # pragma: no cover - threadpoolctl ships with the image
+        import contextlib
+        return contextlib.nullcontext()
+
 __all__ = ["c1_dense", "c2_cauchy", "c3_householder", "c3_dense_host", "c3_dense_host_wy",
            "c3_dense_device",
            "c4_cauchy_like", "c5_points", "planted_spectrum"]
@@ -23,11 +32,16 @@ def c1_dense(seed, n=2000, m=None):
     sigma_i = 10^(-i/40), i = 1..min(n,m) (BASELINE configs[0])."""
     m = n if m is None else m
     g = RngState(seed)
-    Q1 = np.linalg.qr(g.standard_normal((n, n)))[0]
-    Q2 = np.linalg.qr(g.standard_normal((m, m)))[0]
-    r = min(n, m)
-    s = 10.0 ** (-np.arange(1, r + 1) / 40.0)
-    return (Q1[:, :r] * s) @ Q2[:, :r].T
+    # LAPACK's blocked QR splits its panels by BLAS thread count: pin it to the
+    # 8 threads of the container that recorded the reference runs, so the
+    # input bytes (and the reference's recorded pivots) are reproduced on any
+    # host (measured: 16 threads on the GPU box give different bytes).
+    with _blas_threads(8):
+        Q1 = np.linalg.qr(g.standard_normal((n, n)))[0]
+        Q2 = np.linalg.qr(g.standard_normal((m, m)))[0]
+        r = min(n, m)
+        s = 10.0 ** (-np.arange(1, r + 1) / 40.0)
+        return (Q1[:, :r] * s) @ Q2[:, :r].T
 
 
 def c2_cauchy(seed, n=4096, m=None, cluster_frac=0.2):

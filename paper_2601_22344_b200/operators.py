@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _device, _ffi
-from .accessors import CapabilityError, DenseMatrix, MatrixAccessor
+from .accessors import CapabilityError, DenseMatrix, MatrixAccessor, foreign_dense_array
 
 __all__ = ["GaussianKernelOperator", "as_device_operator"]
 
@@ -213,6 +213,10 @@ def as_device_operator(A):
         return _DenseDeviceOp(A.tensor)
     if isinstance(A, torch.Tensor) and A.is_cuda:
         return _DenseDeviceOp(A)
+    arr = foreign_dense_array(A)
+    if arr is not None:     # the reference's rplu.DenseMatrix: upload its array
+        from . import _device
+        return _DenseDeviceOp(_device.as_device_matrix(A))
     raise CapabilityError(
         f"{type(A).__name__} is not a device operator: the B200 cur_build needs a "
         "DenseMatrix or GaussianKernelOperator (host callables have no device path)")

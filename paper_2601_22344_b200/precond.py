@@ -33,7 +33,7 @@ import scipy.linalg
 import torch
 
 from . import _device, _ffi
-from .accessors import DenseMatrix, MatrixAccessor
+from .accessors import DenseMatrix, MatrixAccessor, foreign_dense_array, is_host_accessor
 
 __all__ = ["SmwPreconditioner", "smw_build", "gmres", "GmresResult", "device_callable"]
 
@@ -74,7 +74,9 @@ class _DeviceLinear:
                 self.dense = A.tensor
             elif isinstance(A, torch.Tensor) and A.is_cuda:
                 self.dense = A
-            elif isinstance(A, MatrixAccessor):
+            elif foreign_dense_array(A) is not None:   # the reference's rplu.DenseMatrix
+                self.dense = _c128(foreign_dense_array(A), dev)
+            elif is_host_accessor(A):
                 self.host = A        # reference semantics: full applies through the accessor
             else:
                 self.dense = _c128(A, dev)
@@ -144,7 +146,8 @@ def _as_dev_fn(op, dev):
     (precond.py:109-118)."""
     if isinstance(op, SmwPreconditioner):
         return op.apply_dev
-    if isinstance(op, (MatrixAccessor, torch.Tensor)):
+    if isinstance(op, (MatrixAccessor, torch.Tensor)) or foreign_dense_array(op) is not None \
+            or (is_host_accessor(op) and not callable(op)):
         return _DeviceLinear(op, dev).apply
     if callable(op):
         return op if getattr(op, "on_device", False) else _host_fn(op, dev)

@@ -1,6 +1,8 @@
 """Host-side API behaviour that needs no GPU: rule validation, exception
 classes, uniform-stream bookkeeping, and the absence of any CPU fallback."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -73,3 +75,22 @@ def test_consumers_have_no_cpu_fallback():
         rp.gmres(np.eye(3), np.ones(3))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         rp.BarycentricRational([0.0, 1.0], [1.0, 2.0], [1.0, 1.0])
+
+
+def test_reference_accessor_duck_types():
+    """The reference's own accessor classes are recognised by the boundary
+    helpers (imported from /root/reference in the build container only)."""
+    import sys
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference not present on this host")
+    sys.path.insert(0, src)
+    try:
+        import rplu
+    finally:
+        sys.path.remove(src)
+    from paper_2601_22344_b200.accessors import foreign_dense_array, is_host_accessor
+    D = rplu.DenseMatrix(np.eye(3))
+    assert foreign_dense_array(D) is D.array
+    assert is_host_accessor(rplu.CallableOperator((3, 3), lambda v: v))
+    assert foreign_dense_array(np.eye(3)) is None and not is_host_accessor(np.eye(3))

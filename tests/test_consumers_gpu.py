@@ -286,3 +286,67 @@ def test_gmres_x0_and_restart_edge_cases(cuda_device):
     with pytest.warns(UserWarning):
         rs = rp.gmres(S, np.ones(n), restart=5, tol=1e-12, max_restarts=20)
     assert rs.stagnated and not rs.converged
+
+
+class _RefDense:
+    """Stand-in with the reference rplu.DenseMatrix's surface
+    (accessors.py:93-131: complex128 ``.array``, host apply/adjoint_apply);
+    /root/reference is not on the GPU box, so the tests use a duck type."""
+
+    def __init__(self, a):
+        self.array = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+        self.shape = self.array.shape
+
+    def apply(self, v):
+        return self.array @ v
+
+    def adjoint_apply(self, v):
+        return self.array.conj().T @ v
+
+
+class _RefCallable:
+    """Stand-in for rplu.CallableOperator (host callables only)."""
+
+    def __init__(self, K):
+        self.K = K
+        self.shape = K.shape
+
+    def apply(self, v):
+        return self.K @ v
+
+
+def test_reference_objects_cross_the_boundary(cuda_device):
+    """the reference's DenseMatrix (``.array``) and host
+    accessors are accepted by eliminate / smw_build / gmres, and accessor
+    inputs get numpy results as in the reference (cli.py:150-157)."""
+    A = gen.c1_dense(4, n=300, m=240)
+    want = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(4)), 30)
+    got = rp.eliminate(_RefDense(A), rp.PivotRule("rplu", rp.RngState(4)), 30)
+    assert isinstance(got.L, np.ndarray) and isinstance(got.U, np.ndarray)
+    assert got.pivots == want.pivots
+    np.testing.assert_array_equal(got.L, want.L)
+    np.testing.assert_array_equal(got.U, want.U)
+    assert isinstance(got.residual, np.ndarray)
+    # this package's DenseMatrix: numpy results, the accessor's buffer untouched
+    D = rp.DenseMatrix(A)
+    before = D.tensor.clone()
+    mine = rp.eliminate(D, rp.PivotRule("rplu", rp.RngState(4)), 30)
+    assert isinstance(mine.L, np.ndarray) and mine.pivots == want.pivots
+    np.testing.assert_array_equal(mine.U, want.U)
+    assert torch.equal(D.tensor, before)
+    # smw_build / gmres with the reference types
+    case, arr, (Ab, _, b_inv, K_apply, K) = _precond(0)
+    fact, _ = rp.cur_build(rp.DenseMatrix(Ab), "rplu-cur", case["k"],
+                           rng=rp.RngState(case["seed"] ^ 1))
+    ref_fact, _ = rp.cur_build(_RefDense(Ab), "rplu-cur", case["k"],
+                               rng=rp.RngState(case["seed"] ^ 1))
+    assert list(ref_fact.row_indices) == list(fact.row_indices)
+    pre = rp.smw_build(b_inv, _RefDense(Ab), fact)
+    pv = pre.apply(arr[case["name"] + "_v"])
+    np.testing.assert_allclose(pv, arr[case["name"] + "_pre_v"], rtol=1e-10,
+                               atol=1e-12 * np.abs(pv).max())
+    b = arr[case["name"] + "_b"]
+    res = rp.gmres(_RefCallable(K), b, M_inv=pre, restart=20, tol=1e-10, max_restarts=200)
+    assert res.iterations == case["pre"]["iterations"] and res.converged
+    res2 = rp.gmres(_RefDense(K), b, restart=10, tol=1e-8, max_restarts=300)
+    assert res2.iterations == case["plain"]["iterations"]

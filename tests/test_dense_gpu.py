@@ -18,7 +18,7 @@ import torch
 
 import oracle
 import paper_2601_22344_b200 as rp
-from conftest import GOLDEN, load_golden
+from conftest import GOLDEN, check_dense_parity, load_golden, record_parity
 from paper_2601_22344_b200 import gen
 
 pytestmark = pytest.mark.gpu
@@ -156,46 +156,49 @@ def test_zero_residual_clean_stop(cuda_device):
     assert tr.steps == 0 and tr.clean_early_stop
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2, 7, 19])
-def test_c1_seed_parity(seed, cuda_device):
-    """C1 2000^2, r=100: pivots identical to the oracle on the same bytes; when
-    the input bytes equal the reference run's (same LAPACK), identical to the
-    reference's recorded pivots too."""
-    A = gen.c1_dense(seed)
-    ref = oracle.eliminate_real(A, "rplu", 100, seed=seed, margins=True)
-    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(seed)), 100)
-    mism = [t for t, (a, b) in enumerate(zip(tr.pivots, ref["pivots"])) if a != b]
-    if mism:
-        t = mism[0]
-        assert ref["margins"][t] <= oracle.NEAR_REL, f"divergence at step {t} not near a boundary"
-        return
-    np.testing.assert_array_equal(tr.L, ref["L"])
-    np.testing.assert_array_equal(tr.U, ref["U"])
-    np.testing.assert_allclose(tr.resid_fro, ref["resid_fro"], rtol=1e-12)
-    path = os.path.join(GOLDEN, "c1_reference.json")
-    if os.path.exists(path):
-        runs = {r["seed"]: r for r in json.load(open(path))["runs"]}
-        if seed in runs and hashlib.sha256(A.tobytes()).hexdigest() == runs[seed]["sha256"]:
-            assert [list(p) for p in tr.pivots] == runs[seed]["pivots"]
+def test_c1_all_30_seeds_exact(cuda_device):
+    """C1 2000^2, r=100, seeds 0..29 (BASELINE configs[0]):
 
-
-def test_c1_statistics_30_seeds(cuda_device):
-    """||A-LU||_F/||A||_F over seeds 0..29 agrees with the oracle seed by seed
-    and the statistics agree with the reference's."""
-    errs = []
+    * the generated input bytes equal the ones the reference was run on
+      (sha256 recorded by tests/golden/make_golden.py) -- a mismatch fails;
+    * pivots identical to the reference's recorded pivots for every seed
+      (a divergence is accepted only at a draw the oracle marks within 1e-12
+      of a CDF boundary, and L/U are still checked up to that step);
+    * L, U bit-identical to the C oracle on the same bytes, resid_fro to
+      1e-12 relative of the reference's;
+    * ||A-LU||_F/||A||_F equal to the reference's seed by seed (1e-8) and so
+      are the 30-seed statistics.
+    """
+    from oracle import c_oracle
+    runs = {r["seed"]: r for r in json.load(open(os.path.join(GOLDEN, "c1_reference.json")))["runs"]}
+    errs, near, divergences = [], 0, {}
     for s in range(30):
         A = gen.c1_dense(s)
-        tr = rp.eliminate(torch.from_numpy(A).cuda(), rp.PivotRule("rplu", rp.RngState(s)), 100)
-        Ad = torch.from_numpy(A).cuda()
-        err = float(torch.linalg.norm(Ad - tr.L @ tr.U) / torch.linalg.norm(Ad))
+        assert hashlib.sha256(A.tobytes()).hexdigest() == runs[s]["sha256"], (
+            f"seed {s}: C1 input bytes differ from the reference run's")
+        ref = c_oracle.eliminate_c(A, "rplu", 100, seed=s, margins=True)
+        tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(s)), 100)
+        near += tr.near_boundary_draws
+        t = check_dense_parity(tr, ref)
+        want = [tuple(p) for p in runs[s]["pivots"]]
+        tr_ref = next((q for q, (a, b) in enumerate(zip(tr.pivots, want)) if a != b), None)
+        if tr_ref is not None:
+            assert ref["margins"][tr_ref] <= oracle.NEAR_REL, (s, tr_ref)
+            divergences[s] = tr_ref
+        k = 100 if tr_ref is None else tr_ref
+        np.testing.assert_allclose(tr.resid_fro[:k + 1], runs[s]["resid_fro"][:k + 1],
+                                   rtol=1e-12)
+        assert t == tr_ref
+        err = float(np.linalg.norm(A - tr.L @ tr.U) / np.linalg.norm(A))
         errs.append(err)
+        if tr_ref is None:
+            assert abs(err - runs[s]["rel_err"]) <= 1e-8 * runs[s]["rel_err"], s
     errs = np.array(errs)
-    path = os.path.join(GOLDEN, "c1_reference.json")
-    ref = np.array([r["rel_err"] for r in json.load(open(path))["runs"]])
-    # per-seed agreement (pivots identical => errors equal to rounding)
-    close = np.abs(errs - ref) <= 1e-8 * ref
-    assert close.sum() >= 28, (errs, ref)
-    assert abs(errs.mean() - ref.mean()) <= 0.05 * ref.mean()
+    ref_errs = np.array([runs[s]["rel_err"] for s in range(30)])
+    record_parity("c1_all_30_seeds", divergences=divergences, near_boundary_draws=near,
+                  mean=errs.mean(), min=errs.min(), max=errs.max(),
+                  ref_mean=ref_errs.mean(), ref_min=ref_errs.min(), ref_max=ref_errs.max())
+    assert abs(errs.mean() - ref_errs.mean()) <= 1e-8 * ref_errs.mean()
 
 
 def test_fp32_against_forced_replay(cuda_device):
@@ -221,24 +224,14 @@ def test_c3_reduced_parity(cuda_device):
     A = gen.c3_dense_host(0, n=4096)
     ref = oracle.eliminate_real(A, "rplu", 128, seed=0, margins=True)
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), 128)
-    mism = [t for t, (a, b) in enumerate(zip(tr.pivots, ref["pivots"])) if a != b]
-    if mism:
-        assert ref["margins"][mism[0]] <= oracle.NEAR_REL
-    else:
-        np.testing.assert_array_equal(tr.L, ref["L"])
-        np.testing.assert_array_equal(tr.U, ref["U"])
+    check_dense_parity(tr, ref)
 
 
 def test_complex_dense_parity(cuda_device):
     A = gen.planted_spectrum(300, 200, 0.9, 5)
     ref = oracle.eliminate_c128(A, "rplu", 80, seed=5, margins=True)
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(5)), 80)
-    mism = [t for t, (a, b) in enumerate(zip(tr.pivots, ref["pivots"])) if a != b]
-    if mism:
-        assert ref["margins"][mism[0]] <= 1e-9
-        return
-    np.testing.assert_allclose(tr.L, ref["L"], rtol=1e-12, atol=1e-14)
-    np.testing.assert_allclose(tr.U, ref["U"], rtol=1e-12, atol=1e-14)
+    check_dense_parity(tr, ref, exact=False, rtol=1e-12)
 
 
 @pytest.mark.parametrize("rule", ["c2plu", "cplu"])
@@ -377,12 +370,7 @@ def test_lazy_matches_oracle_c3_reduced(cuda_device):
     A = gen.c3_dense_host(1, n=4096)
     ref = oracle.eliminate_real(A, "rplu", 128, seed=1, margins=True)
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 128, update="lazy")
-    mism = [t for t, (a, b) in enumerate(zip(tr.pivots, ref["pivots"])) if a != b]
-    if mism:
-        assert ref["margins"][mism[0]] <= oracle.NEAR_REL
-    else:
-        np.testing.assert_array_equal(tr.L, ref["L"])
-        np.testing.assert_array_equal(tr.U, ref["U"])
+    check_dense_parity(tr, ref)
 
 
 @pytest.mark.slow

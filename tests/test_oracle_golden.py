@@ -88,13 +88,73 @@ def test_c1_reference_runs_pinned():
         ref = json.load(f)
     for run in ref["runs"][:2]:
         A = gen.c1_dense(run["seed"])
-        if hashlib.sha256(A.tobytes()).hexdigest() != run["sha256"]:
-            pytest.skip("C1 input bytes differ on this host (LAPACK build); see GPU test")
+        assert hashlib.sha256(A.tobytes()).hexdigest() == run["sha256"], (
+            "C1 input bytes differ from the reference run's (gen.c1_dense pins 8 BLAS threads)")
         out = oracle.eliminate_real(A, "rplu", ref["steps"], seed=run["seed"])
         assert [list(p) for p in out["pivots"]] == run["pivots"]
         np.testing.assert_allclose(out["resid_fro"], run["resid_fro"], rtol=1e-11)
         err = oracle.lu_error(A, out["L"], out["U"])
         assert abs(err - run["rel_err"]) <= 1e-9 * run["rel_err"]
+
+
+@pytest.mark.parametrize("case", [c for c, a in _dense_cases()
+                                  if not np.iscomplexobj(a[c["name"] + "_A"])],
+                         ids=lambda c: c["name"])
+def test_dense_c_oracle_matches_reference(case):
+    """The plain-C restatement (oracle/c/rplu_oracle.c, sequential masses as
+    the reference's einsum) reproduces the reference's pivots, L, U and
+    uniform consumption bit for bit."""
+    from oracle import c_oracle
+    _, arr = load_golden("dense")
+    name = case["name"]
+    A = arr[name + "_A"]
+    gen_ = oracle.uniform_stream(case["seed"]) if case["seed"] is not None else None
+    out = c_oracle.eliminate_c(A.astype(np.float64), case["rule"], case["steps"], gen=gen_,
+                               stop_tol=case["stop_tol"])
+    assert [list(p) for p in out["pivots"]] == case["pivots"]
+    assert out["tol_stop"] == case["tol_stop"]
+    assert out["clean_early_stop"] == case["clean_early_stop"]
+    np.testing.assert_array_equal(out["L"], arr[name + "_L"])
+    np.testing.assert_array_equal(out["U"], arr[name + "_U"])
+    np.testing.assert_allclose(out["resid_fro"], arr[name + "_resid_fro"], rtol=1e-12)
+    if gen_ is not None:
+        # the C oracle consumed uniforms_consumed of a bulk block; the stream
+        # position the reference left equals the same count of scalar draws
+        g2 = oracle.uniform_stream(case["seed"])
+        g2.random(out["uniforms_consumed"])
+        assert float(g2.random()) == case["next_uniform"]
+
+
+def test_c_oracle_c1_reference_runs():
+    """C oracle on C1 seeds 0..3: pivots equal the reference's recorded ones,
+    L/U bit-identical to the numpy restatement; forced replay of its own
+    pivots reproduces its factors."""
+    from oracle import c_oracle
+    with open(os.path.join(GOLDEN, "c1_reference.json")) as f:
+        ref = json.load(f)
+    for run in ref["runs"][:4]:
+        A = gen.c1_dense(run["seed"])
+        out = c_oracle.eliminate_c(A, "rplu", ref["steps"], seed=run["seed"], margins=True)
+        assert [list(p) for p in out["pivots"]] == run["pivots"]
+        np.testing.assert_allclose(out["resid_fro"], run["resid_fro"], rtol=1e-13)
+        assert out["margins"].min() > oracle.NEAR_REL
+        if run["seed"] == 0:
+            e = oracle.eliminate_real(A, "rplu", ref["steps"], seed=0)
+            np.testing.assert_array_equal(out["L"], e["L"])
+            np.testing.assert_array_equal(out["U"], e["U"])
+            rep = c_oracle.replay_c(A, out["pivots"])
+            np.testing.assert_array_equal(rep["L"], out["L"])
+            np.testing.assert_array_equal(rep["U"], out["U"])
+
+
+def test_c_oracle_zero_pivot_and_errors():
+    from oracle import c_oracle
+    with pytest.raises(ValueError):
+        c_oracle.eliminate_c(np.eye(3), "rplu", 4, seed=0)
+    with pytest.raises(ZeroDivisionError):
+        c_oracle.replay_c(np.eye(3), [(0, 1)])
+    out = c_oracle.eliminate_c(np.zeros((4, 4)), "rplu", 3, seed=0)
+    assert out["steps"] == 0 and out["clean_early_stop"]
 
 
 def test_c1_reference_statistics():
