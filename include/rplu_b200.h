@@ -385,6 +385,19 @@ int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, c
                       const double* chat, double l2, double floor, int64_t* clamped,
                       double* total, void* stream);
 
+/* K11 error evaluation: out_sq[0] = ||A - L U||_F^2 and
+ * out_sq[1] = ||A||_F^2 in one fused FP64-tensor-core kernel (DMMA), with no
+ * L U panel in memory.  Replaces the reconstruction the reference's error
+ * measures form, EliminationTrace.approximation() = L @ U and
+ * np.linalg.norm(dense - approx) (dense_pivots.py:82-83, cli.py:151-157,
+ * :200-206).  A: device n x m row-major (lda elements), dtype F32 / F64 /
+ * C128; L is passed transposed as Lt: device k x n (ldl) -- the layout
+ * rplu_dense_run fills -- and U: device k x m (ldu), both of A's dtype.
+ * *kernel_ms (optional): CUDA-event time of the product kernel(s). */
+int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int64_t n, int64_t m,
+                  const void* Lt, int64_t ldl, const void* U, int64_t ldu, int64_t k,
+                  double* out_sq, double* kernel_ms, void* stream);
+
 /* Diagnostic: measured FP64 FMA-pipe throughput of the context's GPU
  * (TFLOP/s, best of 5), the roofline denominator of the generated-entry
  * (Cauchy-like, Gaussian-kernel) kernels. */

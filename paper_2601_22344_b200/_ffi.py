@@ -153,6 +153,9 @@ SIGNATURES = {
     "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
     "rplu_kernel_launch_count": (c_i64, []),
+    "rplu_lu_error": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
+                                     c_i64, c_i64, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
+                                     c_vp]),
     "rplu_cauchy_plan_row": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                             c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rplu_cauchy_plan_update": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,

@@ -215,6 +215,8 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->gbar.release();
     ctx->csync.release();
     ctx->krylov.release();
+    ctx->lu_pad.release();
+    ctx->lu_part.release();
     for (auto& b : ctx->scratch) b.release();
     for (auto& e : ctx->graph_exec)
       if (e) cudaGraphExecDestroy(e);
@@ -811,6 +813,19 @@ int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, cons
   if (g.rc) return g.rc;
   return cauchy_plan_update_impl(ctx, p, n, m, x, y, G, Bt, i, j, const_cast<void*>(rbuf), Cout,
                                  Rout, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int64_t n, int64_t m,
+                  const void* Lt, int64_t ldl, const void* U, int64_t ldu, int64_t k,
+                  double* out_sq, double* kernel_ms, void* stream) {
+  if (!ctx || !A || !out_sq || (k > 0 && (!Lt || !U))) {
+    set_error("rplu_lu_error: NULL argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return lu_error_impl(ctx, dtype, A, lda, n, m, Lt, ldl, U, ldu, k, out_sq, kernel_ms,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {

@@ -114,6 +114,11 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int
                       long long* idx, int* near, double* total, cudaStream_t s);
 int cuda_fail(cudaError_t e, const char* where);
 
+// K11 fused ||A - X Y||_F^2, ||A||_F^2 (lu_error.cu); out_sq host[2]
+int lu_error_impl(rplu_ctx* ctx, int dtype, const void* A, long long lda, long long n,
+                  long long m, const void* Xt, long long ldx, const void* Y, long long ldy,
+                  long long k, double* out_sq, double* kernel_ms, cudaStream_t s);
+
 #define RPLU_CUDA(call)                                        \
   do {                                                         \
     cudaError_t _e = (call);                                   \
@@ -158,4 +163,6 @@ struct rplu_ctx {
   rplu::DevBuf gbar;        // grid-barrier counters (persistent dense loop)
   rplu::DevBuf csync;       // Cauchy loop: split-arrival counters + row max slot
   rplu::DevBuf krylov;      // MGS Arnoldi: per-CTA partials + grid barrier
+  rplu::DevBuf lu_pad;      // K11: zero-padded fp64 factor panels
+  rplu::DevBuf lu_part;     // K11: per-CTA partial sums
 };

@@ -81,6 +81,17 @@ class CurFactorization:
         """Solve A[I, J] x = v."""
         return self._solve(v, False)
 
+    def core_solve_block(self, B):
+        """Solve A[I, J] X = B for a k x c device block in one call (the
+        rebuild and the CUR error evaluation; no per-column host round trip)."""
+        Bt = B.to(device=self._W.device, dtype=torch.promote_types(B.dtype, self._W.dtype))
+        if self.rank == 0:
+            return Bt[:0]
+        if self.mode == "inverse":
+            return self._U.to(Bt.dtype) @ Bt
+        Q, R = self._Q.to(Bt.dtype), self._R.to(Bt.dtype)
+        return torch.linalg.solve_triangular(R, Q.conj().T @ Bt, upper=True)
+
     def core_solve_t(self, v):
         """Solve A[I, J]^T x = v (plain transpose)."""
         return self._solve(v, True)
@@ -213,7 +224,7 @@ def _rebuild_row_norms(op, fact, nrow, chunk=256):
     for j0 in range(0, m, chunk):
         j1 = min(j0 + chunk, m)
         blk = op.block_cols_dev(j0, j1)
-        X = torch.stack([fact.core_solve(blk[I, c]) for c in range(j1 - j0)], dim=1)
+        X = fact.core_solve_block(blk[I, :])      # one k x chunk solve
         res = blk - CJ @ X
         nrow += (res.real ** 2 + (res.imag ** 2 if torch.is_complex(res) else 0)).sum(1)
 

@@ -401,7 +401,7 @@ def test_error_evaluation_matches_reference_measures(cuda_device):
     from paper_2601_22344_b200 import errors
     A = gen.c1_dense(1, n=400, m=300)
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 40)
-    fro = errors.lu_error(A, tr.L, tr.U, panel_rows=128)
+    fro = errors.lu_error(A, tr.L, tr.U)
     assert abs(fro - oracle.lu_error(A, tr.L, tr.U)) <= 1e-12 * fro
     # power iteration restated on the host (cli.py:86-99)
     R = A - tr.L @ tr.U
@@ -418,3 +418,45 @@ def test_error_evaluation_matches_reference_measures(cuda_device):
     s = np.linalg.svd(A, compute_uv=False)
     f, sp = errors.truncated_svd_error(A, 40)
     assert abs(f - np.sqrt((s[40:] ** 2).sum())) <= 1e-10 * f and abs(sp - s[40]) <= 1e-10 * sp
+
+
+@pytest.mark.parametrize("n,m,k,dtype", [(1000, 777, 37, np.float64), (129, 1031, 16, np.float64),
+                                         (700, 500, 60, np.complex128), (513, 257, 8, np.float32),
+                                         (300, 200, 0, np.float64), (1, 5, 1, np.float64)])
+def test_k11_lu_error_kernel(n, m, k, dtype, cuda_device):
+    """K11 (rplu_lu_error, DMMA tensor cores, fused subtract + Frobenius) on
+    ragged shapes, complex, fp32 and k = 0 against numpy: ||A - L U||_F to
+    1e-12 relative, ||A||_F to 1e-13."""
+    from paper_2601_22344_b200 import errors
+    rs = np.random.default_rng(n + m + k)
+    A = rs.standard_normal((n, m))
+    L = rs.standard_normal((n, k))
+    U = rs.standard_normal((k, m))
+    if dtype == np.complex128:
+        A = A + 1j * rs.standard_normal((n, m))
+        L = L + 1j * rs.standard_normal((n, k))
+        U = U + 1j * rs.standard_normal((k, m))
+    A, L, U = A.astype(dtype), L.astype(dtype), U.astype(dtype)
+    e, a, ms = errors.lu_error_sq(A, L, U)
+    A64, L64, U64 = (x.astype(np.complex128 if dtype == np.complex128 else np.float64)
+                     for x in (A, L, U))
+    want_e = np.linalg.norm(A64 - L64 @ U64) ** 2
+    want_a = np.linalg.norm(A64) ** 2
+    assert abs(e - want_e) <= 1e-12 * want_e
+    assert abs(a - want_a) <= 1e-13 * want_a
+    assert ms > 0
+
+
+def test_k11_on_elimination_factors(cuda_device):
+    """K11 on the factors of a real elimination (L from Lt, no transpose
+    copy) at 8192^2, r = 512: equal to the oracle's host computation."""
+    from paper_2601_22344_b200 import errors
+    A = gen.c3_dense_device(0, n=8192)
+    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), 512)
+    e, a, ms = errors.lu_error_sq(A, tr.L, tr.U)
+    Ah, Lh, Uh = A.cpu().numpy(), tr.L.cpu().numpy(), tr.U.cpu().numpy()
+    want = oracle.lu_error(Ah, Lh, Uh)
+    assert abs(np.sqrt(e / a) - want) <= 1e-11 * want
+    # the eliminate identity: ||A - LU|| = ||R_k|| = resid_fro[k]
+    assert abs(np.sqrt(e) - tr.resid_fro[-1]) <= 1e-9 * tr.resid_fro[-1]
+    record_parity("k11_8192", tflops=2.0 * 8192 * 8192 * 512 / (ms * 1e-3) / 1e12, ms=ms)

@@ -86,7 +86,7 @@ def test_c3_fp32_full_size_parity(c3_host, cuda_device):
     ok_cols = int(np.count_nonzero(dl_col <= 1e-4))
     record_parity("c3_fp32_full", n=N3, steps=R3, first_divergence=t,
                   near_boundary_draws=tr.near_boundary_draws, U_rel=du, resid_rel=dr,
-                  L_rel_max=float(dl_col.max()), L_cols_within_1e-4=ok_cols,
+                  L_rel_max=float(dl_col.max()), L_cols_within_tol=ok_cols,
                   L_rel_over_model_max=float((dl_col / np.maximum(model, 1e-300)).max()))
     assert du <= 1e-4 and dr <= 1e-4
     assert np.all(dl_col <= np.maximum(1e-4, 16.0 * model)), "L error beyond the fp32 model"
