@@ -50,6 +50,10 @@ CONFIGS = {
                         "through the certified-bound plan path (build_plan + rejection "
                         "sampling), as every in-package Cauchy caller runs it",
                    n=1 << 20, rank=256, dtype="c128", seed=0, kind="cauchy_plan", p=4),
+    "luerr": dict(desc="SURVEY 8(a) a17 / K11: ||A - L U||_F / ||A||_F of the C3 fp64 "
+                       "32768^2 rank-512 elimination (FP64 tensor cores, fused); bench step = "
+                       "one error evaluation",
+                  n=32768, rank=512, dtype="f64", seed=0, kind="luerr"),
     # §8(f4) consumers (not BASELINE configs: supplementary measurement lines)
     "gmres": dict(desc="SURVEY 8(f4) restarted GMRES: one 20-step MGS Arnoldi cycle on n=2^24 "
                        "complex128 (stencil operator); bench step = one restart cycle",
@@ -520,6 +524,92 @@ def run_gmres_arm(args, cfg):
                launches, clk)
 
 
+def run_luerr_arm(args, cfg):
+    """K11 at C3: the fused L.U reconstruction error of the C3 fp64 rank-512
+    elimination (2 n m k flop on the FP64 tensor cores), against the measured
+    DMMA issue rate; cuBLAS DGEMM L @ U (the unfused product alone) timed
+    beside it for reference."""
+    import torch
+
+    import oracle
+    import paper_2601_22344_b200 as rp
+    from paper_2601_22344_b200 import _ffi, errors, gen
+    torch.cuda.set_device(0)
+    n, k, seed = cfg["n"], cfg["rank"], cfg["seed"]
+    A = gen.c3_dense_device(seed, n=n)
+    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(seed)), k)
+    L, U = tr.L, tr.U
+    del tr
+    torch.cuda.empty_cache()
+    for _ in range(args.warmup):
+        errors.lu_error_sq(A, L, U)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _ffi.kernel_launch_count()
+    kms = []
+    e0.record()
+    for _ in range(args.steps):
+        e, a, ms = errors.lu_error_sq(A, L, U)
+        kms.append(ms)
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = e0.elapsed_time(e1)
+    launches = _ffi.kernel_launch_count() - launches0
+    flops = 2.0 * n * n * k
+    value = args.steps / (total_ms / 1e3)
+    peak = _ffi.dmma_peak_tflops(0)
+    achieved = flops / (statistics.mean(kms) / 1e3) / 1e12
+    # cuBLAS DGEMM L @ U alone (n x n output written, no subtraction / norm)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.matmul(L, U)
+    torch.cuda.synchronize()
+    t0.record()
+    P = torch.matmul(L, U)
+    t1.record()
+    torch.cuda.synchronize()
+    cublas_ms = t0.elapsed_time(t1)
+    del P
+    torch.cuda.empty_cache()
+    # e2e: pinned host A, L, U in; the scalar error out
+    Ah = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+    Ah.copy_(A)
+    Lh, Uh = L.cpu().numpy(), U.cpu().numpy()
+    del A
+    torch.cuda.empty_cache()
+    e0.record()
+    err_h = errors.lu_error(Ah.numpy(), Lh, Uh)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    # CPU baseline: the oracle's numpy A - L U and norm on a 1024-row sample
+    rows = 1024
+    t = time.perf_counter()
+    oracle.lu_error(Ah.numpy()[:rows], Lh[:rows], Uh)
+    cpu_s = (time.perf_counter() - t) * n / rows
+    model, _ = _cpu_info()
+    _supp_line(args, cfg, "L.U reconstruction error evaluations/s (K11, C3 rank 512)",
+               "evaluations/s", value, total_ms,
+               {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "lu_error_kernel<double,1> (DMMA m8n8k4, fused subtract + Frobenius)",
+                "algorithmic_flops_per_launch": flops, "avg_launch_ms": statistics.mean(kms),
+                "peak_source": "measured DMMA issue rate (rplu_diag_dmma_peak)",
+                "cublas_dgemm_LU_ms": cublas_ms,
+                "cublas_dgemm_tflops": flops / (cublas_ms / 1e3) / 1e12},
+               {"value": 1.0 / cpu_s, "unit": "evaluations/s",
+                "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                "sample": f"oracle.lu_error on {rows} of {n} rows ({cpu_s * rows / n:.2f}s, "
+                          f"numpy/OpenBLAS), scaled linearly; CPU: {model}"},
+               {"value": 1.0 / (e2e_ms / 1e3), "unit": "evaluations/s",
+                "h2d_bytes_per_step": 8 * (n * n + 2 * n * k), "d2h_bytes_per_step": 8},
+               launches, clk, extra={"dtype": "f64", "rel_error": float(np.sqrt(e / a)),
+                                     "rel_error_e2e": err_h})
+
+
 def run_bary_arm(args, cfg):
     """Barycentric evaluation kernel (generated Cauchy entries, FP64 pipe)
     at 2^24 points, degree 256; plus one cur_aaa fit as the e2e call."""
@@ -705,6 +795,8 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
         return run_gmres_arm(args, cfg)
     if cfg.get("kind") == "bary":
         return run_bary_arm(args, cfg)
+    if cfg.get("kind") == "luerr":
+        return run_luerr_arm(args, cfg)
 
     import paper_2601_22344_b200 as rp
     from paper_2601_22344_b200 import gen

@@ -403,6 +403,10 @@ int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int6
  * (Cauchy-like, Gaussian-kernel) kernels. */
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms);
 
+/* Diagnostic: measured FP64 tensor-core (DMMA m8n8k4) throughput, the K11
+ * roofline denominator (TFLOP/s, best of 5). */
+int rplu_diag_dmma_peak(rplu_ctx* ctx, double* tflops, double* best_ms);
+
 /* sample_index(weights, u) on a device weight vector (rng.py:50-74):
  * first index whose running sum exceeds u*total, top clamp, walk-back over
  * zero weights.  RPLU_ERR_ARG for empty / negative / all-zero weights.

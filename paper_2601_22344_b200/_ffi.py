@@ -142,6 +142,7 @@ SIGNATURES = {
     "rplu_cauchy_row_norms": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                              c_vp, c_vp]),
     "rplu_diag_fp64_peak": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
+    "rplu_diag_dmma_peak": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
     "rplu_tree_bounds": (ctypes.c_int, [c_vp, ctypes.POINTER(TreePlan), c_vp, c_vp, c_vp, c_vp,
                                         c_vp, c_vp]),
     # Gaussian-kernel operator struct is passed by pointer (operators._GaussOpStruct)
@@ -200,6 +201,15 @@ def fp64_peak_tflops(device=0):
     tf, ms = c_dbl(0.0), c_dbl(0.0)
     check(c._lib.rplu_diag_fp64_peak(c.handle, ctypes.byref(tf), ctypes.byref(ms)))
     return tf.value
+
+
+def dmma_peak_tflops(device=0):
+    """Measured FP64 tensor-core (DMMA) throughput of `device` (TFLOP/s)."""
+    c = context(device)
+    tf, ms = c_dbl(0.0), c_dbl(0.0)
+    check(c._lib.rplu_diag_dmma_peak(c.handle, ctypes.byref(tf), ctypes.byref(ms)))
+    return tf.value
+
 
 _lib = None
 _lib_lock = threading.Lock()

@@ -828,6 +828,13 @@ int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int6
                        static_cast<cudaStream_t>(stream));
 }
 
+int rplu_diag_dmma_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {
+  if (!ctx || !tflops) { set_error("rplu_diag_dmma_peak: NULL argument"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return dmma_peak_impl(ctx, tflops, best_ms);
+}
+
 int rplu_diag_fp64_peak(rplu_ctx* ctx, double* tflops, double* best_ms) {
   if (!ctx || !tflops) { set_error("rplu_diag_fp64_peak: NULL argument"); return RPLU_ERR_ARG; }
   DeviceGuard g(ctx->device);

@@ -22,6 +22,55 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, 
   if (s == 12345.678) out[blockIdx.x] = s;  // practically never taken
 }
 
+// FP64 tensor-core (DMMA m8n8k4) issue rate: 8 independent accumulator
+// tiles per warp, the K11 roofline denominator.
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+  double acc[8][2];
+  const double a = 1e-3 * threadIdx.x, b = 0.5;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = c;
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[c][0]), "+d"(acc[c][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+int dmma_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out) {
+  int rc;
+  if ((rc = ctx->scratch[6].ensure(sizeof(double) * 4096))) return rc;
+  double* out = reinterpret_cast<double*>(ctx->scratch[6].ptr);
+  const int blocks = ctx->sm_count * 2;
+  const int iters = 4096;
+  cudaEvent_t e0, e1;
+  RPLU_CUDA(cudaEventCreate(&e0));
+  RPLU_CUDA(cudaEventCreate(&e1));
+  dmma_peak_kernel<<<blocks, 256>>>(out, 64);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    RPLU_CUDA(cudaEventRecord(e0));
+    dmma_peak_kernel<<<blocks, 256>>>(out, iters);
+    RPLU_CUDA(cudaEventRecord(e1));
+    RPLU_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    RPLU_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  // 8 x 8 x 4 FMAs per DMMA, 8 per iteration per warp
+  const double flops = 2.0 * 8 * 8 * 4 * 8 * (double)iters * (blocks * 256 / 32);
+  *tflops = flops / (best * 1e-3) / 1e12;
+  if (ms_out) *ms_out = best;
+  return RPLU_OK;
+}
+
 int fp64_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out) {
   int rc;
   if ((rc = ctx->scratch[6].ensure(sizeof(double) * 4096))) return rc;

@@ -114,6 +114,8 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int
                       long long* idx, int* near, double* total, cudaStream_t s);
 int cuda_fail(cudaError_t e, const char* where);
 
+int dmma_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
+
 // K11 fused ||A - X Y||_F^2, ||A||_F^2 (lu_error.cu); out_sq host[2]
 int lu_error_impl(rplu_ctx* ctx, int dtype, const void* A, long long lda, long long n,
                   long long m, const void* Xt, long long ldx, const void* Y, long long ldy,

@@ -3,10 +3,10 @@
 #   scripts/gpu.sh TAG STEP [STEP ...]
 # STEP is one of
 #   smoke                 __graft_entry__.smoke()
-#   test:EXPR[:ARGS]      pytest -m EXPR (e.g. test:gpu, "test:gpu and not slow", test:gpu:tests/test_x.py)
+#   test:EXPR[:ARGS]      pytest -m EXPR ARGS (ARGS eval'd: quote -k expressions with '')
 #   bench:CONFIG[:ARGS]   bench.py --config CONFIG (CONFIG "ref" = --impl reference)
 #   launches:CONFIG       ncu launch list (gpu__time_duration) of one bench run
-#   full:CONFIG:KERNEL[:COUNT]  ncu --set full of KERNEL (regex) in a bench run
+#   full:CONFIG:KERNEL[:COUNT[:ARGS]]  ncu --set full of KERNEL (regex) in a bench run
 #   py:SCRIPT[:ARGS]      python SCRIPT ARGS
 # Logs go to gpurun_out/TAG/; the parity log to gpurun_out/TAG/parity.jsonl.
 TAG=$1; shift
@@ -23,7 +23,7 @@ for step in "$@"; do
       timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/$i.smoke.log" 2>&1 ;;
     test)
       expr=${rest%%:*}; args=""; [[ $rest == *:* ]] && args=${rest#*:}
-      timeout 3000 python -m pytest -m "$expr" -q -rs $args > "$OUT/$i.test.log" 2>&1 ;;
+      eval "timeout 3000 python -m pytest -m \"$expr\" -q -rs $args" > "$OUT/$i.test.log" 2>&1 ;;
     bench)
       cfg=${rest%%:*}; args=""; [[ $rest == *:* ]] && args=${rest#*:}
       if [[ $cfg == ref ]]; then
@@ -36,9 +36,10 @@ for step in "$@"; do
         --log-file "$OUT/$i.launches_$rest.csv" python bench.py --config "$rest" --steps 1 --warmup 3 \
         > "$OUT/$i.launches_$rest.log" 2>&1 ;;
     full)
-      cfg=${rest%%:*}; r2=${rest#*:}; kern=${r2%%:*}; cnt=1; [[ $r2 == *:* ]] && cnt=${r2#*:}
+      cfg=${rest%%:*}; r2=${rest#*:}; kern=${r2%%:*}; cnt=1; fargs=""
+      if [[ $r2 == *:* ]]; then r3=${r2#*:}; cnt=${r3%%:*}; [[ $r3 == *:* ]] && fargs=${r3#*:}; fi
       timeout 2400 ncu --set full --clock-control none --import-source on -k "regex:$kern" -c "$cnt" \
-        -o "$OUT/$i.full_${cfg}" python bench.py --config "$cfg" --steps 1 --warmup 3 \
+        -o "$OUT/$i.full_${cfg}" python bench.py --config "$cfg" --steps 1 --warmup 1 $fargs \
         > "$OUT/$i.full_$cfg.log" 2>&1 ;;
     py)
       scr=${rest%%:*}; args=""; [[ $rest == *:* ]] && args=${rest#*:}
