@@ -21,6 +21,7 @@ from .operators import GaussianKernelOperator
 from .precond import GmresResult, SmwPreconditioner, device_callable, gmres, smw_build
 from .rational import BarycentricRational, SampleSet, aaa, bary_eval, cur_aaa
 from .rng import RngState, sample_index
+from . import errors, sweep  # noqa: F401  (§8(f2) error evaluation / sweep harness)
 from .treebounds import (CoincidentPointsError, InteractionPlan, PointQuadtree, build_plan,
                          certified_upper_bounds)
 

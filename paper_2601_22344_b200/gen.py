@@ -204,6 +204,7 @@ def planted_spectrum(n, m, rho, seed):
         q, rr = np.linalg.qr(g.complex_normal((k, k)))
         return q * (np.diag(rr) / np.abs(np.diag(rr)))
 
-    U = unitary(n)[:, :r]
-    V = unitary(m)[:, :r]
-    return (U * s) @ V.conj().T
+    with _blas_threads(8):     # input bytes independent of the host's thread count
+        U = unitary(n)[:, :r]
+        V = unitary(m)[:, :r]
+        return (U * s) @ V.conj().T

@@ -390,7 +390,30 @@ def precond_cases():
     save("precond", arrays, info)
 
 
+def sweep_cases():
+    """The reference's error sweep (cli._sweep_rows, cli.py:100-138) over the
+    hot-path methods: rows (rank, method, seed, frob_err/||A||_F,
+    spec_err/||A||_2, seconds, applies, adjoints)."""
+    from rplu import cli
+    info = []
+    for name, A, methods, ranks, trials, seed in (
+            ("planted120x100", gen.planted_spectrum(120, 100, 0.8, 3),
+             ["rplu", "cplu", "c2plu", "rplu-cur", "c2plu-cur", "svd-oracle"], [4, 8, 16], 3, 11),
+            ("c1_300x250", gen.c1_dense(2, n=300, m=250), ["rplu", "rplu-cur", "svd-oracle"],
+             [10, 40], 2, 5)):
+        rows = cli._sweep_rows(rplu.DenseMatrix(A), methods, ranks, trials, seed)
+        info.append({"name": name, "sha256": sha(A), "methods": methods, "ranks": ranks,
+                     "trials": trials, "seed": seed,
+                     "rows": [[int(k), m, int(sd), float(ef), float(es), 0.0, int(na), int(nat)]
+                              for (k, m, sd, ef, es, _sec, na, nat) in rows]})
+    with open(os.path.join(HERE, "sweep.json"), "w") as f:
+        json.dump({"meta": meta(), "cases": info}, f, indent=1)
+
+
 if __name__ == "__main__":
+    if "--sweep" in sys.argv:
+        sweep_cases()
+        sys.exit(0)
     if "--consumers" not in sys.argv:
         sample_index_cases()
         dense_cases()
