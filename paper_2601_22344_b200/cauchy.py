@@ -7,9 +7,10 @@ as Bt (m x p, i.e. the reference's F-order B, column j contiguous).
 ``structured_eliminate`` with ``plan=None`` runs the exact-norm Alg 3 loop
 entirely on the device (K5 generated-entry row masses, K2 selects, K6 row /
 column generation and generator update) through ``rplu_cauchy_run``; with a
-plan (certified tree bounds + rejection sampling) it raises
-CapabilityError instead of silently switching to exact norms, because the
-plan path consumes a different uniform stream.
+plan (certified tree bounds + rejection sampling) it runs the
+reference's proposal / acceptance loop and uniform stream (cauchy.py:259-277)
+over device bound kernels (``csrc/tree.cu``) and the same K6 row / update
+kernels.  ``generator_schur_update`` is the single-step K6 update.
 """
 
 import ctypes
@@ -195,17 +196,37 @@ def tree_bounds_device(plan, M):
 def generator_schur_update(M, pivot):
     """Eliminate one pivot by updating the generators (cauchy.py:140-154).
 
-    O((n+m)p) device work; returns a new CauchyLikeMatrix over the same points.
+    O((n+m)p) device work in the K6 kernels the plan path uses
+    (``rplu_cauchy_plan_row`` then ``rplu_cauchy_plan_update``: numpy-exact
+    complex products and Smith division): r = row i, the relative zero-pivot
+    guard |r_j| <= 1e-14 max|r| (ZeroDivisionError), then
+    G1 = G - (c / a) G_i and B1 = B - B_:,j (r / a) with c = column j.
+    Returns a new CauchyLikeMatrix over the same points (the input's
+    generators are not modified, as the reference allocates new ones).
     """
-    i, j = pivot
-    r = (M.Bt @ M.G[i]) / (M.x[i] - M.y)
-    a = r[j]
-    if float(a.abs()) <= PIVOT_REL_TOL * float(r.abs().max()):
+    i, j = int(pivot[0]), int(pivot[1])
+    n, m = M.shape
+    if not (0 <= i < n and 0 <= j < m):
+        raise IndexError(f"pivot ({i}, {j}) out of range for shape {(n, m)}")
+    dev = M.device
+    c = _device.ctx(dev)
+    stream_h = _device.stream_handle(dev)
+    G1 = M.G.clone()
+    Bt1 = M.Bt.clone()
+    rbuf = torch.empty(m, dtype=torch.complex128, device=dev)
+    wbuf = torch.empty(m, dtype=torch.float64, device=dev)
+    out3 = np.zeros(3)
+    p = M.displacement_rank
+    _ffi.check(c._lib.rplu_cauchy_plan_row(
+        c.handle, p, n, m, M.x.data_ptr(), M.y.data_ptr(), G1.data_ptr(), Bt1.data_ptr(), i,
+        rbuf.data_ptr(), wbuf.data_ptr(), None, out3.ctypes.data, stream_h))
+    a = complex(rbuf[j].item())
+    if abs(a) <= PIVOT_REL_TOL * float(out3[1]):
         raise ZeroDivisionError(f"pivot ({i}, {j}) is numerically zero")
-    c = (M.G @ M.Bt[j]) / (M.x - M.y[j])
-    G1 = M.G - torch.outer(c / a, M.G[i])
-    Bt1 = M.Bt - torch.outer(r / a, M.Bt[j])
-    return CauchyLikeMatrix(M.x, M.y, G1, None, check_points=False, _bt=Bt1.contiguous())
+    _ffi.check(c._lib.rplu_cauchy_plan_update(
+        c.handle, p, n, m, M.x.data_ptr(), M.y.data_ptr(), G1.data_ptr(), Bt1.data_ptr(), i, j,
+        rbuf.data_ptr(), None, None, stream_h))
+    return CauchyLikeMatrix(M.x, M.y, G1, None, check_points=False, _bt=Bt1)
 
 
 @dataclass

@@ -98,6 +98,40 @@ def test_generator_update_matches_dense_schur(cuda_device):
             assert np.abs(E - D).max() <= 1e-10 * np.abs(D).max()
 
 
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_generator_schur_update_k6(p, cuda_device):
+    """a11: the public single-step update runs the K6 kernels: G1, B1 equal to
+    the oracle's restatement of cauchy.py:140-154 to the last few ulps (the
+    reference's G[i] @ B and G @ B[:, j] are OpenBLAS zgemv calls whose
+    internal FMA order is not reproduced; the quotient, the Smith division
+    and the outer update follow numpy); the input generators are untouched;
+    the relative zero-pivot guard raises ZeroDivisionError."""
+
+    def close(a, b):
+        assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+    x, y, G, B = gen.c4_cauchy_like(p + 10, n=300, m=257, p=p)
+    M = rp.CauchyLikeMatrix(x, y, G, B)
+    G0, Bt0 = M.G.clone(), M.Bt.clone()
+    for (i, j) in [(0, 0), (17, 200), (299, 256)]:
+        M1 = rp.generator_schur_update(M, (i, j))
+        G1, B1 = oracle.generator_schur_update(x, y, G, B, i, j)
+        close(M1.G.cpu().numpy(), G1)
+        close(M1.Bt.cpu().numpy(), B1.T)
+    assert torch.equal(M.G, G0) and torch.equal(M.Bt, Bt0)
+    # chained: a second update on the updated generators
+    M2 = rp.generator_schur_update(rp.generator_schur_update(M, (5, 9)), (40, 3))
+    Ga, Ba = oracle.generator_schur_update(x, y, G, B, 5, 9)
+    Gb, Bb = oracle.generator_schur_update(x, y, Ga, Ba, 40, 3)
+    close(M2.G.cpu().numpy(), Gb)
+    close(M2.Bt.cpu().numpy(), Bb.T)
+    # eliminated row / column are numerically zero afterwards
+    E = M2.materialize()
+    assert np.abs(E[40]).max() <= 1e-12 * np.abs(M.materialize()).max()
+    z = rp.CauchyLikeMatrix(x[:4], y[:4], np.zeros((4, 1)) + 0j, np.ones((1, 4)) + 0j)
+    with pytest.raises(ZeroDivisionError):
+        rp.generator_schur_update(z, (1, 2))
+
+
 def test_structured_equals_dense_pivots(cuda_device):
     """With exact norms, structured RPLU picks the dense path's pivots
     (SURVEY §4 probe 2) — both sides on the GPU."""
