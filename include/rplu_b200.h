@@ -15,6 +15,9 @@
  *                    the device primitives of rplu.lowmem_cur.cur_build
  *                    (pkg/src/rplu/lowmem_cur.py:212-300) for the
  *                    Gaussian-kernel operator; the host driver sequences them
+ *   rplu_mf_run      the whole loop of rplu.lowmem_cur.cur_build on the device
+ *                    (Gaussian-kernel or dense real operator)
+ *   rplu_lu_error    the fused L.U reconstruction error (K11, FP64 tensor cores)
  *   rplu_shard_*     row-block sharded eliminate across GPUs
  *
  * Conventions
@@ -397,6 +400,52 @@ int rplu_cur_downdate(rplu_ctx* ctx, int64_t n, double* nrow, const double* g, c
 int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int64_t n, int64_t m,
                   const void* Lt, int64_t ldl, const void* U, int64_t ldu, int64_t k,
                   double* out_sq, double* kernel_ms, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Device-resident matrix-free CUR-form Alg 2 (cur_build,                    */
+/* lowmem_cur.py:212-300, with _rebuild_row_norms :204-209).                 */
+/* The whole loop runs in the library: per step the row / column draws,      */
+/* residual row and column (k-restricted generated products), the one full   */
+/* operator pass g = A l, the row-norm downdate with clamp count, the core    */
+/* extension (an O(k^2) LU update of W = A[I,J] in selection order instead   */
+/* of the reference's per-step QR) and, on > 1% clamps, the rebuild -- one    */
+/* host synchronisation per step, no host arithmetic.                        */
+
+#define RPLU_MF_GAUSS3D 1  /* A_ij = exp(-|p_i - q_j|^2 / (2 h^2)), points P (n x 3), Q (m x 3) */
+#define RPLU_MF_DENSE 2    /* real dense A (n x m row-major, lda), float64, device */
+
+typedef struct rplu_mf_args {
+  int32_t op_kind;   /* RPLU_MF_GAUSS3D | RPLU_MF_DENSE */
+  int32_t rule;      /* RPLU_RULE_RPLU (rplu-cur) | RPLU_RULE_C2PLU (c2plu-cur) */
+  int64_t n, m, rank;
+  double stop_tol;
+  const double* P;   /* device (GAUSS3D) */
+  const double* Q;   /* device (GAUSS3D) */
+  double h;          /* bandwidth (GAUSS3D) */
+  const double* A;   /* device (DENSE) */
+  int64_t lda;       /* DENSE */
+  const double* uniforms; /* host: the caller's stream, row draw then column draw per step */
+  int64_t n_uniforms;
+  void* stream;
+  int32_t flags;     /* RPLU_FLAG_TIME_KERNELS: time the full operator passes */
+  int32_t reserved;
+} rplu_mf_args;
+
+typedef struct rplu_mf_out {
+  int64_t* rows;            /* host [rank]: I in selection order */
+  int64_t* cols;            /* host [rank]: J */
+  double* total_sq_norms;   /* host [rank + 1]: sum of the maintained row norms */
+  int64_t* clamped;         /* host [rank] (optional) */
+  double* core;             /* host [rank * rank] (optional): W = A[I, J], row-major k x k */
+  double* row_norms;        /* host [n] (optional): final maintained row norms */
+  double* row_norms_dev;    /* device [n] (optional) */
+  int64_t steps_done, uniforms_consumed, near_boundary_draws, rebuilds;
+  int32_t degenerate_stop, tol_stop, core_fell_back, reserved;
+  double gemv_ms;           /* summed CUDA-event time of the full operator passes (TIME flag) */
+  int64_t kernel_launches;
+} rplu_mf_out;
+
+int rplu_mf_run(rplu_ctx* ctx, const rplu_mf_args* args, rplu_mf_out* out);
 
 /* Diagnostic: measured FP64 FMA-pipe throughput of the context's GPU
  * (TFLOP/s, best of 5), the roofline denominator of the generated-entry

@@ -65,6 +65,32 @@ class DenseOut(ctypes.Structure):
     ]
 
 
+MF_GAUSS3D = 1
+MF_DENSE = 2
+
+
+class MfArgs(ctypes.Structure):
+    _fields_ = [
+        ("op_kind", c_i32), ("rule", c_i32), ("n", c_i64), ("m", c_i64), ("rank", c_i64),
+        ("stop_tol", c_dbl), ("P", c_vp), ("Q", c_vp), ("h", c_dbl), ("A", c_vp),
+        ("lda", c_i64), ("uniforms", ctypes.POINTER(c_dbl)), ("n_uniforms", c_i64),
+        ("stream", c_vp), ("flags", c_i32), ("reserved", c_i32),
+    ]
+
+
+class MfOut(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.POINTER(c_i64)), ("cols", ctypes.POINTER(c_i64)),
+        ("total_sq_norms", ctypes.POINTER(c_dbl)), ("clamped", ctypes.POINTER(c_i64)),
+        ("core", ctypes.POINTER(c_dbl)), ("row_norms", ctypes.POINTER(c_dbl)),
+        ("row_norms_dev", c_vp),
+        ("steps_done", c_i64), ("uniforms_consumed", c_i64), ("near_boundary_draws", c_i64),
+        ("rebuilds", c_i64), ("degenerate_stop", c_i32), ("tol_stop", c_i32),
+        ("core_fell_back", c_i32), ("reserved", c_i32), ("gemv_ms", c_dbl),
+        ("kernel_launches", c_i64),
+    ]
+
+
 class CauchyArgs(ctypes.Structure):
     _fields_ = [
         ("rule", c_i32), ("p", c_i32), ("n", c_i64), ("m", c_i64), ("rank", c_i64),
@@ -154,6 +180,7 @@ SIGNATURES = {
     "rplu_cur_downdate": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
     "rplu_kernel_launch_count": (c_i64, []),
+    "rplu_mf_run": (ctypes.c_int, [c_vp, ctypes.POINTER(MfArgs), ctypes.POINTER(MfOut)]),
     "rplu_lu_error": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
                                      c_i64, c_i64, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                                      c_vp]),

@@ -217,6 +217,7 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->krylov.release();
     ctx->lu_pad.release();
     ctx->lu_part.release();
+    ctx->mf_buf.release();
     for (auto& b : ctx->scratch) b.release();
     for (auto& e : ctx->graph_exec)
       if (e) cudaGraphExecDestroy(e);
@@ -813,6 +814,13 @@ int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, cons
   if (g.rc) return g.rc;
   return cauchy_plan_update_impl(ctx, p, n, m, x, y, G, Bt, i, j, const_cast<void*>(rbuf), Cout,
                                  Rout, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_mf_run(rplu_ctx* ctx, const rplu_mf_args* args, rplu_mf_out* out) {
+  if (!ctx || !args || !out) { set_error("rplu_mf_run: NULL argument"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return mf_run_impl(ctx, args, out);
 }
 
 int rplu_lu_error(rplu_ctx* ctx, int32_t dtype, const void* A, int64_t lda, int64_t n, int64_t m,

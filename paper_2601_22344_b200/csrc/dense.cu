@@ -1872,108 +1872,33 @@ __global__ void __launch_bounds__(1024) sample_index_kernel(const double* w, lon
 // CDF association therefore differs from the single-CTA one for n above the
 // threshold (both differ from np.cumsum only within rounding of a boundary,
 // counted as near-boundary draws).
-constexpr long long kChunk = 32768;
-constexpr long long kChunkedMinN = 4 * kChunk;
-
 __global__ void __launch_bounds__(1024) sample_chunk_totals_kernel(const double* w, long long n,
                                                                    double* ctot, int* neg) {
-  constexpr int B = 1024;
-  __shared__ CdfSmem<B> sm;
-  const long long c0 = (long long)blockIdx.x * kChunk;
-  const long long nc = min(kChunk, n - c0);
-  const double* wc = w + c0;
-  bool bad = false;
-  for (long long k = threadIdx.x; k < nc; k += B) bad |= wc[k] < 0.0;
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(neg, 1);
-  auto wf = [&](long long k) { return wc[k]; };
-  Cdf<B> c = cdf_build<B>(wf, nc, sm);
-  if (threadIdx.x == 0) ctot[blockIdx.x] = c.total;
+  chunk_totals_block(w, n, ctot, neg);
 }
 
 __global__ void __launch_bounds__(1024) sample_chunked_kernel(const double* w, long long n,
                                                               double u, int mode,
                                                               const double* ctot, long long nch,
                                                               const int* neg, SampleOut* out) {
-  constexpr int B = 1024;
-  __shared__ CdfSmem<B> sm;
-  __shared__ double s_excl, s_total;
-  __shared__ long long s_owner;
+  __shared__ CdfSmem<1024> sm;
   if (*neg) {
     if (threadIdx.x == 0) { out->status = 1; out->idx = -1; out->near = 0; out->total = 0.0; }
     return;
   }
-  const double tg_in = u;
-  if (threadIdx.x == 0) {  // sequential prefix over the chunk totals
-    double e = 0.0;
-    for (long long q = 0; q < nch; ++q) e = e + ctot[q];
-    s_total = e;
-  }
-  __syncthreads();
-  const double total = s_total;
-  if (mode == 2 || !(total > 0.0)) {
-    if (threadIdx.x == 0) {
+  double total;
+  int near;
+  const long long i = chunked_draw_block(w, n, u, mode, ctot, nch, sm, &total, &near);
+  if (threadIdx.x == 0) {
+    if (mode == 2 || !(total > 0.0)) {
       out->status = (mode == 2) ? 0 : 2;
       out->idx = -1;
       out->near = 0;
-      out->total = total;
+    } else {
+      out->near = near;
+      out->idx = i;
+      out->status = 0;
     }
-    return;
-  }
-  const double tg = (mode == 1) ? tg_in : tg_in * total;
-  if (threadIdx.x == 0) {
-    double e = 0.0;
-    long long own = -1;
-    for (long long q = 0; q < nch; ++q) {
-      const double inc = e + ctot[q];
-      if (inc > tg) { own = q; break; }
-      e = inc;
-    }
-    s_owner = own;
-    s_excl = e;
-  }
-  __syncthreads();
-  long long i;
-  if (s_owner < 0) {  // target >= every partial sum: clamp to n - 1
-    i = n - 1;
-    if (threadIdx.x == 0) { sm.lo_c = total; sm.hi_c = total; }
-  } else {
-    const long long c0 = s_owner * kChunk;
-    const long long nc = min(kChunk, n - c0);
-    const double* wc = w + c0;
-    auto wf = [&](long long k) { return wc[k]; };
-    Cdf<B> c = cdf_build<B>(wf, nc, sm);
-    i = c0 + cdf_find_target<B>(wf, nc, c, tg, sm, s_excl, false);
-  }
-  __syncthreads();
-  // walk back over zero weights over the whole array (rng.py:70-73)
-  if (!(w[i] > 0.0)) {
-    long long best_lo = -1, best_any = n;
-    for (long long k = threadIdx.x; k < n; k += B) {
-      if (w[k] > 0.0) {
-        if (k <= i && k > best_lo) best_lo = k;
-        if (k < best_any) best_any = k;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      best_lo = max(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
-      best_any = min(best_any, __shfl_xor_sync(0xffffffffu, best_any, o));
-    }
-    __shared__ long long wlo[B / 32], wany[B / 32];
-    if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = best_lo; wany[threadIdx.x >> 5] = best_any; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long a = -1, b = n;
-      for (int q = 0; q < B / 32; ++q) { a = max(a, wlo[q]); b = min(b, wany[q]); }
-      sm.idx = (a >= 0) ? a : b;
-    }
-    __syncthreads();
-    i = sm.idx;
-  }
-  if (threadIdx.x == 0) {
-    const double tol = kNearBoundaryRel * total;
-    out->near = (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) ? 1 : 0;
-    out->idx = i;
-    out->status = 0;
     out->total = total;
   }
 }

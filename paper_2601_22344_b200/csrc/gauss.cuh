@@ -1,0 +1,68 @@
+// Gaussian-kernel entry evaluation shared by the CUR kernels (cur.cu) and
+// the device-resident CUR loop (mf.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace rplu {
+
+// exp(-d2) for d2 >= 0 (the kernel's exponent), table-driven.  With
+// y = -d2 * 32/ln2, k = round(y) = 32 n + j (0 <= j < 32) and s = y - k
+// (|s| <= 1/2, formed as fma(-K, d2, -k): one rounding, so the Cody-Waite
+// hi/lo reduction of a separately rounded y is not needed),
+//   exp(-d2) = 2^n * 2^(j/32) * p(s),   p(s) = sum_{i<=6} (s ln2/32)^i / i!
+// (truncation < 4e-18 relative).  2^(j/32) comes from a 32-entry table held
+// one entry per lane (fetched with a warp shuffle: no shared-memory bank
+// conflicts), 2^n is added to the table value's exponent field with integer
+// ops, k is read from the low word of the round-to-nearest shifter sum, and
+// the underflow cut (exp(-d2) < 1e-307 -> 0) is an integer compare on k —
+// so an entry costs 17 FP64-pipe operations including the distance and the
+// accumulate (the hi/lo reduction and the FP64 compare of the previous
+// variant cost 19).  A 64-entry table with a degree-5 polynomial saves one
+// more DFMA but needs two 64-bit shuffles per entry and measured 2% slower
+// (DESIGN.md §10).  Relative error ~ 1 ulp + d2 * 2^-53 (the rounding of K d2).
+// Every lane of the warp must call it (warp-synchronous shuffle).
+static __constant__ double kExp2Tab[32] = {
+    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
+    1.0905077326652577, 1.1143867425958924, 1.1387886347566916, 1.1637248587775775,
+    1.189207115002721, 1.215247359980469, 1.241857812073484, 1.2690509571917332,
+    1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
+    1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,
+    1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965,
+    1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,
+    1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002};
+
+using ExpTab = double;  // this lane's 2^(lane/32)
+
+__device__ __forceinline__ ExpTab exp2tab_lane() { return kExp2Tab[threadIdx.x & 31]; }
+
+__device__ __forceinline__ double exp_neg(double d2, ExpTab tab) {
+  const double shifter = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest
+  const double K = 46.16624130844683;          // 32 / ln2
+  const double sft = fma(d2, -K, shifter);
+  const double kd = sft - shifter;
+  const int k = __double2loint(sft);
+  const double s = fma(d2, -K, -kd);           // y - k, |s| <= 1/2
+  double p = 1.4345655584131932e-13;           // L^6/720, L = ln2/32
+  p = fma(p, s, 3.9737099845494154e-11);       // L^5/120
+  p = fma(p, s, 9.172562701824643e-09);        // L^4/24
+  p = fma(p, s, 1.6938509724371819e-06);       // L^3/6
+  p = fma(p, s, 0.00023459619820224677);       // L^2/2
+  p = fma(p, s, 0.02166084939249829);          // L
+  p = fma(p, s, 1.0);
+  const double t = __shfl_sync(0xffffffffu, tab, k & 31);
+  const double ts = __hiloint2double(__double2hiint(t) + ((k >> 5) << 20), __double2loint(t));
+  const double e = p * ts;
+  return k < -32700 ? 0.0 : e;                 // k < -32*1021.9: below 1e-307
+}
+
+// Entry from coordinates prescaled by sc = 1/(sqrt(2) h) (done once per
+// point as it is loaded into registers / shared memory), so the exponent
+// -|p-q|^2/(2h^2) is just -|p'-q'|^2.
+__device__ __forceinline__ double gauss_entry(double px, double py, double pz, double qx,
+                                              double qy, double qz, ExpTab tab) {
+  const double dx = px - qx, dy = py - qy, dz = pz - qz;
+  const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  return exp_neg(d2, tab);
+}
+
+}  // namespace rplu

@@ -390,6 +390,113 @@ __device__ long long block_argmax(const WF& wf, long long n, double* out_val) {
 }
 
 // ---------------------------------------------------------------------------
+// Large-n draws (the plan path's row / column draws over 2^20 weights, the
+// CUR row draws over 2e6): the single-CTA walk is latency bound (222 us at
+// 2^20).  Two levels instead: chunks of kChunk weights, each chunk's total
+// built by one CTA with the single-CTA CDF arithmetic (cdf_build on the
+// chunk), a sequential prefix over the chunk totals, then the single-CTA
+// search inside the owner chunk offset by the chunk's exclusive prefix.  The
+// CDF association therefore differs from the single-CTA one for n above the
+// threshold (both differ from np.cumsum only within rounding of a boundary,
+// counted as near-boundary draws).
+constexpr long long kChunk = 32768;
+constexpr long long kChunkedMinN = 4 * kChunk;
+
+// one CTA of 1024 threads per chunk (blockIdx.x = chunk): its total into
+// ctot[chunk]; *neg |= 1 on a negative weight
+__device__ __forceinline__ void chunk_totals_block(const double* w, long long n, double* ctot,
+                                                   int* neg) {
+  constexpr int B = 1024;
+  __shared__ CdfSmem<B> sm;
+  const long long c0 = (long long)blockIdx.x * kChunk;
+  const long long nc = min(kChunk, n - c0);
+  const double* wc = w + c0;
+  bool bad = false;
+  for (long long k = threadIdx.x; k < nc; k += B) bad |= wc[k] < 0.0;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(neg, 1);
+  auto wf = [&](long long k) { return wc[k]; };
+  Cdf<B> c = cdf_build<B>(wf, nc, sm);
+  if (threadIdx.x == 0) ctot[blockIdx.x] = c.total;
+}
+
+// The draw over the chunk totals (one CTA of 1024): mode 0 u * total, mode
+// 1 absolute target, mode 2 total only.  Returns the index (block-uniform;
+// meaningless when *total_out is not positive or mode == 2); *near_out = 1
+// when the target lies within 1e-12 total of a CDF boundary.
+static __device__ __noinline__ long long chunked_draw_block(const double* w, long long n, double u,
+                                                     int mode, const double* ctot,
+                                                     long long nch, CdfSmem<1024>& sm,
+                                                     double* total_out, int* near_out) {
+  constexpr int B = 1024;
+  __shared__ double s_excl, s_total;
+  __shared__ long long s_owner;
+  if (threadIdx.x == 0) {  // sequential prefix over the chunk totals
+    double e = 0.0;
+    for (long long q = 0; q < nch; ++q) e = e + ctot[q];
+    s_total = e;
+  }
+  __syncthreads();
+  const double total = s_total;
+  *total_out = total;
+  *near_out = 0;
+  if (mode == 2 || !(total > 0.0)) return -1;
+  const double tg = (mode == 1) ? u : u * total;
+  if (threadIdx.x == 0) {
+    double e = 0.0;
+    long long own = -1;
+    for (long long q = 0; q < nch; ++q) {
+      const double inc = e + ctot[q];
+      if (inc > tg) { own = q; break; }
+      e = inc;
+    }
+    s_owner = own;
+    s_excl = e;
+  }
+  __syncthreads();
+  long long i;
+  if (s_owner < 0) {  // target >= every partial sum: clamp to n - 1
+    i = n - 1;
+    if (threadIdx.x == 0) { sm.lo_c = total; sm.hi_c = total; }
+  } else {
+    const long long c0 = s_owner * kChunk;
+    const long long nc = min(kChunk, n - c0);
+    const double* wc = w + c0;
+    auto wf = [&](long long k) { return wc[k]; };
+    Cdf<B> c = cdf_build<B>(wf, nc, sm);
+    i = c0 + cdf_find_target<B>(wf, nc, c, tg, sm, s_excl, false);
+  }
+  __syncthreads();
+  // walk back over zero weights over the whole array (rng.py:70-73)
+  if (!(w[i] > 0.0)) {
+    long long best_lo = -1, best_any = n;
+    for (long long k = threadIdx.x; k < n; k += B) {
+      if (w[k] > 0.0) {
+        if (k <= i && k > best_lo) best_lo = k;
+        if (k < best_any) best_any = k;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      best_lo = max(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
+      best_any = min(best_any, __shfl_xor_sync(0xffffffffu, best_any, o));
+    }
+    __shared__ long long wlo[B / 32], wany[B / 32];
+    if ((threadIdx.x & 31) == 0) { wlo[threadIdx.x >> 5] = best_lo; wany[threadIdx.x >> 5] = best_any; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long a = -1, b = n;
+      for (int q = 0; q < B / 32; ++q) { a = max(a, wlo[q]); b = min(b, wany[q]); }
+      sm.idx = (a >= 0) ? a : b;
+    }
+    __syncthreads();
+    i = sm.idx;
+  }
+  const double tol = kNearBoundaryRel * total;
+  *near_out = (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) ? 1 : 0;
+  __syncthreads();
+  return i;
+}
+
+// ---------------------------------------------------------------------------
 // Grid-wide synchronisation for the persistent (cooperative) loops.
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
   unsigned v;

@@ -115,6 +115,7 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int
 int cuda_fail(cudaError_t e, const char* where);
 
 int dmma_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
+int mf_run_impl(rplu_ctx* ctx, const rplu_mf_args* a, rplu_mf_out* out);
 
 // K11 fused ||A - X Y||_F^2, ||A||_F^2 (lu_error.cu); out_sq host[2]
 int lu_error_impl(rplu_ctx* ctx, int dtype, const void* A, long long lda, long long n,
@@ -167,4 +168,5 @@ struct rplu_ctx {
   rplu::DevBuf krylov;      // MGS Arnoldi: per-CTA partials + grid barrier
   rplu::DevBuf lu_pad;      // K11: zero-padded fp64 factor panels
   rplu::DevBuf lu_part;     // K11: per-CTA partial sums
+  rplu::DevBuf mf_buf;      // rplu_mf_run workspace (vectors, core factors, histories)
 };

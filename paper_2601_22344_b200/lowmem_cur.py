@@ -77,6 +77,25 @@ class CurFactorization:
                                                 upper=True)[:, 0]
         return out if dev_in else out.cpu().numpy()
 
+    @classmethod
+    def from_core(cls, rows, cols, W, mode="qr", fell_back=False):
+        """A factorization of a core A[I, J] built by the device loop: the
+        reference's representation (QR of W, or W^{-1} in inverse mode)
+        computed once instead of at every extension."""
+        f = cls(mode=mode, device=W.device, dtype=W.dtype)
+        f.row_indices = [int(i) for i in rows]
+        f.col_indices = [int(j) for j in cols]
+        f._W = W
+        f.fell_back = bool(fell_back)
+        if fell_back:
+            f.mode = "qr"
+        if len(f.row_indices):
+            if f.mode == "inverse":
+                f._U = torch.linalg.inv(W)
+            else:
+                f._Q, f._R = torch.linalg.qr(W)
+        return f
+
     def core_solve(self, v):
         """Solve A[I, J] x = v."""
         return self._solve(v, False)
@@ -246,6 +265,90 @@ def cur_build(A, rule, rank, stop_tol=0.0, rng=None, core_mode="qr", *, time_gem
     n, m = op.shape
     if not 0 <= rank <= min(n, m):
         raise ValueError(f"rank {rank} out of range [0, {min(n, m)}]")
+    if core_mode not in ("qr", "inverse"):
+        raise ValueError(f"unknown core mode {core_mode!r}")
+    if not torch.is_complex(torch.empty(0, dtype=op.dtype)) and rank <= 8192:
+        return _cur_build_device(op, rule, rank, stop_tol, rng, core_mode, time_gemv)
+    return _cur_build_torch(op, rule, rank, stop_tol, rng, core_mode, time_gemv)
+
+
+def _cur_build_device(op, rule, rank, stop_tol, rng, core_mode, time_gemv):
+    """The whole loop in ``rplu_mf_run`` (csrc/mf.cu): one host
+    synchronisation per step, device draws, device core (LU in selection
+    order), device rebuild.  Real operators: the Gaussian kernel and real
+    dense matrices."""
+    import ctypes
+
+    from . import _device, _ffi
+    from .operators import _GaussDeviceOp
+    n, m = op.shape
+    dev = op.device
+    info = CurBuildInfo()
+    stream = _Stream(rng if rule == "rplu-cur" else None, 3 * max(rank, 1))
+    if isinstance(op, _GaussDeviceOp):
+        g = op.g
+        kind, P, Q, h, Ad, lda = _ffi.MF_GAUSS3D, g.P.data_ptr(), g.Q.data_ptr(), g.h, None, 0
+        keep = (g.P, g.Q)
+    else:
+        At = op.t.to(torch.float64)
+        if At.stride(1) != 1:
+            At = At.contiguous()
+        kind, P, Q, h, Ad, lda = _ffi.MF_DENSE, None, None, 0.0, At.data_ptr(), At.stride(0)
+        keep = (At,)
+    k1 = max(rank, 1)
+    rows = np.zeros(k1, dtype=np.int64)
+    cols = np.zeros(k1, dtype=np.int64)
+    totals = np.zeros(rank + 1)
+    clamped = np.zeros(k1, dtype=np.int64)
+    core = np.zeros(k1 * k1)
+    nrow = torch.empty(n, dtype=torch.float64, device=dev)
+    uni = stream.block.values if stream.block is not None else None
+    args = _ffi.MfArgs(
+        op_kind=kind, rule=_ffi.RULE_IDS["rplu" if rule == "rplu-cur" else "c2plu"], n=n, m=m,
+        rank=rank, stop_tol=float(stop_tol), P=P, Q=Q, h=h, A=Ad, lda=lda,
+        uniforms=uni.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if uni is not None else None,
+        n_uniforms=uni.size if uni is not None else 0,
+        stream=torch.cuda.current_stream(dev).cuda_stream,
+        flags=_ffi.FLAG_TIME_KERNELS if time_gemv else 0)
+    out = _ffi.MfOut(rows=rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                     cols=cols.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                     total_sq_norms=totals.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                     clamped=clamped.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                     core=core.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                     row_norms_dev=nrow.data_ptr())
+    c = _device.ctx(dev)
+    try:
+        status = c._lib.rplu_mf_run(c.handle, ctypes.byref(args), ctypes.byref(out))
+        stream.used = int(out.uniforms_consumed)
+    finally:
+        stream.commit()
+    del keep
+    _ffi.check(status)
+    k = int(out.steps_done)
+    W = torch.from_numpy(core[:k * k].reshape(k, k).copy()).to(dev)
+    if core_mode == "inverse" and out.core_fell_back:
+        warnings.warn("degenerate pivot complement in block-inverse update; core fell back to QR",
+                      stacklevel=3)
+    fact = CurFactorization.from_core(rows[:k], cols[:k], W, mode=core_mode,
+                                      fell_back=core_mode == "inverse" and bool(out.core_fell_back))
+    info.total_sq_norms = [float(x) for x in totals[:k + 1]]
+    info.clamped = [int(x) for x in clamped[:k]]
+    info.rebuilds = int(out.rebuilds)
+    info.degenerate_stop = bool(out.degenerate_stop)
+    info.tol_stop = bool(out.tol_stop)
+    info.row_norms = nrow.cpu().numpy()
+    info.near_boundary_draws = int(out.near_boundary_draws)
+    info.uniforms_consumed = int(out.uniforms_consumed)
+    info.kernel_launches = int(out.kernel_launches)
+    if time_gemv and k:
+        info.gemv_ms = [float(out.gemv_ms) / k] * k
+    return fact, info
+
+
+def _cur_build_torch(op, rule, rank, stop_tol, rng, core_mode, time_gemv):
+    """Complex operators (a complex DenseMatrix): the same loop driven from
+    Python over torch / cuBLAS device ops and the K2 draw kernel."""
+    n, m = op.shape
     dev = op.device
     info = CurBuildInfo()
     fact = CurFactorization(mode=core_mode, device=dev, dtype=op.dtype)

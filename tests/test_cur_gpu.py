@@ -156,3 +156,87 @@ def test_c5_full_size_step(cuda_device):
     fact, info = rp.cur_build(op, "rplu-cur", 2, rng=rp.RngState(0))
     assert info.total_sq_norms[-1] < info.total_sq_norms[0]
     assert len(set(fact.row_indices)) == 2
+
+
+def _exact_residual_row_norms(A, I, J):
+    """||row_t(A - A[:,J] A[I,J]^{-1} A[I,:])||^2 on the host (the quantity
+    the maintained norms track and a rebuild recomputes)."""
+    if not I:
+        return (A * A).sum(1)
+    M = np.linalg.solve(A[np.ix_(I, J)], A[I, :])
+    R = A - A[:, J] @ M
+    return (R * R).sum(1)
+
+
+@pytest.mark.parametrize("kind", ["dense", "gauss"])
+def test_device_loop_rebuilds(kind, cuda_device):
+    """rplu_mf_run's rebuild path (lowmem_cur.py:290-292): on inputs whose
+    downdated norms clamp on > 1% of the rows the device loop rebuilds n_row
+    from the m residual columns; index sets equal the oracle's (divergence
+    only near a CDF boundary) and the final maintained norms equal the exact
+    residual row norms of the skeleton."""
+    if kind == "dense":
+        rs = np.random.default_rng(0)
+        U, _ = np.linalg.qr(rs.standard_normal((60, 60)))
+        V, _ = np.linalg.qr(rs.standard_normal((60, 60)))
+        A = (U * 0.5 ** np.arange(60)) @ V.T
+        host, dev_op, k, seed = oracle.DenseHost(A), rp.DenseMatrix(A), 12, 0
+    else:
+        P, Q = gen.c5_points(3, n=60, m=50)
+        host = oracle.GaussianKernelHost(P, Q, h=0.5)
+        A = host.materialize()
+        dev_op, k, seed = rp.GaussianKernelOperator(P, Q, h=0.5), 20, 3
+    core, ref = oracle.cur_build(host, "rplu-cur", k, seed=seed, margins=True)
+    fact, info = rp.cur_build(dev_op, "rplu-cur", k, rng=rp.RngState(seed))
+    assert info.rebuilds >= 1 and ref["rebuilds"] >= 1
+    got = list(zip(fact.row_indices, fact.col_indices))
+    want = list(zip(core.I, core.J))
+    t = next((s for s, (a, b) in enumerate(zip(got, want)) if a != b), None)
+    if t is not None:
+        assert min(ref["margins"][2 * t:2 * t + 2]) <= oracle.NEAR_REL, t
+    kk = len(got) if t is None else t
+    np.testing.assert_allclose(info.total_sq_norms[:kk + 1], ref["total_sq_norms"][:kk + 1],
+                               rtol=1e-8, atol=1e-13 * ref["total_sq_norms"][0])
+    exact = _exact_residual_row_norms(A, list(fact.row_indices), list(fact.col_indices))
+    assert np.abs(info.row_norms - exact).max() <= 1e-9 * ref["total_sq_norms"][0]
+
+
+def test_device_loop_launch_budget_and_core(cuda_device):
+    """The device loop returns the core W = A[I, J] exactly (entries are
+    operator entries), its QR solves like the reference's, and the per-step
+    host work is one synchronisation (kernel_launches reported)."""
+    P, Q = gen.c5_points(5, n=3000, m=2500)
+    op = rp.GaussianKernelOperator(P, Q)
+    fact, info = rp.cur_build(op, "rplu-cur", 40, rng=rp.RngState(5))
+    A_IJ = np.array([[op.entry(i, j).real for j in fact.col_indices] for i in fact.row_indices])
+    # kernel exp vs the accessor's entry: equal to the last couple of ulps
+    np.testing.assert_allclose(fact.core_matrix(), A_IJ, rtol=1e-13, atol=0)
+    v = np.random.default_rng(0).standard_normal(40)
+    np.testing.assert_allclose(fact.core_solve(v), np.linalg.solve(A_IJ, v), rtol=1e-8)
+    assert info.kernel_launches > 0 and info.uniforms_consumed == 80
+
+
+def test_device_loop_stops_and_greedy(cuda_device):
+    """tol stop, degenerate stop on an exactly low-rank dense input, the
+    zero matrix, c2plu-cur, rank 0 -- against the oracle."""
+    rs = np.random.default_rng(2)
+    A = rs.standard_normal((80, 3)) @ rs.standard_normal((3, 70))
+    core, ref = oracle.cur_build(oracle.DenseHost(A), "rplu-cur", 10, seed=4)
+    fact, info = rp.cur_build(rp.DenseMatrix(A), "rplu-cur", 10, rng=rp.RngState(4))
+    assert info.degenerate_stop == ref["degenerate_stop"] and fact.rank == len(core.I)
+    assert list(fact.row_indices) == core.I[:fact.rank]
+    rs = np.random.default_rng(7)
+    B = rs.standard_normal((200, 5)) @ rs.standard_normal((5, 150)) + \
+        1e-6 * rs.standard_normal((200, 150))
+    core, ref = oracle.cur_build(oracle.DenseHost(B), "rplu-cur", 60, seed=1, stop_tol=1e-3)
+    fact, info = rp.cur_build(rp.DenseMatrix(B), "rplu-cur", 60, rng=rp.RngState(1),
+                              stop_tol=1e-3)
+    assert info.tol_stop and ref["tol_stop"] and fact.rank == len(core.I) == 5
+    core, ref = oracle.cur_build(oracle.DenseHost(B), "c2plu-cur", 20)
+    fact, info = rp.cur_build(rp.DenseMatrix(B), "c2plu-cur", 20)
+    assert list(fact.row_indices) == core.I and list(fact.col_indices) == core.J
+    fact, info = rp.cur_build(rp.DenseMatrix(np.zeros((5, 4))), "rplu-cur", 2,
+                              rng=rp.RngState(0))
+    assert info.degenerate_stop and fact.rank == 0
+    fact, info = rp.cur_build(rp.DenseMatrix(B), "rplu-cur", 0, rng=rp.RngState(0))
+    assert fact.rank == 0 and len(info.total_sq_norms) == 1
