@@ -18,6 +18,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "rplu_common.cuh"
@@ -175,12 +176,25 @@ __global__ void __launch_bounds__(256) cur_downdate_kernel(long long n, double* 
 // ---------------------------------------------------------------------------
 // host launchers
 
-static int gemv_splits(long long n, long long m, int rows_per_cta, int sms) {
-  long long rb = (n + rows_per_cta - 1) / rows_per_cta;
-  long long s = (4LL * sms + rb - 1) / rb;
-  long long max_s = (m + 511) / 512;
-  s = std::max(1LL, std::min(s, max_s));
-  return (int)std::min(s, 1024LL);
+// Column splits of K7: at least ~4 CTAs per SM in total, at least 512
+// columns per split, and -- since every CTA of one launch runs about equally
+// long -- a CTA count that fills its last wave: among the admissible split
+// counts take the one with the smallest wave-quantisation loss
+// ceil(ctas / slots) / (ctas / slots) (C5: 1954 row blocks on 740 resident
+// slots is 2.64 waves with 1 split, 7.92 with 3 splits).
+static int gemv_splits(long long n, long long m, int rows_per_cta, int sms, int per_sm) {
+  const long long rb = (n + rows_per_cta - 1) / rows_per_cta;
+  const long long max_s = std::max(1LL, std::min((m + 511) / 512, 1024LL));
+  long long s0 = std::max(1LL, std::min((4LL * sms + rb - 1) / rb, max_s));
+  const double slots = (double)sms * std::max(per_sm, 1);
+  long long best = s0;
+  double best_eff = 0.0;
+  for (long long s = s0; s <= std::min(max_s, s0 + 8); ++s) {
+    const double waves = (double)(rb * s) / slots;
+    const double eff = waves / std::ceil(waves);
+    if (eff > best_eff + 0.01) { best_eff = eff; best = s; }
+  }
+  return (int)best;
 }
 
 template <int RPT>
@@ -205,7 +219,19 @@ static int gemv_rpt() {
 int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
                     cudaStream_t s, float* ms) {
   const int rpt = gemv_rpt();
-  const int splits = gemv_splits(op.n, op.m, 256 * rpt, ctx->sm_count);
+  static int per_sm[3] = {0, 0, 0};   // resident CTAs per SM of each RPT instantiation
+  const int slot = rpt == 1 ? 0 : (rpt == 2 ? 1 : 2);
+  if (!per_sm[slot]) {
+    int b = 0;
+    if (rpt == 1)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<1, 256, false>, 256, 0);
+    else if (rpt == 2)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<2, 256, false>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<4, 256, false>, 256, 0);
+    per_sm[slot] = b > 0 ? b : 1;
+  }
+  const int splits = gemv_splits(op.n, op.m, 256 * rpt, ctx->sm_count, per_sm[slot]);
   int rc;
   if ((rc = ctx->scratch[4].ensure(sizeof(double) * (size_t)splits * op.n))) return rc;
   double* part = reinterpret_cast<double*>(ctx->scratch[4].ptr);

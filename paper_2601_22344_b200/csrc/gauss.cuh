@@ -9,17 +9,19 @@ namespace rplu {
 // y = -d2 * 32/ln2, k = round(y) = 32 n + j (0 <= j < 32) and s = y - k
 // (|s| <= 1/2, formed as fma(-K, d2, -k): one rounding, so the Cody-Waite
 // hi/lo reduction of a separately rounded y is not needed),
-//   exp(-d2) = 2^n * 2^(j/32) * p(s),   p(s) = sum_{i<=6} (s ln2/32)^i / i!
-// (truncation < 4e-18 relative).  2^(j/32) comes from a 32-entry table held
+//   exp(-d2) = 2^n * 2^(j/32) * p(s),   p(s) ~ exp(s ln2/32) of degree 5
+// (a relative least-squares fit; 2.5e-16 max relative error).  2^(j/32) comes from a 32-entry table held
 // one entry per lane (fetched with a warp shuffle: no shared-memory bank
 // conflicts), 2^n is added to the table value's exponent field with integer
 // ops, k is read from the low word of the round-to-nearest shifter sum, and
 // the underflow cut (exp(-d2) < 1e-307 -> 0) is an integer compare on k —
-// so an entry costs 17 FP64-pipe operations including the distance and the
-// accumulate (the hi/lo reduction and the FP64 compare of the previous
-// variant cost 19).  A 64-entry table with a degree-5 polynomial saves one
-// more DFMA but needs two 64-bit shuffles per entry and measured 2% slower
-// (DESIGN.md §10).  Relative error ~ 1 ulp + d2 * 2^-53 (the rounding of K d2).
+// so an entry costs 16 FP64-pipe operations including the distance and the
+// accumulate (the hi/lo reduction and the FP64 compare of an earlier
+// variant cost 19, the degree-6 Taylor polynomial 17).  A 64-entry table
+// with a degree-4 polynomial would save one more DFMA but needs two 64-bit
+// shuffles per entry (a 64-entry / degree-5 variant measured 2% slower,
+// DESIGN.md §10).  Relative error ~ 1.5 ulp + d2 * 2^-53 (the rounding of
+// K d2).
 // Every lane of the warp must call it (warp-synchronous shuffle).
 static __constant__ double kExp2Tab[32] = {
     1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
@@ -42,12 +44,15 @@ __device__ __forceinline__ double exp_neg(double d2, ExpTab tab) {
   const double kd = sft - shifter;
   const int k = __double2loint(sft);
   const double s = fma(d2, -K, -kd);           // y - k, |s| <= 1/2
-  double p = 1.4345655584131932e-13;           // L^6/720, L = ln2/32
-  p = fma(p, s, 3.9737099845494154e-11);       // L^5/120
-  p = fma(p, s, 9.172562701824643e-09);        // L^4/24
-  p = fma(p, s, 1.6938509724371819e-06);       // L^3/6
-  p = fma(p, s, 0.00023459619820224677);       // L^2/2
-  p = fma(p, s, 0.02166084939249829);          // L
+  // degree-5 fit of exp(s ln2/32) on |s| <= 1/2 (relative least squares at
+  // Chebyshev nodes, extended precision): 2.5e-16 max / 0.36 ulp mean
+  // relative error in FMA Horner, against 0.51 ulp for the degree-6 Taylor
+  // polynomial -- one DFMA less per entry
+  double p = 3.9736907164886624e-11;
+  p = fma(p, s, 9.172616497450463e-09);
+  p = fma(p, s, 1.6938509725336998e-06);
+  p = fma(p, s, 0.00023459619819720352);
+  p = fma(p, s, 0.021660849392498283);
   p = fma(p, s, 1.0);
   const double t = __shfl_sync(0xffffffffu, tab, k & 31);
   const double ts = __hiloint2double(__double2hiint(t) + ((k >> 5) << 20), __double2loint(t));
