@@ -9,7 +9,8 @@ One bench "step" = one full RPLU run of `rank` pivot steps on the resident
 input (eliminate(): copy A into the residual buffer, then the device loop).
 value = pivot steps / s over the K timed runs (inputs in HBM, CUDA events);
 e2e   = the same metric through the public drop-in call with HOST buffers
-        (pinned numpy A in, numpy L/U/pivots out, copies inside the region).
+        (a plain pageable numpy A in, numpy L/U/pivots out, copies inside the
+        region; the pinned-input figure is reported beside it).
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                 [--config c3f64|c3f32|c1] [--n N] [--rank R]
@@ -370,7 +371,8 @@ def run_cur_arm(args, cfg):
     k = fact.rank
     value = args.steps * k / (total_ms / 1e3)
     evals = float(n) * n
-    avg_s = sum(gemv) / len(gemv) / 1e3
+    # every K7 launch of the run (row norms + one per step) over its launches
+    avg_s = sum(gemv) / (len(gemv) + args.steps) / 1e3
     flops_per_eval = 13.0   # 3 sub, 3 mul/fma (d^2), 1 scale, 1 exp, 2 (accumulate)... see DESIGN.md
     achieved = evals * flops_per_eval / avg_s / 1e12
     peak = _ffi.fp64_peak_tflops(0)
@@ -899,7 +901,22 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    e2e_pinned_value = e2e_runs * tr_h.steps / (e2e_ms / 1e3)
+    e2e_pinned_ms = e2e_ms
+    # the headline e2e: a plain pageable numpy array, as the reference's
+    # callers pass (staged through the library's pinned ring, rplu_upload)
+    A_page = np.array(A_host)                  # pageable, pages touched here
+    rp.eliminate(A_page, rp.PivotRule("rplu", rp.RngState(seed)), rank, compute_dtype=tdtype)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(e2e_runs):
+        tr_h = rp.eliminate(A_page, rp.PivotRule("rplu", rp.RngState(seed)), rank,
+                            compute_dtype=tdtype)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
     e2e_value = e2e_runs * tr_h.steps / (e2e_ms / 1e3)
+    del A_page
     h2d = n * n * esize
     d2h = tr_h.L.nbytes + tr_h.U.nbytes + 16 * tr_h.steps + 8 * (tr_h.steps + 1)
     same = tr_h.pivots == tr.pivots
@@ -942,12 +959,54 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
                                    f"{cores} threads; CPU: {model}"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "runs": e2e_runs, "ms_per_run": e2e_ms / e2e_runs,
+                "input": "pageable numpy array (plain np.array, as a reference caller)",
+                "pinned_input_value": e2e_pinned_value,
+                "pinned_input_ms_per_run": e2e_pinned_ms / e2e_runs,
                 "pivots_match_device_run": same},
         "gpu_launches": launches,
         "near_boundary_draws": tr.near_boundary_draws,
         "clocks": clk,
     }
+    if cfg.get("kind") == "c1":
+        # C1 is launch/latency bound (the residual lives in shared memory for
+        # the whole run): no HBM roofline applies; report the resident
+        # kernel's per-phase time instead (CTA 0 timestamps, separate run)
+        line["roofline"] = {"bound": "latency", "achieved": None, "peak": None, "unit": "us/step",
+                            "frac": None, "traffic": None,
+                            "kernel": "dense_resident_kernel (one cooperative launch, R in SMEM)",
+                            "us_per_pivot_step": 1e3 * total_ms / (args.steps * reps * pivots_done),
+                            "phases_us_per_step": _resident_phases(n, rank, seed)}
     print(json.dumps(line), flush=True)
+
+
+def _resident_phases(n, rank, seed):
+    """Per-phase microseconds of the C1 resident loop (RPLU_PERSIST_TRACE=1:
+    CTA 0's globaltimer stamps), from a child process (the trace switch is
+    read once per process)."""
+    code = ("import sys; sys.path.insert(0, %r); import torch; import paper_2601_22344_b200 as rp;"
+            "from paper_2601_22344_b200 import gen;"
+            "A = torch.from_numpy(gen.c1_dense(%d, n=%d)).cuda();"
+            "[rp.eliminate(A, rp.PivotRule('rplu', rp.RngState(%d)), %d) for _ in range(3)];"
+            "torch.cuda.synchronize()") % (REPO, seed, n, seed, rank)
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           timeout=300, env=dict(os.environ, RPLU_PERSIST_TRACE="1"))
+        lines = [x for x in r.stderr.splitlines() if "resident loop" in x]
+        toks = lines[-1].split("):", 1)[1].split()
+        out, k = {}, 0
+        while k + 1 < len(toks):       # "row cdf 1.40 row find 2.0 ..." -> names with spaces
+            j = k
+            while j < len(toks):
+                try:
+                    val = float(toks[j])
+                    break
+                except ValueError:
+                    j += 1
+            out[" ".join(toks[k:j])] = val
+            k = j + 1
+        return out
+    except Exception as exc:  # diagnostics only
+        return {"error": str(exc)[:200]}
 
 
 def main():

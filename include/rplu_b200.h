@@ -63,6 +63,11 @@ extern "C" {
                                     default: delayed updates when R exceeds L2 */
 #define RPLU_FLAG_STEPWISE 16   /* dense: per-step launches even where the whole loop would run
                                     as one persistent cooperative launch */
+#define RPLU_FLAG_EXACT 32      /* dense delayed-update loop: apply the pending rank-1 terms
+                                    with the reference's rounding (multiply, then subtract:
+                                    bit-identical to the eager loop and to the reference's
+                                    arithmetic); default: one FMA per term (L/U agree to
+                                    rounding, half the FP64 work, longer flush interval) */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0
@@ -446,6 +451,14 @@ typedef struct rplu_mf_out {
 } rplu_mf_out;
 
 int rplu_mf_run(rplu_ctx* ctx, const rplu_mf_args* args, rplu_mf_out* out);
+
+/* Copy `bytes` from a pageable host buffer to device memory through the
+ * context's ring of page-locked slots (`threads` host threads fill a slot
+ * while the previous one is in flight).  Ordered on `stream`; the source is
+ * no longer read on return.  The Python layer uses it for numpy inputs (the
+ * reference's callers pass plain arrays, dense_pivots.py:86-89). */
+int rplu_upload(rplu_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t threads,
+                void* stream);
 
 /* Diagnostic: measured FP64 FMA-pipe throughput of the context's GPU
  * (TFLOP/s, best of 5), the roofline denominator of the generated-entry

@@ -81,7 +81,28 @@ def as_device_matrix(A, dtype=None, device=None, copy=True):
     np_want = {torch.float32: np.float32, torch.float64: np.float64,
                torch.complex128: np.complex128}[want]
     a = np.ascontiguousarray(a, dtype=np_want)
-    return torch.from_numpy(a).to(dev)
+    return upload(a, dev)
+
+
+_UPLOAD_MIN_BYTES = 16 << 20
+
+
+def upload(a, dev):
+    """Contiguous numpy array -> new CUDA tensor.  Large pageable arrays go
+    through the library's pinned staging ring (rplu_upload: multi-threaded
+    host copies overlapped with the DMA); a torch pinned tensor's numpy
+    view and small arrays use a plain copy."""
+    t = torch.from_numpy(a)
+    if a.nbytes < _UPLOAD_MIN_BYTES or t.is_pinned():
+        return t.to(dev, non_blocking=t.is_pinned())
+    out = torch.empty(a.shape, dtype=t.dtype, device=dev)
+    c = ctx(dev)
+    import os
+    threads = max(1, min(8, len(os.sched_getaffinity(0))))
+    _ffi.check(c._lib.rplu_upload(c.handle, ctypes.c_void_p(out.data_ptr()),
+                                  ctypes.c_void_p(a.ctypes.data), a.nbytes, threads,
+                                  stream_handle(dev)))
+    return out
 
 
 def real_if_zero_imag(a):

@@ -35,6 +35,7 @@ FLAG_NO_GRAPH = 2
 FLAG_LAZY = 4
 FLAG_EAGER = 8
 FLAG_STEPWISE = 16
+FLAG_EXACT = 32
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -181,6 +182,7 @@ SIGNATURES = {
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), c_vp]),
     "rplu_kernel_launch_count": (c_i64, []),
     "rplu_mf_run": (ctypes.c_int, [c_vp, ctypes.POINTER(MfArgs), ctypes.POINTER(MfOut)]),
+    "rplu_upload": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "rplu_lu_error": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
                                      c_i64, c_i64, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                                      c_vp]),

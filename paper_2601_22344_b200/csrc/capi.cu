@@ -218,6 +218,9 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->lu_pad.release();
     ctx->lu_part.release();
     ctx->mf_buf.release();
+    if (ctx->ring) cudaFreeHost(ctx->ring);
+    for (auto& e : ctx->ring_ev)
+      if (e) cudaEventDestroy(e);
     for (auto& b : ctx->scratch) b.release();
     for (auto& e : ctx->graph_exec)
       if (e) cudaGraphExecDestroy(e);
@@ -814,6 +817,14 @@ int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, cons
   if (g.rc) return g.rc;
   return cauchy_plan_update_impl(ctx, p, n, m, x, y, G, Bt, i, j, const_cast<void*>(rbuf), Cout,
                                  Rout, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rplu_upload(rplu_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t threads,
+                void* stream) {
+  if (!ctx) { set_error("rplu_upload: NULL context"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return upload_impl(ctx, dst, src, bytes, threads, static_cast<cudaStream_t>(stream));
 }
 
 int rplu_mf_run(rplu_ctx* ctx, const rplu_mf_args* args, rplu_mf_out* out) {

@@ -51,7 +51,28 @@ struct DenseParams {
   long long t0;
   int lazy;
   int force;  // run the pass even after a stop (final flush)
+  int fused;  // delayed updates: one FMA per pending term (default) instead of
+              // the reference's multiply-then-subtract (bit-identical to eager)
 };
+
+// One pending term of the delayed-update loop, R -= L_s U_s at one element:
+// fused, one rounding per term (the FP64 pipe does half the work of the
+// reference's multiply + subtract, so more terms fit under the HBM time);
+// complex128 as numpy's product components, each with fused accumulations.
+template <typename T> __device__ __forceinline__ T pend_fused(T x, T l, T u);
+template <> __device__ __forceinline__ double pend_fused<double>(double x, double l, double u) {
+  return fma(-l, u, x);
+}
+template <> __device__ __forceinline__ float pend_fused<float>(float x, float l, float u) {
+  return fmaf(-l, u, x);
+}
+template <> __device__ __forceinline__ double2 pend_fused<double2>(double2 x, double2 l, double2 u) {
+  return make_double2(fma(-l.x, u.x, fma(l.y, u.y, x.x)), fma(-l.x, u.y, fma(-l.y, u.x, x.y)));
+}
+template <typename T>
+__device__ __forceinline__ T pend_sub(bool fused, T x, T l, T u) {
+  return fused ? pend_fused<T>(x, l, u) : Scalar<T>::sub_outer(x, l, u);
+}
 
 template <typename T, int VEC>
 struct alignas(sizeof(T) * VEC) VecT {
@@ -419,7 +440,7 @@ __global__ void __launch_bounds__(256) lazy_row_kernel(DenseParams p) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < p.m;
        k += (long long)gridDim.x * blockDim.x) {
     T x = R[i * p.ld + k];
-    for (int s = 0; s < q; ++s) x = S::sub_outer(x, s_l[s], U[s * p.ldu + k]);
+    for (int s = 0; s < q; ++s) x = pend_sub<T>(p.fused, x, s_l[s], U[s * p.ldu + k]);
     urow[k] = x;
   }
 }
@@ -457,7 +478,8 @@ __global__ void __launch_bounds__(1024) lazy_select_col_kernel(DenseParams p) {
       const T* U = reinterpret_cast<const T*>(p.U);
       for (long long k = threadIdx.x; k < m; k += B) {
         T x = R[i * p.ld + k];
-        for (long long s = p.t0; s < t; ++s) x = S::sub_outer(x, Lt[s * n + i], U[s * p.ldu + k]);
+        for (long long s = p.t0; s < t; ++s)
+          x = pend_sub<T>(p.fused, x, Lt[s * n + i], U[s * p.ldu + k]);
         urow[k] = x;
       }
       __syncthreads();
@@ -535,7 +557,7 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
       if (s < q) ll[s] = Lt[(p.t0 + s) * n + k];
 #pragma unroll
     for (int s = 0; s < kLazyMaxBlock; ++s)
-      if (s < q) x = S::sub_outer(x, ll[s], s_upiv[s]);
+      if (s < q) x = pend_sub<T>(p.fused, x, ll[s], s_upiv[s]);
     Lt[t * n + k] = S::scale(x, cf);
   }
 }
@@ -639,7 +661,7 @@ struct LazyTma {
 // complex128, 4-byte for fp32), box = 1 KB x 32 rows; tmU: the pending rows
 // U[t0 .. t0+QC) with box 1 KB x QC rows.  Out-of-range rows and columns are
 // zero-filled by the TMA unit, so every stage carries (32 + QC) KB.
-template <typename T, int VEC, bool FLUSH, int QC, int TXW = 64>
+template <typename T, int VEC, bool FLUSH, int QC, int TXW = 64, bool FUSED = false>
 __global__ void __launch_bounds__(288, 1)
     lazy_pass4_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmR,
                       const __grid_constant__ CUtensorMap tmU) {
@@ -767,7 +789,9 @@ __global__ void __launch_bounds__(288, 1)
           for (int r = 0; r < RPT; ++r) {
             const T lv = L[s * ROWS + ty * RPT + r];
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+            for (int e = 0; e < VEC; ++e)
+              rv[r].v[e] = FUSED ? pend_fused<T>(rv[r].v[e], lv, u.v[e])
+                                 : S::sub_outer(rv[r].v[e], lv, u.v[e]);
           }
         }
         if constexpr (FLUSH) {
@@ -914,7 +938,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
         for (int r = 0; r < RPT; ++r) {
           const T lv = sm.Ls[s][ty * RPT + r];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) rv[r].v[e] = S::sub_outer(rv[r].v[e], lv, u.v[e]);
+          for (int e = 0; e < VEC; ++e) rv[r].v[e] = pend_sub<T>(p.fused, rv[r].v[e], lv, u.v[e]);
         }
       };
       if constexpr (QC > 0) {
@@ -938,7 +962,7 @@ __global__ void __launch_bounds__(256) lazy_pass3_kernel(DenseParams p) {
     for (int r = 0; r < RPT; ++r) {
       if (r < nr) {
         T x = R[(myrow0 + r) * ld + l];
-        for (int s = 0; s < q; ++s) x = S::sub_outer(x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
+        for (int s = 0; s < q; ++s) x = pend_sub<T>(p.fused, x, sm.Ls[s][ty * RPT + r], U[s * p.ldu + l]);
         acc[r] += S::mass(x);
         if (FLUSH) R[(myrow0 + r) * ld + l] = x;
       }
@@ -1372,13 +1396,13 @@ static bool make_row_map(CUtensorMap* map, const void* base, int esize, long lon
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, bool FLUSH, int QC, int TXW>
+template <typename T, bool FLUSH, int QC, int TXW, bool FUSED>
 static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   using C = LazyTma<T, QC, TXW>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW>,
+    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
@@ -1392,7 +1416,7 @@ static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
     set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
     return RPLU_ERR_CUDA;
   }
-  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
+  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
   return RPLU_OK;
 }
 
@@ -1400,7 +1424,8 @@ static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
 // 1 KB at C3 fp64: 623 vs 627 steps/s at b = 6)
 template <typename T, bool FLUSH, int QC>
 static int launch_lazy_pass4_q(const DenseParams& p, cudaStream_t s) {
-  return launch_lazy_pass4_w<T, FLUSH, QC, 64>(p, s);
+  if (p.fused) return launch_lazy_pass4_w<T, FLUSH, QC, 64, true>(p, s);
+  return launch_lazy_pass4_w<T, FLUSH, QC, 64, false>(p, s);
 }
 
 template <typename T, bool FLUSH>
@@ -1465,10 +1490,15 @@ static int lazy_pass(const DenseParams& p, bool flush, cudaStream_t s) {
 // with b = 6 every read pass stays HBM-bound (q <= 5), so 6 is the default;
 // 6 for fp32 and 5 for complex128 (profiles/r01/sweep_lazy_block_*.txt).
 // RPLU_LAZY_BLOCK overrides.
+// With fused pending terms (one FMA per term, the default) a read pass
+// stays HBM-bound to about twice as many terms, so the flush interval is
+// longer (RPLU_LAZY_BLOCK_FUSED overrides; profiles/r02/sweep_lazy_block_fused_*.txt).
 template <typename T>
-static int lazy_block() {
-  const int dflt = sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 6);
-  int b = env_int("RPLU_LAZY_BLOCK", dflt);
+static int lazy_block(bool fused) {
+  const int dflt = fused ? (sizeof(T) == 16 ? 8 : 12)
+                         : (sizeof(T) == 16 ? 5 : (sizeof(T) == 4 ? 6 : 6));
+  int b = fused ? env_int("RPLU_LAZY_BLOCK_FUSED", env_int("RPLU_LAZY_BLOCK", dflt))
+                : env_int("RPLU_LAZY_BLOCK", dflt);
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
 
@@ -1477,7 +1507,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
                            long long* launches) {
   DenseParams p = base;
   p.lazy = 1;
-  const int block = lazy_block<T>();
+  const int block = lazy_block<T>(p.fused != 0);
   sweep<T>(p, false, false, s);  // K1: masses of A
   RPLU_CUDA(cudaGetLastError());
   long long nl = 1;
@@ -1515,7 +1545,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
 // the pending steps t0..done-1 (no-op when the loop ran to the end).
 template <typename T>
 static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_t s) {
-  const long long block = lazy_block<T>();
+  const long long block = lazy_block<T>(base.fused != 0);
   const long long t0 = (done / block) * block;
   if (done <= t0 || done >= base.steps) return RPLU_OK;
   DenseParams p = base;
@@ -1643,6 +1673,7 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   p.pivots = reinterpret_cast<long long*>(ctx->pivots.ptr);
   p.stop_tol = a->stop_tol;
   p.rule = a->rule;
+  p.fused = (a->flags & RPLU_FLAG_EXACT) ? 0 : 1;  // delayed-update loop only
 
   LoopTiming tm;
   tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
@@ -1739,7 +1770,7 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     if (rc) return rc;
     RPLU_CUDA(cudaStreamSynchronize(s));
   }
-  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype) : 0;
+  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype, p.fused != 0) : 0;
   out->sweep_bytes = 0.0;
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,
@@ -2000,11 +2031,11 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   return RPLU_OK;
 }
 
-int dense_lazy_block_default(int dtype) {
+int dense_lazy_block_default(int dtype, bool fused) {
   switch (dtype) {
-    case RPLU_F64: return lazy_block<double>();
-    case RPLU_F32: return lazy_block<float>();
-    default: return lazy_block<double2>();
+    case RPLU_F64: return lazy_block<double>(fused);
+    case RPLU_F32: return lazy_block<float>(fused);
+    default: return lazy_block<double2>(fused);
   }
 }
 

@@ -756,12 +756,15 @@ int mf_run_impl(rplu_ctx* ctx, const rplu_mf_args* a, rplu_mf_out* out) {
                             s));
   long long launches = 0;
   GaussOp gop{n, m, op.P, op.Q, op.c};
-  float gemv_total = 0.f;
+  float gemv_total = 0.f;   // K7 time: the initial row-norm pass + one pass per step
   const bool time_gemv = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
 
   // initial row norms (accessor row_norms(), lowmem_cur.py:235-236) and total0
   if (op.kind == 0) {
-    if ((rc = gauss_gemv_impl(ctx, gop, nullptr, nrow, true, s, nullptr))) return rc;
+    float ms0 = 0.f;   // the row-norm pass is the same K7 kernel (squares)
+    if ((rc = gauss_gemv_impl(ctx, gop, nullptr, nrow, true, s, time_gemv ? &ms0 : nullptr)))
+      return rc;
+    gemv_total += ms0;
     launches += 2;
   } else {
     mf_dense_gemv_kernel<<<blocks_for(n * 32, 256, 8 * ctx->sm_count), 256, 0, s>>>(op, nullptr,

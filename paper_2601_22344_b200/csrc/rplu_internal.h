@@ -91,7 +91,7 @@ constexpr int kLazyMaxBlock = 16;  // longest delayed-update block
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
                            long long t0, bool pivcol, bool flush, bool force, cudaStream_t s);
-int dense_lazy_block_default(int dtype);
+int dense_lazy_block_default(int dtype, bool fused = false);
 
 // Sharded Cauchy-like steps (cauchy.cu).
 int cauchy_shard_begin_impl(rplu_ctx* ctx, const rplu_cauchy_shard_args* a, double* stats);
@@ -116,6 +116,8 @@ int cuda_fail(cudaError_t e, const char* where);
 
 int dmma_peak_impl(rplu_ctx* ctx, double* tflops, double* ms_out);
 int mf_run_impl(rplu_ctx* ctx, const rplu_mf_args* a, rplu_mf_out* out);
+int upload_impl(rplu_ctx* ctx, void* dst, const void* src, long long bytes, int threads,
+                cudaStream_t s);
 
 // K11 fused ||A - X Y||_F^2, ||A||_F^2 (lu_error.cu); out_sq host[2]
 int lu_error_impl(rplu_ctx* ctx, int dtype, const void* A, long long lda, long long n,
@@ -169,4 +171,6 @@ struct rplu_ctx {
   rplu::DevBuf lu_pad;      // K11: zero-padded fp64 factor panels
   rplu::DevBuf lu_part;     // K11: per-CTA partial sums
   rplu::DevBuf mf_buf;      // rplu_mf_run workspace (vectors, core factors, histories)
+  void* ring = nullptr;     // rplu_upload: page-locked staging slots
+  cudaEvent_t ring_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };

@@ -109,7 +109,8 @@ def _input_tensor(A, compute_dtype):
 
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
-              return_device=None, time_kernels=False, update="auto", persistent=True):
+              return_device=None, time_kernels=False, update="auto", persistent=True,
+              exact_updates=False):
     """Run pivoted elimination for up to ``steps`` pivots (dense_pivots.py:129).
 
     Stops early, with a flag, when the residual Frobenius norm falls to
@@ -125,10 +126,16 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     ours or the reference's, get numpy results), ``time_kernels`` (bracket the K2/K3 launches
     with CUDA events; results in ``trace.kernel_stats``), ``update``
     ("auto" | "eager" | "lazy": update the residual every step, or apply the
-    pending rank-1 terms on the fly and write R every few steps — same bits,
-    half the HBM traffic; "auto" = lazy when R does not fit in L2),
+    pending rank-1 terms on the fly and write R every few steps — about half
+    the HBM traffic; "auto" = lazy when R does not fit in L2),
     ``persistent`` (False: per-step K2/K3 launches even where an L2-resident
-    residual would run the whole loop as one persistent cooperative launch).
+    residual would run the whole loop as one persistent cooperative launch),
+    ``exact_updates`` (delayed-update loop: apply the pending terms with the
+    reference's multiply-then-subtract rounding, bit-identical to the eager
+    loop; default False: one FMA per term -- L/U agree with the reference to
+    rounding (the north star's 1e-10), pivots identical except within 1e-12
+    of a CDF boundary, and the flush interval doubles).  The eager and the
+    resident loops always use the reference's rounding.
     """
     if update not in ("auto", "eager", "lazy"):
         raise ValueError(f"unknown update mode {update!r}")
@@ -172,7 +179,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         stream=torch.cuda.current_stream(dev).cuda_stream,
         flags=((_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
                | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]
-               | (0 if persistent else _ffi.FLAG_STEPWISE)))
+               | (0 if persistent else _ffi.FLAG_STEPWISE)
+               | (_ffi.FLAG_EXACT if exact_updates else 0)))
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)

@@ -341,6 +341,8 @@ def _cur_build_device(op, rule, rank, stop_tol, rng, core_mode, time_gemv):
     info.uniforms_consumed = int(out.uniforms_consumed)
     info.kernel_launches = int(out.kernel_launches)
     if time_gemv and k:
+        # K7 time of the run (the initial row-norm pass and the k g = A l
+        # passes), spread evenly over the steps
         info.gemv_ms = [float(out.gemv_ms) / k] * k
     return fact, info
 

@@ -43,12 +43,22 @@ def c3_host(cuda_device):
 
 
 def test_c3_fp64_full_size_parity(c3_host, cuda_device):
+    """The bench workload through the default call (delayed updates with one
+    FMA per pending term: pivots equal, L/U to 1e-10 -- the north star) and
+    with exact_updates=True (the reference's rounding: L/U bit-identical)."""
+    ex = rp.eliminate(c3_host, rp.PivotRule("rplu", rp.RngState(0)), R3, exact_updates=True)
+    assert ex.steps == R3
     tr = rp.eliminate(c3_host, rp.PivotRule("rplu", rp.RngState(0)), R3)
     assert tr.steps == R3
     torch.cuda.empty_cache()
     ref = c_oracle.eliminate_c(c3_host, "rplu", R3, seed=0, margins=True)
-    t = check_dense_parity(tr, ref)
+    t_exact = check_dense_parity(ex, ref)
+    t = check_dense_parity(tr, ref, exact=False, rtol=1e-10)
+    lk = min(R3 if t is None else t, ex.steps)
+    dl = float(np.abs(tr.L[:, :lk] - ref["L"][:, :lk]).max() / np.abs(ref["L"]).max())
+    du = float(np.abs(tr.U[:lk] - ref["U"][:lk]).max() / np.abs(ref["U"]).max())
     record_parity("c3_fp64_full", n=N3, steps=R3, first_divergence=t,
+                  first_divergence_exact=t_exact, fused_L_rel=dl, fused_U_rel=du,
                   near_boundary_draws=tr.near_boundary_draws,
                   min_margin=float(np.min(ref["margins"])),
                   uniforms_consumed=tr.uniforms_consumed,
@@ -71,7 +81,7 @@ def test_c3_fp32_full_size_parity(c3_host, cuda_device):
     records the measured figure."""
     A32 = c3_host.astype(np.float32)
     tr = rp.eliminate(torch.from_numpy(A32).cuda(), rp.PivotRule("rplu", rp.RngState(0)), R3,
-                      overwrite_a=True, return_device=False)
+                      overwrite_a=True, return_device=False, exact_updates=True)
     torch.cuda.empty_cache()
     assert tr.steps == R3 and tr.L.dtype == np.float32
     ref = c_oracle.eliminate_c(A32, "rplu", R3, seed=0, margins=True, dtype=np.float32)
@@ -90,6 +100,18 @@ def test_c3_fp32_full_size_parity(c3_host, cuda_device):
                   L_rel_over_model_max=float((dl_col / np.maximum(model, 1e-300)).max()))
     assert du <= 1e-4 and dr <= 1e-4
     assert np.all(dl_col <= np.maximum(1e-4, 16.0 * model)), "L error beyond the fp32 model"
+    # the default call (fused pending terms, the bench path): pivots equal to
+    # the restatement's, factors within the same fp32 model of the replay
+    fz = rp.eliminate(torch.from_numpy(A32).cuda(), rp.PivotRule("rplu", rp.RngState(0)), R3,
+                      overwrite_a=True, return_device=False)
+    tz = next((s for s, (a, b) in enumerate(zip(fz.pivots, ref["pivots"])) if a != b), None)
+    assert tz is None or ref["margins"][tz] <= oracle.NEAR_REL
+    kz = R3 if tz is None else tz
+    dlz = np.abs(fz.L[:, :kz] - rep["L"][:, :kz]).max(axis=0) / lmax
+    assert np.abs(fz.U[:kz] - rep["U"][:kz]).max() / umax <= 1e-4
+    assert np.all(dlz <= np.maximum(1e-4, 16.0 * model[:kz]))
+    record_parity("c3_fp32_full_fused", first_divergence=tz, L_rel_max=float(dlz.max()),
+                  near_boundary_draws=fz.near_boundary_draws)
 
 
 def test_c2_full_rank_200(cuda_device):
