@@ -66,8 +66,9 @@ extern "C" {
 #define RPLU_FLAG_EXACT 32      /* dense delayed-update loop: apply the pending rank-1 terms
                                     with the reference's rounding (multiply, then subtract:
                                     bit-identical to the eager loop and to the reference's
-                                    arithmetic); default: one FMA per term (L/U agree to
-                                    rounding, half the FP64 work, longer flush interval) */
+                                    arithmetic; the Python layer always sets it unless
+                                    fused_updates=True); without it: one FMA per term (L/U
+                                    agree to rounding, half the FP64 work) */
 
 /* pivot rules: rplu (random, 2 uniforms/step), c2plu / cplu (greedy) */
 #define RPLU_RULE_RPLU 0

@@ -110,7 +110,7 @@ def _input_tensor(A, compute_dtype):
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
               return_device=None, time_kernels=False, update="auto", persistent=True,
-              exact_updates=False):
+              fused_updates=False):
     """Run pivoted elimination for up to ``steps`` pivots (dense_pivots.py:129).
 
     Stops early, with a flag, when the residual Frobenius norm falls to
@@ -130,12 +130,12 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     the HBM traffic; "auto" = lazy when R does not fit in L2),
     ``persistent`` (False: per-step K2/K3 launches even where an L2-resident
     residual would run the whole loop as one persistent cooperative launch),
-    ``exact_updates`` (delayed-update loop: apply the pending terms with the
-    reference's multiply-then-subtract rounding, bit-identical to the eager
-    loop; default False: one FMA per term -- L/U agree with the reference to
-    rounding (the north star's 1e-10), pivots identical except within 1e-12
-    of a CDF boundary, and the flush interval doubles).  The eager and the
-    resident loops always use the reference's rounding.
+    ``fused_updates`` (delayed-update loop: apply each pending term with one
+    FMA instead of the reference's multiply-then-subtract; L/U then agree
+    with the reference to rounding (the north star's 1e-10) instead of bit
+    for bit; measured no faster at C3 -- the pass is shared-memory / power
+    bound -- so off by default).  The eager and the resident loops always
+    use the reference's rounding.
     """
     if update not in ("auto", "eager", "lazy"):
         raise ValueError(f"unknown update mode {update!r}")
@@ -180,7 +180,7 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         flags=((_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
                | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]
                | (0 if persistent else _ffi.FLAG_STEPWISE)
-               | (_ffi.FLAG_EXACT if exact_updates else 0)))
+               | (0 if fused_updates else _ffi.FLAG_EXACT)))
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)

@@ -3,7 +3,7 @@
     python scripts/sweep_lazy_block.py [f64|f32|c128] [b,b,...] [exact|fused]
 
 exact: the reference's multiply-then-subtract per pending term
-(RPLU_LAZY_BLOCK, exact_updates=True; pivots and U checked identical to the
+(RPLU_LAZY_BLOCK, fused_updates=False; pivots and U checked identical to the
 eager loop); fused (default arithmetic): one FMA per term
 (RPLU_LAZY_BLOCK_FUSED; pivots identical, U to 1e-12 of its scale)."""
 import os
@@ -28,7 +28,7 @@ A = gen.c3_dense_device(0, n=n, dtype=torch.float64).to(dt)
 
 def run(update, timed=False):
     return rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), steps, update=update,
-                        time_kernels=timed, exact_updates=exact)
+                        time_kernels=timed, fused_updates=not exact)
 
 
 ref = run("eager")

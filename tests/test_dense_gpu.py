@@ -276,7 +276,7 @@ def test_lazy_update_is_bit_identical(dtype, n, m, steps, cuda_device):
     At = torch.from_numpy(A).to("cuda", dtype)
     e = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(3)), steps, update="eager")
     z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(3)), steps, update="lazy",
-                     time_kernels=True, exact_updates=True)
+                     time_kernels=True, fused_updates=False)
     assert z.kernel_stats["lazy_block"] > 0 and e.kernel_stats["lazy_block"] == 0
     assert z.pivots == e.pivots
     assert torch.equal(z.L, e.L) and torch.equal(z.U, e.U)
@@ -301,7 +301,7 @@ def test_lazy_every_flush_interval_is_bit_identical(dtype, block, cuda_device, m
     At = torch.from_numpy(A).to("cuda", dtype)
     e = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(5)), steps, update="eager")
     z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(5)), steps, update="lazy",
-                     time_kernels=True, exact_updates=True)
+                     time_kernels=True, fused_updates=False)
     assert z.kernel_stats["lazy_block"] == block
     assert z.pivots == e.pivots
     assert torch.equal(z.L, e.L) and torch.equal(z.U, e.U)
@@ -312,8 +312,8 @@ def test_lazy_every_flush_interval_is_bit_identical(dtype, block, cuda_device, m
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.complex128])
 @pytest.mark.parametrize("block", [1, 3, 8, 12, 16])
 def test_lazy_fused_every_flush_interval(dtype, block, cuda_device, monkeypatch):
-    """The default delayed-update arithmetic (one FMA per pending term) for
-    every instantiated pending-term count: pivots equal to the eager loop's
+    """The optional fused delayed-update arithmetic (one FMA per pending
+    term) for every instantiated pending-term count: pivots equal to the eager loop's
     (reference rounding), L / U / residual to 1e-12 of their scale (fp64,
     complex128) or 1e-5 (fp32)."""
     monkeypatch.setenv("RPLU_LAZY_BLOCK_FUSED", str(block))
@@ -325,7 +325,7 @@ def test_lazy_fused_every_flush_interval(dtype, block, cuda_device, monkeypatch)
     At = torch.from_numpy(A).to("cuda", dtype)
     e = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(6)), steps, update="eager")
     z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(6)), steps, update="lazy",
-                     time_kernels=True)
+                     time_kernels=True, fused_updates=True)
     assert z.kernel_stats["lazy_block"] == block
     assert z.pivots == e.pivots
     tol = 1e-5 if dtype == torch.float32 else 1e-12
@@ -381,17 +381,17 @@ def test_lazy_early_stops_flush_the_residual(rule, cuda_device):
     A = torch.from_numpy(gen.c1_dense(2, n=600, m=512)).cuda()
     mk = (lambda: rp.PivotRule("rplu", rp.RngState(2))) if rule == "rplu" else (lambda: "c2plu")
     e = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="eager")
-    z = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="lazy", exact_updates=True)
+    z = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="lazy", fused_updates=False)
     assert e.tol_stop and z.tol_stop and z.steps == e.steps
     assert torch.equal(z.residual, e.residual) and torch.equal(z.L, e.L)
-    f = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="lazy")     # fused terms
+    f = rp.eliminate(A, mk(), 300, stop_tol=0.3, update="lazy", fused_updates=True)
     assert f.tol_stop and f.steps == e.steps and f.pivots == e.pivots
     assert float((f.residual - e.residual).abs().max()) <= 1e-12 * float(A.abs().max())
     # clean stop on an exactly low-rank matrix
     B = torch.from_numpy(np.diag(np.arange(1.0, 31.0))).cuda()
     e = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30, update="eager")
     z = rp.eliminate(B, rp.PivotRule("rplu", rp.RngState(0)), 30, update="lazy",
-                     exact_updates=True)
+                     fused_updates=False)
     assert z.pivots == e.pivots and torch.equal(z.residual, e.residual)
 
 
@@ -399,9 +399,10 @@ def test_lazy_matches_oracle_c3_reduced(cuda_device):
     A = gen.c3_dense_host(1, n=4096)
     ref = oracle.eliminate_real(A, "rplu", 128, seed=1, margins=True)
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 128, update="lazy",
-                      exact_updates=True)
+                      fused_updates=False)
     check_dense_parity(tr, ref)
-    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 128, update="lazy")
+    tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(1)), 128, update="lazy",
+                      fused_updates=True)
     check_dense_parity(tr, ref, exact=False, rtol=1e-12)
 
 

@@ -89,7 +89,7 @@ def test_shard_rows_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 3), (3, 5)])
+@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 3), (3, 5), (8, 0), (8, 4)])
 def test_sharded_matches_single_process(world, lazy_block):
     import oracle
     from paper_2601_22344_b200 import gen
@@ -169,7 +169,7 @@ def _run_cauchy(x, y, G, B, rule, seed, steps, world=2, stop_tol=0.0):
 
 
 @pytest.mark.parametrize("world,rule,stop_tol", [(2, "rplu", 0.0), (3, "rplu", 1e-3),
-                                                 (2, "c2plu", 0.0)])
+                                                 (2, "c2plu", 0.0), (8, "rplu", 0.0)])
 def test_sharded_cauchy_matches_single_process(world, rule, stop_tol):
     """Row-sharded Cauchy-like elimination (x / G sharded, y / B replicated)
     reproduces the single-process oracle: pivots, bound statistics, and the
@@ -217,7 +217,7 @@ def _cur_worker(rank, world, port, A, seed, k, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_cur_matches_oracle(world):
     """Row-sharded cur_build (replicated operator, local row norms / g / c
     rows, g[I] by a -0.0 allreduce) picks the oracle's skeleton."""

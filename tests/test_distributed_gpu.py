@@ -79,7 +79,7 @@ def test_lazy_rejects_graph_and_device_steps(cuda_device):
         be.select(-1, tot)
 
 
-@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 4), (3, 5)])
+@pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 4), (3, 5), (8, 0), (8, 6)])
 def test_emulated_shards(world, lazy_block, cuda_device):
     A = gen.c1_dense(6, n=500, m=333)
     steps = 120
@@ -122,6 +122,45 @@ def test_emulated_shards(world, lazy_block, cuda_device):
     np.testing.assert_allclose(res[0]["resid_fro"], ref["resid_fro"], rtol=1e-12)
     Rs = torch.cat([b.R for b in bes], dim=0).cpu().numpy()
     np.testing.assert_array_equal(Rs, ref["residual"])
+
+
+def _emulate_dense(A_dev, world, steps, seed, lazy_block):
+    """world shards of a device matrix on one GPU (own contexts; the
+    allreduce / allgather replaced by device-side sums / concatenation)."""
+    n, m = A_dev.shape
+    bes = []
+    for r in range(world):
+        lo, hi = shard_rows(n, world, r)
+        bes.append(CudaShardBackend(A_dev[lo:hi].clone(), lo, world, r,
+                                    rp.PivotRule("rplu", rp.RngState(seed)), steps,
+                                    ctx=_ffi.Context(0), lazy_block=lazy_block))
+    totals = torch.cat([b.begin().clone() for b in bes])
+    for t in range(steps + 1):
+        ms = [b.select(t, totals).clone() for b in bes]
+        if t == steps:
+            break
+        msg = ms[0]
+        for x in ms[1:]:
+            msg = msg + x
+        totals = torch.cat([b.update(t, msg).clone() for b in bes])
+    return bes, [b.finish() for b in bes]
+
+
+@pytest.mark.parametrize("lazy_block", [0, 6])
+def test_eight_shards_reduced_c3(lazy_block, cuda_device):
+    """SURVEY §8(e) at G = 8 (emulated on one GPU): the reduced C3
+    construction (n = 4096, 128 pivots), eager and delayed-update shard
+    steps, pivots / L / U / residual bit-identical to the single-GPU eager
+    elimination (the reference's rounding)."""
+    A = gen.c3_dense_device(0, n=4096)
+    ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), 128, update="eager")
+    bes, res = _emulate_dense(A, 8, 128, 0, lazy_block)
+    for r in res:
+        assert r["pivots"] == ref.pivots
+    L = torch.cat([r["L_local"] for r in res], dim=0)
+    assert torch.equal(L, ref.L) and torch.equal(res[0]["U"], ref.U)
+    assert torch.equal(torch.cat([b.R for b in bes], dim=0), ref.residual_device)
+    np.testing.assert_allclose(res[0]["resid_fro"], ref.resid_fro, rtol=1e-12)
 
 
 # ---------------------------------------------------------------------------
@@ -200,6 +239,39 @@ def test_cauchy_emulated_shards(world, rule, stop_tol, cuda_device):
     for t, (c, r, a) in enumerate(ref["steps"]):
         assert np.abs(C[t] - c).max() <= 1e-10 * np.abs(c).max()
         assert np.abs(bes[0].R[t].cpu().numpy() - r).max() <= 1e-10 * np.abs(r).max()
+
+
+@pytest.mark.slow
+def test_cauchy_one_vs_eight_shards_full_n(cuda_device):
+    """SURVEY §8(d) C4 bar "1-vs-8-GPU pivot identity at full n": the C4
+    generators at n = m = 2^20, p = 4, three pivot steps, single GPU against
+    8 emulated shards: identical pivots and bound sums / maxes to 1e-11."""
+    x, y, G, B = gen.c4_cauchy_like(0)
+    K = 3
+    ref = rp.structured_eliminate(rp.CauchyLikeMatrix(x, y, G, B, check_points=False), "rplu",
+                                  K, rng=rp.RngState(0))
+    world = 8
+    bes = []
+    for r in range(world):
+        lo, hi = shard_rows(x.size, world, r)
+        Ml = rp.CauchyLikeMatrix(x[lo:hi], y, G[lo:hi], B, check_points=False)
+        bes.append(CudaCauchyShardBackend(Ml, lo, world, r, "rplu", rp.RngState(0), K,
+                                          ctx=_ffi.Context(0)))
+    stats = torch.cat([b.begin().clone() for b in bes])
+    for t in range(K):
+        ms = [b.select(t, stats).clone() for b in bes]
+        msg = ms[0]
+        for m2 in ms[1:]:
+            msg = msg + m2
+        stats = torch.cat([b.update(t, msg).clone() for b in bes])
+    outs = [b.finish() for b in bes]
+    k = int(outs[0].steps_done)
+    assert k == K
+    for b in bes:
+        assert [int(v) for v in b.rows[:k]] == ref.row_indices
+        assert [int(v) for v in b.cols[:k]] == ref.col_indices
+    np.testing.assert_allclose(bes[0].bmax[:k], ref.bound_maxes[:k], rtol=1e-11)
+    np.testing.assert_allclose(bes[0].bsum[:k], ref.bound_sums[:k], rtol=1e-11)
 
 
 # ---------------------------------------------------------------------------
