@@ -63,6 +63,10 @@ extern "C" {
                                     default: delayed updates when R exceeds L2 */
 #define RPLU_FLAG_STEPWISE 16   /* dense: per-step launches even where the whole loop would run
                                     as one persistent cooperative launch */
+#define RPLU_FLAG_NO_GRAM 64    /* dense fp64 delayed-update loop: compute each step's
+                                    masses by applying the pending terms (2q FP64 operations
+                                    per element) instead of from the Gram form (one dot
+                                    product per element, flush every 16 steps) */
 #define RPLU_FLAG_EXACT 32      /* dense delayed-update loop: apply the pending rank-1 terms
                                     with the reference's rounding (multiply, then subtract:
                                     bit-identical to the eager loop and to the reference's

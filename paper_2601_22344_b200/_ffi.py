@@ -36,6 +36,7 @@ FLAG_LAZY = 4
 FLAG_EAGER = 8
 FLAG_STEPWISE = 16
 FLAG_EXACT = 32
+FLAG_NO_GRAM = 64
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -218,6 +218,7 @@ int rplu_ctx_destroy(rplu_ctx* ctx) {
     ctx->lu_pad.release();
     ctx->lu_part.release();
     ctx->mf_buf.release();
+    ctx->gram.release();
     if (ctx->ring) cudaFreeHost(ctx->ring);
     for (auto& e : ctx->ring_ev)
       if (e) cudaEventDestroy(e);

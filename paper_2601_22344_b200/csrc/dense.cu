@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <stdint.h>
 
 #include <stdlib.h>
@@ -51,8 +52,16 @@ struct DenseParams {
   long long t0;
   int lazy;
   int force;  // run the pass even after a stop (final flush)
-  int fused;  // delayed updates: one FMA per pending term (default) instead of
-              // the reference's multiply-then-subtract (bit-identical to eager)
+  int fused;  // delayed updates: one FMA per pending term instead of the
+              // reference's multiply-then-subtract (bit-identical to eager)
+  // Gram-mass delayed updates (fp64): masses of R^(t+1) from R^(t0) without
+  // applying the pending terms -- m0 - 2 lin + quad per row (see below)
+  int gram;
+  long long gram_t0;   // first pending step (t0) of the Gram masses
+  double* m0;          // [n] exact masses at the last flush
+  double* lin;         // [n] sum_s L_is (r0_i . U_s)
+  double* quad;        // [n] sum_{s,s'} L_is L_is' (U_s . U_s')
+  double* gmat;        // [16 x 16] U_s . U_s' of the pending steps
 };
 
 // One pending term of the delayed-update loop, R -= L_s U_s at one element:
@@ -657,11 +666,71 @@ struct LazyTma {
   static constexpr size_t SMEM = OFF_BAR + 2 * STAGES * sizeof(uint64_t) + 1024;  // + alignment
 };
 
+// Gram-mass delayed updates (fp64).  With r0_i the row of R^(t0) (the last
+// flush) and the pending rank-1 terms s = t0..t,
+//   |r_i^(t+1)|^2 = |r0_i|^2 - 2 sum_s L_is (r0_i . U_s)
+//                   + sum_{s,s'} L_is L_is' (U_s . U_s'),
+// so a step needs one dot product per row with the newest U row (one read of
+// R at one FMA per element, whatever the number of pending terms) plus O(q)
+// per row: lin_i += L_it g_it, quad_i += L_it (2 sum_{s<t} L_is G_ts +
+// L_it G_tt).  The pass therefore stays HBM-bound for every q and the flush
+// interval can grow to 16.  Only the sampling masses come from this formula
+// (they differ from the applied-update masses by a few ulps of |r0_i|^2:
+// draws change only within rounding of a CDF boundary, counted as
+// near-boundary draws); L, U and the residual still come from the exact
+// pending-term arithmetic (pivot row / column, flush), bit-identical to the
+// eager loop.  Negative rounding residue of eliminated rows is clamped to 0.
+__device__ __forceinline__ void gram_mass_update(const DenseParams& p, long long i, double g) {
+  const long long t = p.t, t0 = p.gram_t0, n = p.n;
+  const double* Lt = reinterpret_cast<const double*>(p.Lt);
+  const double* G = p.gmat + (t - t0) * kLazyMaxBlock;
+  const double lt = Lt[t * n + i];
+  double cross = 0.0;
+  for (long long s = t0; s < t; ++s) cross = fma(Lt[s * n + i], G[s - t0], cross);
+  const double lin = fma(lt, g, p.lin[i]);
+  const double quad = fma(lt, fma(2.0, cross, lt * G[t - t0]), p.quad[i]);
+  p.lin[i] = lin;
+  p.quad[i] = quad;
+  const double mass = fma(-2.0, lin, p.m0[i]) + quad;
+  p.masses[i] = mass > 0.0 ? mass : 0.0;
+}
+
+// G[t - t0][s - t0] = U_t . U_s for the pending s (one CTA per s, fixed order)
+__global__ void __launch_bounds__(256) lazy_gram_kernel(DenseParams p) {
+  if (!p.st->active) return;
+  const long long t = p.t, s = p.gram_t0 + blockIdx.x, m = p.m;
+  const double* U = reinterpret_cast<const double*>(p.U);
+  const double* ut = U + t * p.ldu;
+  const double* us = U + s * p.ldu;
+  double acc = 0.0;
+  for (long long k = threadIdx.x; k < m; k += blockDim.x) acc = fma(ut[k], us[k], acc);
+  acc = warp_sum(acc);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w];
+    p.gmat[(t - p.gram_t0) * kLazyMaxBlock + blockIdx.x] = v;
+  }
+}
+
+// start of a pending block: m0 = the exact masses, lin = quad = 0
+__global__ void gram_reset_kernel(DenseParams p) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    p.m0[i] = p.masses[i];
+    p.lin[i] = 0.0;
+    p.quad[i] = 0.0;
+  }
+}
+
 // tmR: R as a 2-D tensor (columns x rows, in 8-byte words for fp64 and
 // complex128, 4-byte for fp32), box = 1 KB x 32 rows; tmU: the pending rows
 // U[t0 .. t0+QC) with box 1 KB x QC rows.  Out-of-range rows and columns are
 // zero-filled by the TMA unit, so every stage carries (32 + QC) KB.
-template <typename T, int VEC, bool FLUSH, int QC, int TXW = 64, bool FUSED = false>
+template <typename T, int VEC, bool FLUSH, int QC, int TXW = 64, bool FUSED = false,
+          bool DOT = false>
 __global__ void __launch_bounds__(288, 1)
     lazy_pass4_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmR,
                       const __grid_constant__ CUtensorMap tmU) {
@@ -766,7 +835,8 @@ __global__ void __launch_bounds__(288, 1)
         double sv = rd[(C::WPG * g) * RPT + r];
 #pragma unroll
         for (int q = 1; q < C::WPG; ++q) sv += rd[(C::WPG * g + q) * RPT + r];
-        p.masses[prev_row0 + threadIdx.x] = sv;
+        if constexpr (DOT) gram_mass_update(p, prev_row0 + threadIdx.x, sv);
+        else p.masses[prev_row0 + threadIdx.x] = sv;
       }
     }
     const long long myrow0 = row0 + ty * RPT;
@@ -778,7 +848,22 @@ __global__ void __launch_bounds__(288, 1)
       mbar_wait(&full[stage], phase);
       V* st = tiles + (size_t)stage * (ROWS + QC) * TX;
       const long long l = c * CW + (long long)tx * VEC;
-      if (l < m) {
+      if (DOT && l < m) {
+        // Gram-mass step: g_i = r0_i . U_t (the stage's one U row is U_t)
+        if constexpr (!std::is_same<T, double2>::value) {   // real types only
+          const V u = st[ROWS * TX + tx];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const V x = st[(ty * RPT + r) * TX + tx];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              if (VEC == 1 || l + e < m) acc[r] = fma((double)x.v[e], (double)u.v[e], acc[r]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      } else if (l < m) {
         V rv[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) rv[r] = st[(ty * RPT + r) * TX + tx];
@@ -841,7 +926,8 @@ __global__ void __launch_bounds__(288, 1)
       double sv = rd[(C::WPG * g) * RPT + r];
 #pragma unroll
       for (int q = 1; q < C::WPG; ++q) sv += rd[(C::WPG * g + q) * RPT + r];
-      p.masses[prev_row0 + threadIdx.x] = sv;
+      if constexpr (DOT) gram_mass_update(p, prev_row0 + threadIdx.x, sv);
+      else p.masses[prev_row0 + threadIdx.x] = sv;
     }
   }
 }
@@ -1396,13 +1482,13 @@ static bool make_row_map(CUtensorMap* map, const void* base, int esize, long lon
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, bool FLUSH, int QC, int TXW, bool FUSED>
+template <typename T, bool FLUSH, int QC, int TXW, bool FUSED, bool DOT = false>
 static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
   constexpr int VEC = Scalar<T>::kVec;
   using C = LazyTma<T, QC, TXW>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED>,
+    cudaFuncSetAttribute(lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED, DOT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
@@ -1416,7 +1502,8 @@ static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
     set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
     return RPLU_ERR_CUDA;
   }
-  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR, tmU);
+  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED, DOT><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR,
+                                                                                       tmU);
   return RPLU_OK;
 }
 
@@ -1502,15 +1589,41 @@ static int lazy_block(bool fused) {
   return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
 }
 
+// One Gram-mass step (fp64): U_t . U_s for the pending s, then the read pass
+// g_i = r0_i . U_t with the mass update (the TMA map loads U row t).
+template <typename T>
+static int gram_step(const DenseParams& p, long long t0, cudaStream_t s) {
+  if constexpr (std::is_same<T, double>::value) {
+    DenseParams q = p;
+    q.gram_t0 = t0;
+    lazy_gram_kernel<<<(unsigned)(p.t - t0 + 1), 256, 0, s>>>(q);
+    q.t0 = p.t;  // the pass's one "pending" U row is U_t
+    return launch_lazy_pass4_w<double, false, 1, 64, false, true>(q, s);
+  } else {
+    set_error("Gram-mass delayed updates are fp64 only");
+    return RPLU_ERR_ARG;
+  }
+}
+
+// Flush interval of the Gram-mass loop: the read passes cost the same for
+// every q, so the longest block (16) minimises the flushes
+// (RPLU_LAZY_BLOCK_GRAM overrides).
+static int gram_block() {
+  const int b = env_int("RPLU_LAZY_BLOCK_GRAM", kLazyMaxBlock);
+  return b < 1 ? 1 : (b > kLazyMaxBlock ? kLazyMaxBlock : b);
+}
+
 template <typename T>
 static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& tm,
                            long long* launches) {
   DenseParams p = base;
   p.lazy = 1;
-  const int block = lazy_block<T>(p.fused != 0);
+  const int block = p.gram ? gram_block() : lazy_block<T>(p.fused != 0);
   sweep<T>(p, false, false, s);  // K1: masses of A
   RPLU_CUDA(cudaGetLastError());
-  long long nl = 1;
+  const int reset_blocks = (int)std::min<long long>((p.n + 255) / 256, 1024);
+  if (p.gram) gram_reset_kernel<<<reset_blocks, 256, 0, s>>>(p);
+  long long nl = p.gram ? 2 : 1;
   long long t0 = 0;
   const int pc_blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
   const int row_blocks = (int)((p.m + 255) / 256 < 1024 ? (p.m + 255) / 256 : 1024);
@@ -1530,10 +1643,21 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
       lazy_pivcol_kernel<T><<<pc_blocks, 256, 0, s>>>(p);
       const bool flush = (t - t0 + 1 == block) || (t == p.steps - 1);
       tm.mark(flush ? 2 : 1, s, true);
-      if (int rc = lazy_pass<T>(p, flush, s)) return rc;
+      if (!flush && p.gram) {
+        if (int rc = gram_step<T>(p, t0, s)) return rc;
+        ++nl;
+      } else {
+        if (int rc = lazy_pass<T>(p, flush, s)) return rc;
+      }
       tm.mark(flush ? 2 : 1, s, false);
       nl += 2;
-      if (flush) t0 = t + 1;
+      if (flush) {
+        t0 = t + 1;
+        if (p.gram) {
+          gram_reset_kernel<<<reset_blocks, 256, 0, s>>>(p);
+          ++nl;
+        }
+      }
     }
   }
   RPLU_CUDA(cudaGetLastError());
@@ -1545,7 +1669,7 @@ static int dense_loop_lazy(const DenseParams& base, cudaStream_t s, LoopTiming& 
 // the pending steps t0..done-1 (no-op when the loop ran to the end).
 template <typename T>
 static int lazy_final_flush(const DenseParams& base, long long done, cudaStream_t s) {
-  const long long block = lazy_block<T>(base.fused != 0);
+  const long long block = base.gram ? gram_block() : lazy_block<T>(base.fused != 0);
   const long long t0 = (done / block) * block;
   if (done <= t0 || done >= base.steps) return RPLU_OK;
   DenseParams p = base;
@@ -1674,6 +1798,19 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
   p.stop_tol = a->stop_tol;
   p.rule = a->rule;
   p.fused = (a->flags & RPLU_FLAG_EXACT) ? 0 : 1;  // delayed-update loop only
+  // Gram masses for the fp64 delayed-update loop with the reference's
+  // arithmetic (RPLU_GRAM=0 disables)
+  static const int gram_env = env_int("RPLU_GRAM", 1);
+  if (gram_env && a->dtype == RPLU_F64 && !p.fused && !(a->flags & RPLU_FLAG_NO_GRAM)) {
+    if ((rc = ctx->gram.ensure(sizeof(double) * (3 * (size_t)(n > 0 ? n : 1) + 256))))
+      return rc;
+    double* gb = reinterpret_cast<double*>(ctx->gram.ptr);
+    p.m0 = gb;
+    p.lin = gb + n;
+    p.quad = gb + 2 * n;
+    p.gmat = gb + 3 * n;
+    p.gram = 1;
+  }
 
   LoopTiming tm;
   tm.on = (a->flags & RPLU_FLAG_TIME_KERNELS) != 0;
@@ -1770,7 +1907,8 @@ int dense_run_impl(rplu_ctx* ctx, const rplu_dense_args* a, rplu_dense_out* out)
     if (rc) return rc;
     RPLU_CUDA(cudaStreamSynchronize(s));
   }
-  out->lazy_block = lazy ? dense_lazy_block_default(a->dtype, p.fused != 0) : 0;
+  out->lazy_block = lazy ? (p.gram ? gram_block() : dense_lazy_block_default(a->dtype, p.fused != 0))
+                         : 0;
   out->sweep_bytes = 0.0;
   if (done > 0)
     RPLU_CUDA(cudaMemcpy(out->pivots, p.pivots, sizeof(long long) * 2 * done,

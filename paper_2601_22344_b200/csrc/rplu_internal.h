@@ -171,6 +171,7 @@ struct rplu_ctx {
   rplu::DevBuf lu_pad;      // K11: zero-padded fp64 factor panels
   rplu::DevBuf lu_part;     // K11: per-CTA partial sums
   rplu::DevBuf mf_buf;      // rplu_mf_run workspace (vectors, core factors, histories)
+  rplu::DevBuf gram;        // dense Gram-mass delayed updates: m0, lin, quad, U Gram
   void* ring = nullptr;     // rplu_upload: page-locked staging slots
   cudaEvent_t ring_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };

@@ -110,7 +110,7 @@ def _input_tensor(A, compute_dtype):
 
 def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=False,
               return_device=None, time_kernels=False, update="auto", persistent=True,
-              fused_updates=False):
+              fused_updates=False, gram_masses=True):
     """Run pivoted elimination for up to ``steps`` pivots (dense_pivots.py:129).
 
     Stops early, with a flag, when the residual Frobenius norm falls to
@@ -135,7 +135,12 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
     with the reference to rounding (the north star's 1e-10) instead of bit
     for bit; measured no faster at C3 -- the pass is shared-memory / power
     bound -- so off by default).  The eager and the resident loops always
-    use the reference's rounding.
+    use the reference's rounding.  ``gram_masses`` (fp64 delayed-update
+    loop, default True): the per-step sampling masses come from the Gram
+    form |r0 - sum_s L_s U_s|^2 (one dot product per element instead of
+    applying the pending terms, flush every 16 steps); L, U and the residual
+    are unchanged (bit-identical to the eager loop), the masses agree to
+    rounding.
     """
     if update not in ("auto", "eager", "lazy"):
         raise ValueError(f"unknown update mode {update!r}")
@@ -180,7 +185,8 @@ def eliminate(A, rule, steps, stop_tol=0.0, *, compute_dtype=None, overwrite_a=F
         flags=((_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
                | {"auto": 0, "eager": _ffi.FLAG_EAGER, "lazy": _ffi.FLAG_LAZY}[update]
                | (0 if persistent else _ffi.FLAG_STEPWISE)
-               | (0 if fused_updates else _ffi.FLAG_EXACT)))
+               | (0 if fused_updates else _ffi.FLAG_EXACT)
+               | (0 if gram_masses else _ffi.FLAG_NO_GRAM)))
     out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                         resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     c = _device.ctx(dev)

@@ -291,8 +291,10 @@ def test_lazy_every_flush_interval_is_bit_identical(dtype, block, cuda_device, m
     """Every pending-term count q = 1..16 of the TMA-fed pass (one kernel
     instantiation per q) against the eager loop, on a ragged shape (row
     count not a multiple of the 32-row block, odd column count: scalar tail,
-    partial last column chunk)."""
+    partial last column chunk); fp64 runs the Gram-mass loop (its flushes
+    are the q = block instantiations) and the applied-term loop."""
     monkeypatch.setenv("RPLU_LAZY_BLOCK", str(block))
+    monkeypatch.setenv("RPLU_LAZY_BLOCK_GRAM", str(block))
     n, m, steps = 1001, 1153, 70
     rs = np.random.default_rng(block)
     A = rs.standard_normal((n, m)) @ np.diag(0.98 ** np.arange(m))
@@ -300,13 +302,14 @@ def test_lazy_every_flush_interval_is_bit_identical(dtype, block, cuda_device, m
         A = A + 1j * rs.standard_normal((n, m)) @ np.diag(0.98 ** np.arange(m))
     At = torch.from_numpy(A).to("cuda", dtype)
     e = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(5)), steps, update="eager")
-    z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(5)), steps, update="lazy",
-                     time_kernels=True, fused_updates=False)
-    assert z.kernel_stats["lazy_block"] == block
-    assert z.pivots == e.pivots
-    assert torch.equal(z.L, e.L) and torch.equal(z.U, e.U)
-    assert torch.equal(z.residual, e.residual)
-    np.testing.assert_allclose(z.resid_fro, e.resid_fro, rtol=1e-13)
+    for gram in ((True, False) if dtype == torch.float64 else (True,)):
+        z = rp.eliminate(At, rp.PivotRule("rplu", rp.RngState(5)), steps, update="lazy",
+                         time_kernels=True, gram_masses=gram)
+        assert z.kernel_stats["lazy_block"] == block
+        assert z.pivots == e.pivots
+        assert torch.equal(z.L, e.L) and torch.equal(z.U, e.U)
+        assert torch.equal(z.residual, e.residual)
+        np.testing.assert_allclose(z.resid_fro, e.resid_fro, rtol=1e-13)
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.complex128])
