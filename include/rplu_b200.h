@@ -158,10 +158,11 @@ int rplu_dense_run(rplu_ctx* ctx, const rplu_dense_args* args, rplu_dense_out* o
 typedef struct rplu_shard_args {
   int32_t dtype;          /* RPLU_F32 | RPLU_F64 | RPLU_C128 */
   int32_t world, rank;    /* shard count and this shard's index */
-  int32_t lazy_block;     /* 0: eager K3 update; > 0 (<= 12): delayed-update
+  int32_t lazy_block;     /* 0: eager K3 update; > 0 (<= 16): delayed-update
                            * block (flush every lazy_block steps; needs the
                            * host step loop, t >= 0, and 16-byte aligned rows
-                           * of R and U); < 0: the single-GPU default */
+                           * of R and U); < 0: the default (fp64: Gram-form
+                           * masses, flush every 16 steps; else 6 / 5) */
   int64_t n_local, m;     /* local row block shape */
   int64_t ld;             /* row stride of R (elements) */
   int64_t row_offset;     /* global index of local row 0 */
@@ -193,6 +194,37 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
 int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active);
 /* Copy pivots / residual norms / flags to the host (out as for rplu_dense_run). */
 int rplu_shard_finish(rplu_ctx* ctx, const rplu_shard_args* a, rplu_dense_out* out);
+
+/* The same sharded elimination driven entirely from C across the GPUs of one
+ * node: one host thread, NCCL communicators from ncclCommInitAll (libnccl is
+ * loaded at run time), per step the shard select on every device, one grouped
+ * ncclAllReduce(sum) of the pivot message, the shard update and one grouped
+ * ncclAllGather of the shard totals (SURVEY §8(b) rplu_ctx_create(ngpus,
+ * devs), §8(e)).  A group owns one context and one stream per device. */
+typedef struct rplu_group rplu_group;
+int rplu_group_create(int32_t ngpus, const int32_t* devs, rplu_group** out);
+int rplu_group_destroy(rplu_group* g);
+
+typedef struct rplu_group_shard {
+  void* R;              /* device (on devs[d]): n_local x ld rows, updated in place */
+  void* Lt;             /* device: steps x n_local */
+  void* U;              /* device: (steps + 1) x ldu, replicated */
+  int64_t n_local, ld, row_offset;
+} rplu_group_shard;
+
+typedef struct rplu_group_dense_args {
+  int32_t dtype;
+  int32_t lazy_block;   /* as rplu_shard_args.lazy_block (0: eager, < 0: default) */
+  int64_t m, steps, ldu;
+  double stop_tol;
+  const double* uniforms;  /* host */
+  int64_t n_uniforms;
+  const rplu_group_shard* shards;  /* [ngpus], contiguous row blocks in device order */
+} rplu_group_dense_args;
+
+/* Replicated results (pivots, resid_fro, flags) in out, as rplu_dense_run;
+ * each shard's L rows stay in its Lt, U is replicated in every shard's U. */
+int rplu_group_dense_run(rplu_group* g, const rplu_group_dense_args* a, rplu_dense_out* out);
 
 /* Squared row masses sum_j |R_ij|^2 of a device matrix (K1), written to the
  * device array `masses` (n doubles).  Used by the sharded driver for step 0

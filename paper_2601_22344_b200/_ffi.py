@@ -93,6 +93,17 @@ class MfOut(ctypes.Structure):
     ]
 
 
+class GroupShard(ctypes.Structure):
+    _fields_ = [("R", c_vp), ("Lt", c_vp), ("U", c_vp), ("n_local", c_i64), ("ld", c_i64),
+                ("row_offset", c_i64)]
+
+
+class GroupDenseArgs(ctypes.Structure):
+    _fields_ = [("dtype", c_i32), ("lazy_block", c_i32), ("m", c_i64), ("steps", c_i64),
+                ("ldu", c_i64), ("stop_tol", c_dbl), ("uniforms", ctypes.POINTER(c_dbl)),
+                ("n_uniforms", c_i64), ("shards", ctypes.POINTER(GroupShard))]
+
+
 class CauchyArgs(ctypes.Structure):
     _fields_ = [
         ("rule", c_i32), ("p", c_i32), ("n", c_i64), ("m", c_i64), ("rank", c_i64),
@@ -184,6 +195,10 @@ SIGNATURES = {
     "rplu_kernel_launch_count": (c_i64, []),
     "rplu_mf_run": (ctypes.c_int, [c_vp, ctypes.POINTER(MfArgs), ctypes.POINTER(MfOut)]),
     "rplu_upload": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "rplu_group_create": (ctypes.c_int, [c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_vp)]),
+    "rplu_group_destroy": (ctypes.c_int, [c_vp]),
+    "rplu_group_dense_run": (ctypes.c_int, [c_vp, ctypes.POINTER(GroupDenseArgs),
+                                            ctypes.POINTER(DenseOut)]),
     "rplu_lu_error": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
                                      c_i64, c_i64, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                                      c_vp]),

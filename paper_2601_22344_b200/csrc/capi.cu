@@ -1,6 +1,7 @@
 // C ABI entry points (include/rplu_b200.h): context, errors, argument
 // validation with the reference's error classes, dispatch to the paths.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -383,8 +384,27 @@ static int shard_check(rplu_ctx* ctx, const rplu_shard_args* a) {
   return RPLU_OK;
 }
 
+// fp64 delayed-update shards use the Gram-form masses (RPLU_GRAM=0 disables)
+static bool shard_gram(const rplu_shard_args* a) {
+  static const bool env = [] {
+    const char* e = getenv("RPLU_GRAM");
+    return !(e && e[0] == '0');
+  }();
+  return env && a->dtype == RPLU_F64 && a->lazy_block != 0;
+}
+
 static int shard_block(const rplu_shard_args* a) {
-  return a->lazy_block < 0 ? dense_lazy_block_default(a->dtype) : a->lazy_block;
+  if (a->lazy_block >= 0) return a->lazy_block;
+  return shard_gram(a) ? dense_gram_block() : dense_lazy_block_default(a->dtype);
+}
+
+static double* shard_gram_buf(rplu_ctx* ctx, const rplu_shard_args* a, int* rc) {
+  *rc = RPLU_OK;
+  if (!shard_gram(a)) return nullptr;
+  if ((*rc = ctx->gram.ensure(sizeof(double) * (3 * (size_t)std::max<long long>(a->n_local, 1) +
+                                                256))))
+    return nullptr;
+  return reinterpret_cast<double*>(ctx->gram.ptr);
 }
 
 static ShardParams shard_params(rplu_ctx* ctx, const rplu_shard_args* a) {
@@ -447,6 +467,9 @@ int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_tota
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
                                  masses, nullptr, 0, false, s)))
       return rc;
+    double* gram = shard_gram_buf(ctx, a, &rc);
+    if (rc) return rc;
+    if (gram && (rc = dense_gram_reset_launch(a->n_local, masses, gram, s))) return rc;
   }
   return shard_total_impl(masses, a->n_local, local_total, nullptr, s);
 }
@@ -497,8 +520,11 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   if (p.lazy_block > 0) {
     const long long b = p.lazy_block, t0 = (t / b) * b;
     const bool flush = (t + 1 - t0 == b) || (t == a->steps - 1);
+    double* gram = shard_gram_buf(ctx, a, &rc);
+    if (rc) return rc;
     if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
-                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, s)))
+                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, s,
+                                     gram)))
       return rc;
   } else if (a->n_local > 0) {
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,

@@ -2136,13 +2136,46 @@ static int lazy_step_t(const DenseParams& p, bool pivcol, bool flush, cudaStream
     const int blocks = (int)((p.n + 255) / 256 < 1024 ? (p.n + 255) / 256 : 1024);
     lazy_pivcol_kernel<T><<<blocks, 256, 0, s>>>(p);
   }
-  return lazy_pass<T>(p, flush, s);
+  if (p.gram && !flush) return gram_step<T>(p, p.t0, s);
+  if (int rc = lazy_pass<T>(p, flush, s)) return rc;
+  if (p.gram && flush && !p.force) {
+    const int rb = (int)std::min<long long>((p.n + 255) / 256, 1024);
+    gram_reset_kernel<<<rb, 256, 0, s>>>(p);
+  }
+  return RPLU_OK;
 }
+
+static void set_gram(DenseParams& p, double* gram) {
+  if (!gram) return;
+  p.gram = 1;
+  p.m0 = gram;
+  p.lin = gram + p.n;
+  p.quad = gram + 2 * p.n;
+  p.gmat = gram + 3 * p.n;
+}
+
+int dense_gram_reset_launch(long long n, double* masses, double* gram, cudaStream_t s) {
+  if (n == 0) return RPLU_OK;
+  DenseParams p{};
+  p.n = n;
+  p.masses = masses;
+  set_gram(p, gram);
+  gram_reset_kernel<<<(int)std::min<long long>((n + 255) / 256, 1024), 256, 0, s>>>(p);
+  RPLU_CUDA(cudaGetLastError());
+  return RPLU_OK;
+}
+
+int dense_gram_block() { return gram_block(); }
 
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
-                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s) {
+                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s,
+                           double* gram) {
   if (n == 0) return RPLU_OK;
+  if (gram && dtype != RPLU_F64) {
+    set_error("Gram-mass delayed updates are fp64 only");
+    return RPLU_ERR_ARG;
+  }
   DenseParams p{};
   p.R = R;
   p.ld = ld;
@@ -2157,6 +2190,7 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   p.t0 = t0;
   p.lazy = 1;
   p.force = force ? 1 : 0;
+  set_gram(p, gram);
   int rc;
   switch (dtype) {
     case RPLU_F64: rc = lazy_step_t<double>(p, pivcol, flush, s); break;

@@ -88,9 +88,15 @@ constexpr int kLazyMaxBlock = 16;  // longest delayed-update block
 // Delayed-update pieces on a row block, from dense.cu: (pivcol) the pivot
 // column L[:,t] rebuilt from R^(t0) and the pending terms, then the pass
 // (masses of R^(t+1); flush writes it).  force runs the pass after a stop.
+// gram (fp64 only; nullptr: applied-term masses): [m0 | lin | quad](n) + 256
+// doubles of U Gram -- the Gram-form masses of dense.cu (non-flush steps
+// run the dot pass, flushes reset m0 / lin / quad)
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
-                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s);
+                           long long t0, bool pivcol, bool flush, bool force, cudaStream_t s,
+                           double* gram = nullptr);
+int dense_gram_reset_launch(long long n, double* masses, double* gram, cudaStream_t s);
+int dense_gram_block();
 int dense_lazy_block_default(int dtype, bool fused = false);
 
 // Sharded Cauchy-like steps (cauchy.cu).

@@ -36,7 +36,7 @@ from .accessors import CapabilityError
 from .dense_pivots import EliminationTrace, PivotRule
 from .rng import UniformBlock
 
-__all__ = ["shard_rows", "run_sharded", "run_sharded_graph", "sharded_eliminate",
+__all__ = ["shard_rows", "run_sharded", "run_sharded_graph", "sharded_eliminate", "group_eliminate",
            "CudaShardBackend", "run_sharded_cauchy", "CudaCauchyShardBackend",
            "sharded_structured_eliminate"]
 
@@ -249,6 +249,74 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
         tol_stop=res["tol_stop"], near_boundary_draws=res["near_boundary_draws"],
         uniforms_consumed=res["uniforms_consumed"], host=False)
     tr.lazy_block = backend.lazy_block_used   # 0: eager updates
+    return tr
+
+
+def group_eliminate(A, rule, steps, devices=(0,), stop_tol=0.0, compute_dtype=None,
+                    update="eager"):
+    """Row-block sharded RPLU across ``devices`` from ONE process, driven by
+    the library's C loop (``rplu_group_dense_run``: NCCL communicators from
+    ncclCommInitAll, grouped allreduce / allgather per step -- no
+    torch.distributed, no Python per step).  ``A`` (host or device) is split
+    into contiguous row blocks in device order.  Returns an EliminationTrace
+    with L gathered on devices[0] and U / pivots / resid_fro replicated.
+    ``update``: "eager" (fused update every step) or "lazy" (delayed updates,
+    fp64 with Gram-form masses)."""
+    if update not in ("eager", "lazy"):
+        raise ValueError(f"update must be 'eager' or 'lazy', not {update!r}")
+    if isinstance(rule, str):
+        rule = PivotRule(rule)
+    if rule.tag != "rplu":
+        raise CapabilityError("the sharded path implements rule 'rplu'")
+    devices = [int(d) for d in devices]
+    G = len(devices)
+    host = _device.as_device_matrix(A, dtype=compute_dtype, device=devices[0])
+    n, m = host.shape
+    if not 0 <= steps <= min(n, m):
+        raise ValueError(f"steps {steps} out of range [0, {min(n, m)}]")
+    vec = _device.vec_of(host.dtype)
+    ldu = ((m + vec - 1) // vec) * vec
+    lib = _ffi.load_library()
+    bufs, shards = [], (_ffi.GroupShard * G)()
+    for d, dev in enumerate(devices):
+        lo, hi = shard_rows(n, G, d)
+        R = torch.zeros((hi - lo, ldu), dtype=host.dtype, device=f"cuda:{dev}")
+        R[:, :m].copy_(host[lo:hi])
+        Lt = torch.empty((max(steps, 1), max(hi - lo, 1)), dtype=host.dtype, device=R.device)
+        U = torch.empty((max(steps, 1) + 1, ldu), dtype=host.dtype, device=R.device)
+        bufs.append((R, Lt, U, lo, hi))
+        shards[d] = _ffi.GroupShard(R=R.data_ptr(), Lt=Lt.data_ptr(), U=U.data_ptr(),
+                                    n_local=hi - lo, ld=ldu, row_offset=lo)
+    for dev in devices:
+        torch.cuda.synchronize(dev)
+    block = UniformBlock(rule.rng, 2 * steps + 2)
+    args = _ffi.GroupDenseArgs(dtype=_device.DTYPE_IDS[host.dtype],
+                               lazy_block=0 if update == "eager" else -1, m=m, steps=steps,
+                               ldu=ldu, stop_tol=float(stop_tol), uniforms=block.pointer(),
+                               n_uniforms=block.values.size, shards=shards)
+    pivots = np.zeros(2 * max(steps, 1), dtype=np.int64)
+    resid = np.zeros(steps + 1)
+    out = _ffi.DenseOut(pivots=pivots.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                        resid_fro=resid.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    grp = ctypes.c_void_p()
+    _ffi.check(lib.rplu_group_create(G, (ctypes.c_int32 * G)(*devices), ctypes.byref(grp)))
+    try:
+        status = lib.rplu_group_dense_run(grp, ctypes.byref(args), ctypes.byref(out))
+        block.commit(out.uniforms_consumed)
+        _ffi.check(status)
+    finally:
+        lib.rplu_group_destroy(grp)
+    k = int(out.steps_done)
+    L = torch.cat([Lt[:k, :hi - lo].T.to(f"cuda:{devices[0]}") for (_, Lt, _, lo, hi) in bufs],
+                  dim=0)
+    Rfull = torch.cat([R[:, :m].to(f"cuda:{devices[0]}") for (R, _, _, _, _) in bufs], dim=0)
+    tr = EliminationTrace(
+        pivots=[(int(pivots[2 * t]), int(pivots[2 * t + 1])) for t in range(k)], L=L,
+        U=bufs[0][2][:k, :m], resid_fro=resid[:k + 1].copy(), residual=Rfull, steps=k,
+        clean_early_stop=bool(out.clean_early_stop), tol_stop=bool(out.tol_stop),
+        near_boundary_draws=int(out.near_boundary_draws),
+        uniforms_consumed=int(out.uniforms_consumed), host=False)
+    tr.lazy_block = int(out.lazy_block)
     return tr
 
 

@@ -67,6 +67,25 @@ def test_world1_lazy_equals_eager(dtype, lazy_block, cuda_device):
         np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-13)
 
 
+@pytest.mark.parametrize("update", ["eager", "lazy"])
+def test_c_group_driver_world1(update, cuda_device):
+    """rplu_group_dense_run (the C loop over NCCL from ncclCommInitAll, no
+    torch.distributed) at one device: bit-identical to eliminate."""
+    from paper_2601_22344_b200.distributed import group_eliminate
+    A = torch.from_numpy(gen.c1_dense(4, n=600, m=450)).cuda()
+    ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(4)), 120, update="eager")
+    rng = rp.RngState(4)
+    tr = group_eliminate(A, rp.PivotRule("rplu", rng), 120, devices=[0], update=update)
+    assert tr.pivots == ref.pivots
+    assert torch.equal(tr.L, ref.L) and torch.equal(tr.U, ref.U)
+    assert torch.equal(tr.residual_device, ref.residual_device)
+    np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-12)
+    assert (tr.lazy_block > 0) == (update == "lazy")
+    ref2 = rp.RngState(4)
+    rp.eliminate(A, rp.PivotRule("rplu", ref2), 120)
+    assert rng.uniform() == ref2.uniform()
+
+
 def test_lazy_rejects_graph_and_device_steps(cuda_device):
     A = torch.from_numpy(gen.c1_dense(2, n=64, m=64)).cuda()
     with pytest.raises(ValueError):
