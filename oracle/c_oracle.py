@@ -105,3 +105,63 @@ def replay_c(A, pivots, threads=None, dtype=np.float64):
     R = np.array(A, dtype=dtype, order="C")
     forced = np.array(pivots, dtype=np.int64).reshape(-1, 2)
     return _run(R, "rplu", len(forced), None, forced, 0.0, threads, False)
+
+
+def structured_eliminate_c(x, y, G, B, rule, rank, seed=None, gen=None, stop_tol=0.0,
+                           keep_steps=False, threads=None):
+    """cauchy.py:177-256 (plan=None) in C (oracle/c/cauchy_oracle.c): same
+    result dict as ``rplu_oracle.structured_eliminate`` (row / column
+    indices, bound maxes / sums, stop flags, kept (c, r, a) steps, final
+    G / B, margins of the draws) plus ``uniforms_consumed``."""
+    lib = _load()
+    if not hasattr(lib, "_cauchy_typed"):
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        lib.oracle_cauchy.argtypes = [P, P, P, P, i64, i64, ctypes.c_int, i64, ctypes.c_int, P,
+                                      i64, ctypes.c_double, ctypes.c_int, P, P, P, P, P, P, P,
+                                      P, P]
+        lib.oracle_cauchy.restype = ctypes.c_int
+        lib._cauchy_typed = True
+    if rule not in ("rplu", "c2plu"):
+        raise ValueError(f"unknown structured rule {rule!r}")
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.complex128).ravel())
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.complex128).ravel())
+    Gc = np.array(G, dtype=np.complex128, order="C")
+    Bt = np.array(np.asarray(B, dtype=np.complex128).T, order="C")   # m x p
+    n, p = Gc.shape
+    m = Bt.shape[0]
+    k = max(rank, 1)
+    uniforms = np.zeros(1)
+    if rule == "rplu":
+        g = gen if gen is not None else uniform_stream(seed)
+        uniforms = g.random(3 * k)
+    rows = np.zeros(k, dtype=np.int64)
+    cols = np.zeros(k, dtype=np.int64)
+    bmax = np.zeros(k)
+    bsum = np.zeros(k)
+    mg = np.full(k, np.inf)
+    R = np.zeros((k, m), dtype=np.complex128) if keep_steps else None
+    C = np.zeros((k, n), dtype=np.complex128) if keep_steps else None
+    av = np.zeros(k, dtype=np.complex128) if keep_steps else None
+    out = np.zeros(5, dtype=np.int64)
+    st = lib.oracle_cauchy(_ptr(x), _ptr(y), _ptr(Gc), _ptr(Bt), n, m, p, rank,
+                           0 if rule == "rplu" else 1, _ptr(uniforms),
+                           uniforms.size if rule == "rplu" else 0, float(stop_tol),
+                           int(threads or os.cpu_count() or 1), _ptr(rows), _ptr(cols),
+                           _ptr(bmax), _ptr(bsum), _ptr(mg), _ptr(R), _ptr(C), _ptr(av),
+                           _ptr(out))
+    if st == -1:
+        raise ZeroDivisionError(f"pivot at step {int(out[4])} is numerically zero")
+    if st == -2:
+        raise ValueError(f"rank {rank} out of range [0, {min(n, m)}]")
+    if st:
+        raise RuntimeError(f"oracle_cauchy failed ({st})")
+    done = int(out[0])
+    nb = done + (1 if (out[2] or out[3]) else 0)
+    res = dict(row_indices=[int(v) for v in rows[:done]], col_indices=[int(v) for v in cols[:done]],
+               bound_maxes=list(bmax[:nb]), bound_sums=list(bsum[:nb]), tol_stop=bool(out[2]),
+               degenerate_stop=bool(out[3]), margins=mg[:done], uniforms_consumed=int(out[1]),
+               G=Gc, B=Bt.T.copy(), steps=[])
+    if keep_steps:
+        res["steps"] = [(C[t].copy(), R[t].copy(), complex(av[t])) for t in range(done)]
+    return res

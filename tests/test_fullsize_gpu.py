@@ -141,3 +141,33 @@ def test_c2_full_rank_200(cuda_device):
                   near_boundary_draws=tr.near_boundary_draws,
                   min_margin=float(np.min(ref["margins"])))
     assert worst_l <= 1e-10 and worst_u <= 1e-10
+
+
+def test_c4_reduced_16384_rank64(cuda_device):
+    """SURVEY §8(d) C4 parity bar at its stated reduced size (n = m = 16384,
+    p = 4, 64 pivots) against the C restatement of the exact-norm loop:
+    pivots equal (a divergence only near a CDF boundary), bound maxes /
+    sums to 1e-11, pivot rows U = r and columns L = c / a to 1e-10."""
+    x, y, G, B = gen.c4_cauchy_like(0, n=16384, p=4)
+    K = 64
+    tr = rp.structured_eliminate(rp.CauchyLikeMatrix(x, y, G, B, check_points=False), "rplu", K,
+                                 rng=rp.RngState(0), keep_steps=True)
+    ref = c_oracle.structured_eliminate_c(x, y, G, B, "rplu", K, seed=0, keep_steps=True)
+    got = list(zip(tr.row_indices, tr.col_indices))
+    want = list(zip(ref["row_indices"], ref["col_indices"]))
+    t = next((s for s, (a, b) in enumerate(zip(got, want)) if a != b), None)
+    if t is not None:
+        assert ref["margins"][t] <= oracle.NEAR_REL, f"divergence at {t} not near a boundary"
+    k = K if t is None else t
+    np.testing.assert_allclose(tr.bound_maxes[:k], ref["bound_maxes"][:k], rtol=1e-11)
+    np.testing.assert_allclose(tr.bound_sums[:k], ref["bound_sums"][:k], rtol=1e-11)
+    wl = wu = 0.0
+    for s in range(k):
+        c, r, a = tr.steps[s]
+        rc, rr, ra = ref["steps"][s]
+        wu = max(wu, np.abs(r - rr).max() / np.abs(rr).max())
+        wl = max(wl, np.abs(c / a - rc / ra).max() / np.abs(rc / ra).max())
+    record_parity("c4_reduced_16384_k64", first_divergence=t, steps=k, L_rel=wl, U_rel=wu,
+                  near_boundary_draws=tr.near_boundary_draws,
+                  min_margin=float(np.min(ref["margins"])))
+    assert wl <= 1e-10 and wu <= 1e-10

@@ -308,3 +308,29 @@ def test_oracle_certified_bounds_match_reference():
         plan = tb.build_plan(x, y, nu=case["nu"], leaf_size=case["leaf_size"])
         u = oracle.plan.certified_upper_bounds(plan, arr[name + "_G"], arr[name + "_B"])
         np.testing.assert_allclose(u, arr[name + "_u0"], rtol=1e-13)
+
+
+def test_cauchy_c_oracle_matches_reference():
+    """The C restatement of structured_eliminate(plan=None)
+    (oracle/c/cauchy_oracle.c) against the reference's Cauchy goldens:
+    pivots, stop flags and uniform stream identical, bound maxes / sums to
+    1e-11, kept pivot rows to 1e-10 of their scale."""
+    from oracle import c_oracle
+    info, arr = load_golden("cauchy")
+    for c in info["cases"]:
+        nm = c["name"]
+        x, y, G, B = (arr[nm + k] for k in ("_x", "_y", "_G", "_B"))
+        gen_ = oracle.uniform_stream(c["seed"]) if c["seed"] is not None else None
+        o = c_oracle.structured_eliminate_c(x, y, G, B, c["rule"], c["rank"], gen=gen_,
+                                            stop_tol=c["stop_tol"], keep_steps=True)
+        assert o["row_indices"] == c["rows"] and o["col_indices"] == c["cols"], nm
+        assert o["tol_stop"] == c["tol_stop"] and o["degenerate_stop"] == c["degenerate_stop"]
+        np.testing.assert_allclose(o["bound_maxes"], c["bound_maxes"], rtol=1e-11)
+        np.testing.assert_allclose(o["bound_sums"], c["bound_sums"], rtol=1e-11)
+        for t, (_, r, _) in enumerate(o["steps"]):
+            ref = arr[nm + "_r"][t]
+            assert np.abs(r - ref).max() <= 1e-10 * np.abs(ref).max()
+        if c["seed"] is not None:
+            g2 = oracle.uniform_stream(c["seed"])
+            g2.random(o["uniforms_consumed"])
+            assert float(g2.random()) == c["next_uniform"]
