@@ -159,10 +159,10 @@ typedef struct rplu_shard_args {
   int32_t dtype;          /* RPLU_F32 | RPLU_F64 | RPLU_C128 */
   int32_t world, rank;    /* shard count and this shard's index */
   int32_t lazy_block;     /* 0: eager K3 update; > 0 (<= 16): delayed-update
-                           * block (flush every lazy_block steps; needs the
-                           * host step loop, t >= 0, and 16-byte aligned rows
-                           * of R and U); < 0: the default (fp64: Gram-form
-                           * masses, flush every 16 steps; else 6 / 5) */
+                           * block (flush every lazy_block steps; 16-byte
+                           * aligned rows of R and U); < 0: the default (fp64:
+                           * Gram-form masses, flush every 16 steps; else
+                           * 6 / 5).  rplu_shard_lazy_block resolves it. */
   int64_t n_local, m;     /* local row block shape */
   int64_t ld;             /* row stride of R (elements) */
   int64_t row_offset;     /* global index of local row 0 */
@@ -187,9 +187,16 @@ int rplu_shard_begin(rplu_ctx* ctx, const rplu_shard_args* a, double* local_tota
 int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const double* totals,
                       void* msg);
 /* Post the reduced message (state + U[t,:]), K3 fused update of the local
- * rows, local total; advances the device step counter. */
+ * rows, local total; advances the device step counter.  Delayed-update
+ * shards with t < 0: -1 - t is the step's position inside its block of
+ * lazy_block steps (the number of pending terms and the flush at the last
+ * position are fixed at launch, the absolute step comes from the device
+ * counter), so one whole block -- kernels and collectives -- is captured
+ * once and replayed; a trailing partial block runs with explicit t. */
 int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const void* msg,
                       double* local_total);
+/* The flush interval the shard calls use for these arguments (0: eager). */
+int rplu_shard_lazy_block(const rplu_shard_args* a);
 /* 1 if the loop is still running (synchronizes the stream). */
 int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active);
 /* Copy pivots / residual norms / flags to the host (out as for rplu_dense_run). */

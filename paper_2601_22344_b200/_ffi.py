@@ -221,6 +221,7 @@ SIGNATURES = {
     "rplu_shard_select": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),
     "rplu_shard_update": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), c_i64, c_vp, c_vp]),
     "rplu_shard_active": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs), ctypes.POINTER(c_i32)]),
+    "rplu_shard_lazy_block": (ctypes.c_int, [ctypes.POINTER(ShardArgs)]),
     "rplu_shard_finish": (ctypes.c_int, [c_vp, ctypes.POINTER(ShardArgs),
                                          ctypes.POINTER(DenseOut)]),
     "rplu_cauchy_shard_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(CauchyShardArgs), c_vp]),

@@ -488,13 +488,8 @@ int rplu_shard_select(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   p.t = t < 0 ? -1 : t;
   p.totals = totals;
   p.msg = msg;
-  if (p.lazy_block > 0) {
-    if (t < 0) {
-      set_error("rplu_shard_select: the delayed-update loop needs explicit steps (t >= 0)");
-      return RPLU_ERR_ARG;
-    }
+  if (p.lazy_block > 0)   // t < 0: the step comes from the device counter (captured blocks)
     return shard_lazy_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
-  }
   return shard_select_impl(p, reinterpret_cast<cudaStream_t>(a->stream));
 }
 
@@ -512,19 +507,25 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   ShardParams p = shard_params(ctx, a);
   p.t = t < 0 ? -1 : t;
   p.msg = const_cast<void*>(msg);
-  if (p.lazy_block > 0 && t < 0) {
-    set_error("rplu_shard_update: the delayed-update loop needs explicit steps (t >= 0)");
+  // Delayed-update shards with t < 0 (captured blocks): -1 - t is the step's
+  // position inside its block; the absolute step comes from the device
+  // counter, so one captured block of lazy_block steps can be replayed.  Only
+  // whole blocks run this way (the flush sits at the block's last position).
+  const long long b = p.lazy_block;
+  const long long pos = t < 0 ? -1 - t : t % (b > 0 ? b : 1);
+  if (b > 0 && pos >= b) {
+    set_error("rplu_shard_update: block position out of range");
     return RPLU_ERR_ARG;
   }
   if ((rc = shard_post_impl(p, s))) return rc;
-  if (p.lazy_block > 0) {
-    const long long b = p.lazy_block, t0 = (t / b) * b;
-    const bool flush = (t + 1 - t0 == b) || (t == a->steps - 1);
+  if (b > 0) {
+    const bool rel = t < 0;
+    const bool flush = (pos + 1 == b) || (!rel && t == a->steps - 1);
     double* gram = shard_gram_buf(ctx, a, &rc);
     if (rc) return rc;
     if ((rc = dense_lazy_step_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U,
-                                     a->ldu, p.masses, p.st, t, t0, true, flush, false, s,
-                                     gram)))
+                                     a->ldu, p.masses, p.st, rel ? pos : t, rel ? 0 : t - pos,
+                                     true, flush, false, s, gram, rel, a->steps)))
       return rc;
   } else if (a->n_local > 0) {
     if ((rc = dense_sweep_launch(a->dtype, a->R, a->ld, a->n_local, a->m, a->Lt, a->U, a->ldu,
@@ -533,6 +534,8 @@ int rplu_shard_update(rplu_ctx* ctx, const rplu_shard_args* a, int64_t t, const 
   }
   return shard_total_impl(p.masses, a->n_local, local_total, p.st, s);
 }
+
+int rplu_shard_lazy_block(const rplu_shard_args* a) { return a ? shard_block(a) : 0; }
 
 int rplu_shard_active(rplu_ctx* ctx, const rplu_shard_args* a, int32_t* active) {
   int rc;

@@ -31,10 +31,203 @@ namespace rplu {
 // K7: out[i] (+split partial) = sum_j A_ij v_j, or sum_j A_ij^2 (SQUARE, v
 // ignored) for row norms.  Row side in registers, column side (q_j, v_j) in
 // shared-memory tiles; columns split across gridDim.y for small n.
+//
+// Two forms of the exponent, chosen on the device from the points' bounding
+// box (gauss_geo_kernel; no host round trip -- both kernels are launched and
+// the one that does not apply exits at once):
+//  * difference form (gauss_gemv_kernel): -|p'-q'|^2 from three differences,
+//    16 FP64-pipe operations per entry, entries to ~1.5 ulp + d2 2^-53;
+//  * dot-product form (gauss_gemv_dot_kernel): with the points centred on the
+//    middle c0 of Q's bounding box and y the exponent in table units
+//    (K = 32/ln2),  y = a_i + b_j + p~_i . q~~_j,  a_i = -K |p~_i|^2,
+//    b_j = -K |q~_j|^2,  q~~_j = 2K q~_j  -- three DFMA and one DADD, then
+//    exp_tab_units: 14 FP64-pipe operations per entry and no compare/select.
+//    y carries an absolute rounding error of a few eps K r2 (r2 = the largest
+//    squared scaled distance of a point from c0), i.e. a relative entry error
+//    <= ~10 eps K r2 ln2/32; the form is taken only while K r2 < 8000 (then
+//    also y > -32000: no underflow cut), so entries agree with the difference
+//    form to <= 2e-13 relative in the worst case (C5: K r2 ~ 5600, typical
+//    error ~3e-14, below the sqrt(m) eps of the row sum itself).  The centre
+//    depends on Q only, so a row-sharded apply produces the same bits as the
+//    unsharded one.  Pivot rows / columns and the core (K8) always use the
+//    difference form.
+constexpr double kExpK = 46.16624130844683;   // 32 / ln 2
+constexpr double kDotRange = 8000.0;
+
+// per-CTA bounding boxes: part[b][0..5] = lo/hi of Q, part[b][6..11] = lo/hi of P u Q
+__global__ void __launch_bounds__(256) gauss_bbox_kernel(GaussOp op, double* __restrict__ part) {
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double ql[3] = {inf, inf, inf}, qh[3] = {-inf, -inf, -inf};
+  double al[3] = {inf, inf, inf}, ah[3] = {-inf, -inf, -inf};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < op.m; k += stride) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double x = op.Q[k * 3 + c];
+      ql[c] = fmin(ql[c], x);
+      qh[c] = fmax(qh[c], x);
+    }
+  }
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < op.n; k += stride) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double x = op.P[k * 3 + c];
+      al[c] = fmin(al[c], x);
+      ah[c] = fmax(ah[c], x);
+    }
+  }
+  __shared__ double red[8][12];
+  double vals[12];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vals[c] = ql[c];
+    vals[3 + c] = -qh[c];
+    vals[6 + c] = fmin(al[c], ql[c]);
+    vals[9 + c] = -fmax(ah[c], qh[c]);
+  }
+#pragma unroll
+  for (int e = 0; e < 12; ++e) {   // every slot is a minimum (upper bounds negated)
+    double x = vals[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][e] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 12) {
+    double x = red[0][threadIdx.x];
+    for (int w = 1; w < 8; ++w) x = fmin(x, red[w][threadIdx.x]);
+    part[blockIdx.x * 12 + threadIdx.x] = x;
+  }
+}
+
+// geo = [c0x, c0y, c0z, K c^2 r2]: c0 the middle of Q's box, r2 the largest
+// squared distance of a corner of the (P u Q) box from c0.  Non-finite
+// coordinates give a non-finite range, which selects the difference form.
+__global__ void gauss_geo_kernel(const double* __restrict__ part, int nparts, double c,
+                                 double* __restrict__ geo) {
+  __shared__ double mn[12];
+  if (threadIdx.x < 12) {
+    double x = part[threadIdx.x];
+    for (int b = 1; b < nparts; ++b) x = fmin(x, part[b * 12 + threadIdx.x]);
+    mn[threadIdx.x] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double c0 = 0.5 * (mn[k] - mn[3 + k]);
+      const double d = fmax(fabs(mn[6 + k] - c0), fabs(-mn[9 + k] - c0)) * c;
+      geo[k] = c0;
+      r2 += d * d;
+    }
+    const double range = kExpK * r2;
+    geo[3] = range == range ? range : __longlong_as_double(0x7ff0000000000000LL);
+  }
+}
+
+template <int RPT, int TJ, bool SQUARE, int CU = 2>
+__global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
+                                                             const double* __restrict__ v,
+                                                             double* __restrict__ partial,
+                                                             int splits,
+                                                             const double* __restrict__ geo) {
+  constexpr int NT = 256;
+  if (!(geo[3] < kDotRange)) return;
+  __shared__ __align__(16) double sq[TJ * 6];
+  const double c0x = geo[0], c0y = geo[1], c0z = geo[2];
+  const long long row_base = (long long)blockIdx.x * NT * RPT;
+  const long long cols_per = (op.m + splits - 1) / splits;
+  const long long j0 = (long long)blockIdx.y * cols_per;
+  const long long j1 = min(op.m, j0 + cols_per);
+  const ExpTab tl = exp2tab_lane_comp();
+  double px[RPT], py[RPT], pz[RPT], pa[RPT], acc[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    long long ii = i < op.n ? i : 0;
+    px[r] = op.c * (op.P[ii * 3 + 0] - c0x);
+    py[r] = op.c * (op.P[ii * 3 + 1] - c0y);
+    pz[r] = op.c * (op.P[ii * 3 + 2] - c0z);
+    pa[r] = -kExpK * fma(pz[r], pz[r], fma(py[r], py[r], px[r] * px[r]));
+    acc[r] = 0.0;
+  }
+  for (long long jt = j0; jt < j1; jt += TJ) {
+    const int cnt = (int)min((long long)TJ, j1 - jt);
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < cnt; cc += NT) {
+      const long long j = jt + cc;
+      const double qx = op.c * (op.Q[j * 3 + 0] - c0x);
+      const double qy = op.c * (op.Q[j * 3 + 1] - c0y);
+      const double qz = op.c * (op.Q[j * 3 + 2] - c0z);
+      sq[cc * 6 + 0] = (2.0 * kExpK) * qx;
+      sq[cc * 6 + 1] = (2.0 * kExpK) * qy;
+      sq[cc * 6 + 2] = (2.0 * kExpK) * qz;
+      sq[cc * 6 + 3] = -kExpK * fma(qz, qz, fma(qy, qy, qx * qx));
+      sq[cc * 6 + 4] = SQUARE ? 1.0 : v[j];
+    }
+    __syncthreads();
+    // CU columns x RPT rows = E independent entries per trip, every stage
+    // issued for all E before the next (interleaved dependency chains)
+    constexpr int E = CU * RPT;
+    int cc = 0;
+    for (; cc + CU <= cnt; cc += CU) {
+      double y[E], e[E], vj[CU];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const double qz = sq[(cc + u) * 6 + 2], qb = sq[(cc + u) * 6 + 3];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(pz[r], qz, qb);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const double qy = sq[(cc + u) * 6 + 1];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(py[r], qy, y[u * RPT + r]);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const double qx = sq[(cc + u) * 6 + 0];
+        vj[u] = sq[(cc + u) * 6 + 4];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(px[r], qx, y[u * RPT + r]);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u)
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) y[u * RPT + r] += pa[r];
+      exp_tab_units_v<E>(y, e, tl);
+#pragma unroll
+      for (int u = 0; u < CU; ++u)
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+          acc[r] = SQUARE ? fma(e[u * RPT + r], e[u * RPT + r], acc[r])
+                          : fma(e[u * RPT + r], vj[u], acc[r]);
+    }
+    for (; cc < cnt; ++cc) {   // tile tail (cnt % CU columns)
+      const double qx = sq[cc * 6 + 0], qy = sq[cc * 6 + 1], qz = sq[cc * 6 + 2];
+      const double qb = sq[cc * 6 + 3], vj = sq[cc * 6 + 4];
+      double y[RPT], e[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        y[r] = fma(px[r], qx, fma(py[r], qy, fma(pz[r], qz, qb))) + pa[r];
+      exp_tab_units_v<RPT>(y, e, tl);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) acc[r] = SQUARE ? fma(e[r], e[r], acc[r]) : fma(e[r], vj, acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    long long i = row_base + threadIdx.x + (long long)r * NT;
+    if (i < op.n) partial[(long long)blockIdx.y * op.n + i] = acc[r];
+  }
+}
+
 template <int RPT, int TJ, bool SQUARE>
 __global__ void __launch_bounds__(256) gauss_gemv_kernel(GaussOp op, const double* __restrict__ v,
-                                                         double* __restrict__ partial, int splits) {
+                                                         double* __restrict__ partial, int splits,
+                                                         const double* __restrict__ geo) {
   constexpr int NT = 256;
+  if (geo[3] < kDotRange) return;   // the dot-product form below runs instead
   __shared__ double sq[TJ * 4];
   const long long row_base = (long long)blockIdx.x * NT * RPT;
   const long long cols_per = (op.m + splits - 1) / splits;
@@ -197,13 +390,33 @@ static int gemv_splits(long long n, long long m, int rows_per_cta, int sms, int 
   return (int)best;
 }
 
+// RPLU_GEMV_CU: columns per interleaved group of the dot kernel (1, 2 or 4)
+static int gemv_cu() {
+  static const int cu = [] {
+    const char* e = getenv("RPLU_GEMV_CU");
+    const int c = e ? atoi(e) : 4;   // measured at 1e6: 1 -> 1099 ms, 2 -> 1049, 4 -> 1021
+    return (c == 1 || c == 2) ? c : 4;
+  }();
+  return cu;
+}
+
 template <int RPT>
 static void gemv_launch(const GaussOp& op, const double* v, double* part, int splits, bool square,
-                        cudaStream_t s) {
+                        const double* geo, cudaStream_t s) {
   constexpr int TJ = 256;
   dim3 grid((unsigned)((op.n + 256 * RPT - 1) / (256 * RPT)), (unsigned)splits);
-  if (square) gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits);
-  else gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits);
+  const int cu = gemv_cu();
+  if (square) {
+    if (cu == 1) gauss_gemv_dot_kernel<RPT, TJ, true, 1><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    else if (cu == 2) gauss_gemv_dot_kernel<RPT, TJ, true, 2><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    else gauss_gemv_dot_kernel<RPT, TJ, true, 4><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+  } else {
+    if (cu == 1) gauss_gemv_dot_kernel<RPT, TJ, false, 1><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    else if (cu == 2) gauss_gemv_dot_kernel<RPT, TJ, false, 2><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    else gauss_gemv_dot_kernel<RPT, TJ, false, 4><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+  }
 }
 
 // rows per thread of K7 (RPLU_GEMV_RPT experiment override: 1, 2 or 4)
@@ -216,35 +429,72 @@ static int gemv_rpt() {
   return v;
 }
 
+// RPLU_GEMV_DOT=0 forces the difference form (experiment / comparison knob)
+static bool gemv_dot_enabled() {
+  static bool v = [] {
+    const char* e = getenv("RPLU_GEMV_DOT");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+__global__ void gauss_geo_off_kernel(double* geo) {
+  if (threadIdx.x == 0) geo[3] = __longlong_as_double(0x7ff0000000000000LL);
+}
+
 int gauss_gemv_impl(rplu_ctx* ctx, const GaussOp& op, const double* v, double* out, bool square,
                     cudaStream_t s, float* ms) {
   const int rpt = gemv_rpt();
-  static int per_sm[3] = {0, 0, 0};   // resident CTAs per SM of each RPT instantiation
+  // resident CTAs per SM of the kernel that normally runs (the dot-product
+  // form; the split count balances its last wave)
+  static int per_sm[3] = {0, 0, 0};
   const int slot = rpt == 1 ? 0 : (rpt == 2 ? 1 : 2);
   if (!per_sm[slot]) {
     int b = 0;
-    if (rpt == 1)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<1, 256, false>, 256, 0);
-    else if (rpt == 2)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<2, 256, false>, 256, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<4, 256, false>, 256, 0);
+    const bool dot = gemv_dot_enabled();
+    const int cu = gemv_cu();
+#define RPLU_OCC(R)                                                                              \
+  (dot ? (cu == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(                               \
+                        &b, gauss_gemv_dot_kernel<R, 256, false, 1>, 256, 0)                     \
+                  : cu == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(                     \
+                                  &b, gauss_gemv_dot_kernel<R, 256, false, 2>, 256, 0)           \
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(                     \
+                                  &b, gauss_gemv_dot_kernel<R, 256, false, 4>, 256, 0))          \
+       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gauss_gemv_kernel<R, 256, false>,     \
+                                                       256, 0))
+    if (rpt == 1) RPLU_OCC(1);
+    else if (rpt == 2) RPLU_OCC(2);
+    else RPLU_OCC(4);
+#undef RPLU_OCC
     per_sm[slot] = b > 0 ? b : 1;
   }
   const int splits = gemv_splits(op.n, op.m, 256 * rpt, ctx->sm_count, per_sm[slot]);
   int rc;
-  if ((rc = ctx->scratch[4].ensure(sizeof(double) * (size_t)splits * op.n))) return rc;
-  double* part = reinterpret_cast<double*>(ctx->scratch[4].ptr);
+  // scratch: [bounding-box partials | geo | split partials]
+  const int nbox = (int)std::min<long long>((std::max(op.n, op.m) + 255) / 256, ctx->sm_count);
+  constexpr size_t kGeoDoubles = 4096;   // >= 12 * SMs + 4
+  if ((rc = ctx->scratch[4].ensure(sizeof(double) * (kGeoDoubles + (size_t)splits * op.n))))
+    return rc;
+  double* boxes = reinterpret_cast<double*>(ctx->scratch[4].ptr);
+  double* geo = boxes + kGeoDoubles - 8;
+  double* part = boxes + kGeoDoubles;
+  count_launches(2);
+  if (gemv_dot_enabled()) {
+    gauss_bbox_kernel<<<nbox, 256, 0, s>>>(op, boxes);
+    gauss_geo_kernel<<<1, 32, 0, s>>>(boxes, nbox, op.c, geo);
+  } else {
+    gauss_geo_off_kernel<<<1, 32, 0, s>>>(geo);
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ms) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  count_launches(1);
-  if (rpt == 1) gemv_launch<1>(op, v, part, splits, square, s);
-  else if (rpt == 2) gemv_launch<2>(op, v, part, splits, square, s);
-  else gemv_launch<4>(op, v, part, splits, square, s);
+  count_launches(2);
+  if (rpt == 1) gemv_launch<1>(op, v, part, splits, square, geo, s);
+  else if (rpt == 2) gemv_launch<2>(op, v, part, splits, square, geo, s);
+  else gemv_launch<4>(op, v, part, splits, square, geo, s);
   if (ms) cudaEventRecord(e1, s);
   count_launches(1);
   reduce_splits_kernel<<<(unsigned)((op.n + 255) / 256), 256, 0, s>>>(part, splits, op.n, out);

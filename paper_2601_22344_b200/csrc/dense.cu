@@ -62,7 +62,22 @@ struct DenseParams {
   double* lin;         // [n] sum_s L_is (r0_i . U_s)
   double* quad;        // [n] sum_{s,s'} L_is L_is' (U_s . U_s')
   double* gmat;        // [16 x 16] U_s . U_s' of the pending steps
+  // Block-relative steps (captured shard blocks): the kernels take the
+  // absolute step from the device counter st->step; t, t0 and gram_t0 then
+  // only carry their differences (t - t0 = pending terms before this step).
+  int rel;
+  long long u_rows;    // rows of U the tensor map may cover (rel mode)
 };
+
+__device__ __forceinline__ long long lz_t(const DenseParams& p) {
+  return p.rel ? p.st->step : p.t;
+}
+__device__ __forceinline__ long long lz_t0(const DenseParams& p) {
+  return p.rel ? p.st->step - (p.t - p.t0) : p.t0;
+}
+__device__ __forceinline__ long long lz_g0(const DenseParams& p) {
+  return p.rel ? p.st->step - (p.t - p.gram_t0) : p.gram_t0;
+}
 
 // One pending term of the delayed-update loop, R -= L_s U_s at one element:
 // fused, one rounding per term (the FP64 pipe does half the work of the
@@ -548,14 +563,14 @@ template <typename T>
 __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
   using S = Scalar<T>;
   if (!p.st->active) return;
-  const long long n = p.n, j = p.st->pj, t = p.t;
+  const long long n = p.n, j = p.st->pj, t = lz_t(p), t0 = lz_t0(p);
   const T* R = reinterpret_cast<const T*>(p.R);
   T* Lt = reinterpret_cast<T*>(p.Lt);
   const T* U = reinterpret_cast<const T*>(p.U);
   const typename S::coef_t cf = load_coef<T>(p.st);
-  const int q = (int)(t - p.t0);
+  const int q = (int)(t - t0);
   __shared__ T s_upiv[kLazyMaxBlock];  // U[s][j] of the pending steps
-  if ((int)threadIdx.x < q) s_upiv[threadIdx.x] = U[(p.t0 + threadIdx.x) * p.ldu + j];
+  if ((int)threadIdx.x < q) s_upiv[threadIdx.x] = U[(t0 + threadIdx.x) * p.ldu + j];
   __syncthreads();
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x) {
@@ -563,7 +578,7 @@ __global__ void __launch_bounds__(256) lazy_pivcol_kernel(DenseParams p) {
     T ll[kLazyMaxBlock];
 #pragma unroll
     for (int s = 0; s < kLazyMaxBlock; ++s)
-      if (s < q) ll[s] = Lt[(p.t0 + s) * n + k];
+      if (s < q) ll[s] = Lt[(t0 + s) * n + k];
 #pragma unroll
     for (int s = 0; s < kLazyMaxBlock; ++s)
       if (s < q) x = pend_sub<T>(p.fused, x, ll[s], s_upiv[s]);
@@ -681,7 +696,7 @@ struct LazyTma {
 // pending-term arithmetic (pivot row / column, flush), bit-identical to the
 // eager loop.  Negative rounding residue of eliminated rows is clamped to 0.
 __device__ __forceinline__ void gram_mass_update(const DenseParams& p, long long i, double g) {
-  const long long t = p.t, t0 = p.gram_t0, n = p.n;
+  const long long t = lz_t(p), t0 = lz_g0(p), n = p.n;
   const double* Lt = reinterpret_cast<const double*>(p.Lt);
   const double* G = p.gmat + (t - t0) * kLazyMaxBlock;
   const double lt = Lt[t * n + i];
@@ -698,7 +713,7 @@ __device__ __forceinline__ void gram_mass_update(const DenseParams& p, long long
 // G[t - t0][s - t0] = U_t . U_s for the pending s (one CTA per s, fixed order)
 __global__ void __launch_bounds__(256) lazy_gram_kernel(DenseParams p) {
   if (!p.st->active) return;
-  const long long t = p.t, s = p.gram_t0 + blockIdx.x, m = p.m;
+  const long long t = lz_t(p), g0 = lz_g0(p), s = g0 + blockIdx.x, m = p.m;
   const double* U = reinterpret_cast<const double*>(p.U);
   const double* ut = U + t * p.ldu;
   const double* us = U + s * p.ldu;
@@ -711,7 +726,7 @@ __global__ void __launch_bounds__(256) lazy_gram_kernel(DenseParams p) {
   if (threadIdx.x == 0) {
     double v = 0.0;
     for (int w = 0; w < 8; ++w) v += red[w];
-    p.gmat[(t - p.gram_t0) * kLazyMaxBlock + blockIdx.x] = v;
+    p.gmat[(t - g0) * kLazyMaxBlock + blockIdx.x] = v;
   }
 }
 
@@ -764,12 +779,14 @@ __global__ void __launch_bounds__(288, 1)
   const long long nchunks = (m + CW - 1) / CW;
   const long long nblocks = (n + ROWS - 1) / ROWS;
   const T* Lt = reinterpret_cast<const T*>(p.Lt);
+  const long long l_row0 = lz_t0(p);
 
   if (warp == C::NCW) {  // producer warp: one elected lane issues two TMA loads per stage
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmR) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmU) : "memory");
       const uint64_t pol_r = policy_evict_first(), pol_u = policy_evict_last();
+      const int u_row0 = (int)lz_t0(p);
       int stage = 0;
       unsigned phase = 0;
       long long i = 0;  // items (row block, column chunk) issued by this CTA
@@ -795,7 +812,7 @@ __global__ void __launch_bounds__(288, 1)
           }
           mbar_expect_tx(&full[stage], (unsigned)C::STAGE);
           tma_load_2d(st, &tmR, (int)(c * WORDS), (int)(rb * ROWS), &full[stage], pol_r);
-          tma_load_2d(st + ROWS * TX, &tmU, (int)(c * WORDS), (int)p.t0, &full[stage], pol_u);
+          tma_load_2d(st + ROWS * TX, &tmU, (int)(c * WORDS), u_row0, &full[stage], pol_u);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -825,7 +842,7 @@ __global__ void __launch_bounds__(288, 1)
     T* L = Ls + buf * QC * ROWS;
     for (int idx = threadIdx.x; idx < QC * ROWS; idx += C::NCW * 32) {
       const int s = idx / ROWS, r = idx % ROWS;
-      L[idx] = (row0 + r < n) ? Lt[(p.t0 + s) * n + row0 + r] : S::zero();
+      L[idx] = (row0 + r < n) ? Lt[(l_row0 + s) * n + row0 + r] : S::zero();
     }
     consumer_bar();  // L visible; red[buf^1] of the previous block complete
     if (prev_row0 >= 0 && threadIdx.x < ROWS) {
@@ -1496,7 +1513,7 @@ static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
   const long long g = nblocks < sm_count() ? nblocks : sm_count();
   if (g <= 0 || p.m <= 0) return RPLU_OK;
   CUtensorMap tmR, tmU;
-  const long long urows = p.t0 + QC;  // U rows 0 .. t0+QC-1 exist
+  const long long urows = p.rel ? p.u_rows : p.t0 + QC;  // U rows 0 .. t0+QC-1 exist
   if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, C::ROWS, C::LINE) ||
       !make_row_map(&tmU, p.U, (int)sizeof(T), urows, p.m, p.ldu, QC, C::LINE)) {
     set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
@@ -2170,7 +2187,7 @@ int dense_gram_block() { return gram_block(); }
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
                            long long t0, bool pivcol, bool flush, bool force, cudaStream_t s,
-                           double* gram) {
+                           double* gram, bool rel, long long u_rows) {
   if (n == 0) return RPLU_OK;
   if (gram && dtype != RPLU_F64) {
     set_error("Gram-mass delayed updates are fp64 only");
@@ -2190,6 +2207,8 @@ int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long l
   p.t0 = t0;
   p.lazy = 1;
   p.force = force ? 1 : 0;
+  p.rel = rel ? 1 : 0;      // t, t0: block-relative, absolute step from st->step
+  p.u_rows = u_rows;
   set_gram(p, gram);
   int rc;
   switch (dtype) {

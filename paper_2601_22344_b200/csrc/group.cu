@@ -18,6 +18,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -220,28 +221,119 @@ int rplu_group_dense_run(rplu_group* g, const rplu_group_dense_args* a, rplu_den
     if ((rc = rplu_shard_begin(g->ctxs[d], &sa[d], static_cast<double*>(tot[d])))) return fail(rc);
   if ((rc = allgather_totals())) return fail(rc);
   const bool eager = a->lazy_block == 0;
-  for (long long t = 0; t <= a->steps; ++t) {
-    const long long tt = eager ? -1 : t;   // eager: the device step counter
+  // One pivot step on every device: tt >= 0 explicit step, tt == -1 the
+  // device step counter (eager), tt < -1 ... block position -1 - tt of a
+  // delayed-update block (select takes the counter, update the position).
+  auto step = [&](long long tt) -> int {
+    int r;
     for (int d = 0; d < G; ++d)
-      if ((rc = rplu_shard_select(g->ctxs[d], &sa[d], tt, static_cast<double*>(totals[d]),
-                                  msg[d])))
-        return fail(rc);
-    if (t == a->steps) break;
+      if ((r = rplu_shard_select(g->ctxs[d], &sa[d], tt < 0 ? -1 : tt,
+                                 static_cast<double*>(totals[d]), msg[d])))
+        return r;
     RPLU_NCCL(api.groupStart());
     for (int d = 0; d < G; ++d)
       RPLU_NCCL(api.allReduce(msg[d], msg[d], red_count, red_t, ncclSum, g->comms[d],
                               g->streams[d]));
     RPLU_NCCL(api.groupEnd());
     for (int d = 0; d < G; ++d)
-      if ((rc = rplu_shard_update(g->ctxs[d], &sa[d], tt, msg[d], static_cast<double*>(tot[d]))))
-        return fail(rc);
-    if ((rc = allgather_totals())) return fail(rc);
-    if ((t + 1) % 32 == 0) {
-      int32_t active = 0;
-      if ((rc = rplu_shard_active(g->ctxs[0], &sa[0], &active))) return fail(rc);
-      if (!active) break;
+      if ((r = rplu_shard_update(g->ctxs[d], &sa[d], tt, msg[d], static_cast<double*>(tot[d]))))
+        return r;
+    return allgather_totals();
+  };
+  auto poll_active = [&](int32_t* active) { return rplu_shard_active(g->ctxs[0], &sa[0], active); };
+
+  // Delayed-update shards: after the first block (explicit steps; it also
+  // sizes every scratch buffer and sets the kernel attributes) one whole
+  // flush block -- b steps of kernels on every device plus the grouped
+  // collectives -- is captured into ONE multi-device CUDA graph (stream 0
+  // forks to the other devices' streams through events) and replayed once per
+  // block: one graph launch per b steps for all GPUs instead of ~12 G
+  // launches per step from this one host thread.  RPLU_GROUP_GRAPH=0 keeps
+  // the plain loop; a failed capture falls back to it.
+  const long long b = eager ? 0 : rplu_shard_lazy_block(&sa[0]);
+  const char* genv = getenv("RPLU_GROUP_GRAPH");
+  bool use_graph = b > 0 && a->steps >= 2 * b && !(genv && genv[0] == '0');
+  long long t = 0;
+  int32_t active = 1;
+  if (use_graph) {
+    for (; t < b; ++t)
+      if ((rc = step(t))) return fail(rc);
+    if ((rc = poll_active(&active))) return fail(rc);
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> ev(G + 1, nullptr);
+    auto drop_graph = [&]() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      for (int d = 0; d <= G; ++d)
+        if (ev[d]) cudaEventDestroy(ev[d]);
+      exec = nullptr;
+      graph = nullptr;
+    };
+    bool captured = false;
+    if (active) {
+      for (int d = 0; d < G; ++d) {
+        cudaSetDevice(g->devs[d]);
+        cudaStreamSynchronize(g->streams[d]);
+        cudaEventCreateWithFlags(&ev[d], cudaEventDisableTiming);
+      }
+      cudaSetDevice(g->devs[0]);
+      cudaEventCreateWithFlags(&ev[G], cudaEventDisableTiming);
+      int crc = RPLU_OK;
+      if (cudaStreamBeginCapture(g->streams[0], cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+        cudaEventRecord(ev[G], g->streams[0]);                       // fork
+        for (int d = 1; d < G; ++d) cudaStreamWaitEvent(g->streams[d], ev[G], 0);
+        for (long long pos = 0; pos < b && crc == RPLU_OK; ++pos) crc = step(-1 - pos);
+        for (int d = 1; d < G; ++d) {                                // join
+          cudaSetDevice(g->devs[d]);
+          cudaEventRecord(ev[d], g->streams[d]);
+          cudaStreamWaitEvent(g->streams[0], ev[d], 0);
+        }
+        cudaSetDevice(g->devs[0]);
+        const cudaError_t ce = cudaStreamEndCapture(g->streams[0], &graph);
+        if (crc == RPLU_OK && ce == cudaSuccess && graph &&
+            cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess)
+          captured = true;
+      }
+      if (!captured) {
+        for (int d = 0; d < G; ++d) {
+          cudaSetDevice(g->devs[d]);
+          cudaGetLastError();
+        }
+        drop_graph();
+      }
+    }
+    if (captured) {
+      cudaSetDevice(g->devs[0]);
+      long long k = 1;
+      for (; t + b <= a->steps; t += b, ++k) {
+        if (cudaGraphLaunch(exec, g->streams[0]) != cudaSuccess) {
+          drop_graph();
+          set_error("rplu_group_dense_run: graph launch failed");
+          return fail(RPLU_ERR_CUDA);
+        }
+        if (k % 2 == 0) {
+          // the other devices' work was forked from stream 0 and joined back
+          if ((rc = poll_active(&active))) { drop_graph(); return fail(rc); }
+          if (!active) break;
+        }
+      }
+      cudaStreamSynchronize(g->streams[0]);
+      drop_graph();
+      if (active && (rc = poll_active(&active))) return fail(rc);
     }
   }
+  for (; active && t < a->steps; ++t) {
+    if ((rc = step(eager ? -1 : t))) return fail(rc);
+    if ((t + 1) % 32 == 0) {
+      if ((rc = poll_active(&active))) return fail(rc);
+    }
+  }
+  // final residual norm / stop flags
+  for (int d = 0; d < G; ++d)
+    if ((rc = rplu_shard_select(g->ctxs[d], &sa[d], -1, static_cast<double*>(totals[d]),
+                                msg[d])))
+      return fail(rc);
   // every shard's finish (the delayed loop applies its pending steps); the
   // replicated results come from shard 0
   for (int d = G - 1; d >= 0; --d) {

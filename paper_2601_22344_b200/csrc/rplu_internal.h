@@ -94,7 +94,7 @@ constexpr int kLazyMaxBlock = 16;  // longest delayed-update block
 int dense_lazy_step_launch(int dtype, void* R, long long ld, long long n, long long m, void* Lt,
                            void* U, long long ldu, double* masses, DevState* st, long long t,
                            long long t0, bool pivcol, bool flush, bool force, cudaStream_t s,
-                           double* gram = nullptr);
+                           double* gram = nullptr, bool rel = false, long long u_rows = 0);
 int dense_gram_reset_launch(long long n, double* masses, double* gram, cudaStream_t s);
 int dense_gram_block();
 int dense_lazy_block_default(int dtype, bool fused = false);

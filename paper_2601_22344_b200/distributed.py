@@ -85,12 +85,60 @@ def run_sharded(backend, steps, group=None, poll_every=32, step_hook=None):
     return backend.finish()
 
 
+def _run_sharded_block_graph(backend, steps, group, block):
+    """Delayed-update shards: one whole block of `block` steps (per step the
+    select kernels, the allreduce, post + pivot column + read pass -- the
+    flush at the block's last position -- and the allgather) is captured once
+    and replayed.  Inside a block the number of pending terms of each step is
+    fixed at capture; the absolute step comes from the device counter.  The
+    first block runs uncaptured (it also warms every kernel variant), a
+    trailing partial block runs with explicit steps."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    local_total = backend.begin()
+    totals = torch.empty(world, dtype=torch.float64, device=backend.dev)
+    totals.copy_(_all_gather_scalar(local_total, group, world))
+
+    def step(t):
+        msg = backend.select(t, totals)
+        if dist.is_initialized():
+            dist.all_reduce(msg, op=dist.ReduceOp.SUM, group=group)
+        lt = backend.update(t, msg)
+        _all_gather_scalar(lt, group, world, out=totals)
+
+    nblocks = steps // block
+    t = 0
+    if nblocks >= 1:
+        for _ in range(block):
+            step(t)
+            t += 1
+    if nblocks >= 2 and backend.active():
+        torch.cuda.synchronize(backend.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for pos in range(block):
+                step(-1 - pos)
+        for k in range(1, nblocks):
+            g.replay()
+            t += block
+            if k % 2 == 0 and k + 1 < nblocks and not backend.active():
+                break
+    if t < steps and backend.active():
+        for tt in range(t, steps):      # trailing partial block (or a one-block run)
+            step(tt)
+    backend.select(-1, totals)          # final residual norm / stop flags
+    return backend.finish()
+
+
 def run_sharded_graph(backend, steps, group=None, chunk=32):
     """The same choreography with one step (select, allreduce, update,
     allgather) captured once in a CUDA graph and replayed: the kernels read
     the step index from the device counter, the collectives run on static
     buffers.  Replays go in chunks of `chunk` steps with a stop poll between
-    chunks."""
+    chunks.  Delayed-update backends capture one flush block instead
+    (`_run_sharded_block_graph`)."""
+    block = getattr(backend, "block_len", 0)
+    if block > 0:
+        return _run_sharded_block_graph(backend, steps, group, block)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     local_total = backend.begin()
     totals = torch.empty(world, dtype=torch.float64, device=backend.dev)
@@ -155,6 +203,8 @@ class CudaShardBackend:
         c = ctx if ctx is not None else _device.ctx(self.dev)
         self._ctx = c
         self._lib, self._h = c._lib, c.handle
+        # resolved flush interval (0: eager updates)
+        self.block_len = int(self._lib.rplu_shard_lazy_block(ctypes.byref(self.args)))
         self.pivots = np.zeros(2 * max(steps, 1), dtype=np.int64)
         self.resid = np.zeros(steps + 1)
 
@@ -213,11 +263,12 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
     EliminationTrace whose L holds this rank's rows of L (device tensor) and
     whose U / pivots / resid_fro are the global (replicated) values.
 
-    ``update``: "eager" (fused K3 update every step; the only mode a CUDA
-    graph can replay), "lazy" (delayed updates: one read of the row block per
-    step, a write every ``lazy_block`` steps; host step loop), or "auto"
-    (lazy when not graphing and the local block exceeds 256 MB, as on one
-    GPU).  Results are bit-identical across modes.
+    ``update``: "eager" (fused K3 update every step), "lazy" (delayed
+    updates: one read of the row block per step, a write every ``lazy_block``
+    steps), or "auto" (lazy when the local block exceeds 256 MB, as on one
+    GPU).  ``graph=True`` captures one step (eager) or one whole flush block
+    (lazy) with its collectives in a CUDA graph and replays it.  Results are
+    bit-identical across modes.
     """
     if update not in ("auto", "eager", "lazy"):
         raise ValueError(f"update must be 'auto', 'eager' or 'lazy', not {update!r}")
@@ -234,9 +285,7 @@ def sharded_eliminate(A_local, row_offset, rule, steps, stop_tol=0.0, group=None
     n_local, m = src.shape
     if update == "auto":
         big = n_local * m * R.element_size() > 256e6
-        update = "lazy" if big and not graph and steps >= 2 else "eager"
-    if update == "lazy" and graph:
-        raise ValueError("the delayed-update shard loop runs on the host (graph=False)")
+        update = "lazy" if big and steps >= 2 else "eager"
     lb = 0 if update == "eager" else (-1 if lazy_block is None else int(lazy_block))
     backend = CudaShardBackend(R, row_offset, world, rank, rule, steps, stop_tol, lazy_block=lb)
     if graph and step_hook is None:
@@ -503,11 +552,12 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit, sampler_c
         e.record()
         sweep_ev.append(e)
 
-    # RPLU_SHARD_UPDATE=lazy (default: delayed updates, host step loop) or
-    # eager (fused K3 update; one step captured in a CUDA graph and replayed
-    # unless RPLU_SHARD_GRAPH=0)
+    # RPLU_SHARD_UPDATE=lazy (default: delayed updates, one flush block with
+    # its collectives captured in a CUDA graph and replayed) or eager (fused
+    # K3 update; one step captured and replayed); RPLU_SHARD_GRAPH=0: host
+    # step loop
     mode = os.environ.get("RPLU_SHARD_UPDATE", "lazy")
-    use_graph = mode == "eager" and os.environ.get("RPLU_SHARD_GRAPH", "1") == "1"
+    use_graph = os.environ.get("RPLU_SHARD_GRAPH", "1") == "1"
     lazy_used = [0]
 
     def one(timed=False):
@@ -588,7 +638,8 @@ def bench_sharded(args, cfg, dist_mod, rank, world, dev, metric, unit, sampler_c
             "dtype": cfg["dtype"], "data": "synthetic (seeded BASELINE construction)",
             "config": {"workload": cfg["desc"], "n": n, "m": n, "rank": k, "seed": seed,
                        "parallelism": f"row-block shards x{world} (NCCL allgather + allreduce)",
-                       "step_loop": "CUDA graph of one step replayed" if use_graph else "host loop",
+                       "step_loop": (("CUDA graph of one flush block replayed" if b else
+                                      "CUDA graph of one step replayed") if use_graph else "host loop"),
                        "update": f"delayed (flush every {b} steps)" if b else "eager (K3)",
                        "step": f"one full elimination of {k} pivot steps",
                        "l2": "inputs larger than L2"},

@@ -6,7 +6,8 @@
 #   test:EXPR[:ARGS]      pytest -m EXPR ARGS (ARGS eval'd: quote -k expressions with '')
 #   bench:CONFIG[:ARGS]   bench.py --config CONFIG (CONFIG "ref" = --impl reference)
 #   launches:CONFIG       ncu launch list (gpu__time_duration) of one bench run
-#   full:CONFIG:KERNEL[:COUNT[:ARGS]]  ncu --set full of KERNEL (regex) in a bench run
+#   full:CONFIG:KERNEL[:COUNT[:SKIP[:ARGS]]]  ncu --set full of KERNEL (regex) in a bench run
+#                         (COUNT launches after skipping SKIP matching ones)
 #   py:SCRIPT[:ARGS]      python SCRIPT ARGS
 # Logs go to gpurun_out/TAG/; the parity log to gpurun_out/TAG/parity.jsonl.
 TAG=$1; shift
@@ -36,11 +37,17 @@ for step in "$@"; do
         --log-file "$OUT/$i.launches_$rest.csv" python bench.py --config "$rest" --steps 1 --warmup 3 \
         > "$OUT/$i.launches_$rest.log" 2>&1 ;;
     full)
-      cfg=${rest%%:*}; r2=${rest#*:}; kern=${r2%%:*}; cnt=1; fargs=""
-      if [[ $r2 == *:* ]]; then r3=${r2#*:}; cnt=${r3%%:*}; [[ $r3 == *:* ]] && fargs=${r3#*:}; fi
-      timeout 2400 ncu --set full --clock-control none --import-source on -k "regex:$kern" -c "$cnt" \
+      cfg=${rest%%:*}; r2=${rest#*:}; kern=${r2%%:*}; cnt=1; skip=0; fargs=""
+      if [[ $r2 == *:* ]]; then r3=${r2#*:}; cnt=${r3%%:*};
+        if [[ $r3 == *:* ]]; then r4=${r3#*:}; skip=${r4%%:*}; [[ $r4 == *:* ]] && fargs=${r4#*:}; fi; fi
+      timeout 2400 ncu --set full --clock-control none --import-source on -k "regex:$kern" -s "$skip" -c "$cnt" \
         -o "$OUT/$i.full_${cfg}" python bench.py --config "$cfg" --steps 1 --warmup 1 $fargs \
         > "$OUT/$i.full_$cfg.log" 2>&1 ;;
+    shard1)   # world-1 sharded C3 over NCCL (torchrun, one rank); rest = env assignments
+      envs=""; [[ $rest != shard1 ]] && envs=$rest
+      env $envs timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
+        --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 2 --warmup 1 \
+        > "$OUT/$i.shard1.log" 2>&1 ;;
     py)
       scr=${rest%%:*}; args=""; [[ $rest == *:* ]] && args=${rest#*:}
       timeout 3000 python $scr $args > "$OUT/$i.py.log" 2>&1 ;;

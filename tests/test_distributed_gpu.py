@@ -86,16 +86,59 @@ def test_c_group_driver_world1(update, cuda_device):
     assert rng.uniform() == ref2.uniform()
 
 
-def test_lazy_rejects_graph_and_device_steps(cuda_device):
-    A = torch.from_numpy(gen.c1_dense(2, n=64, m=64)).cuda()
-    with pytest.raises(ValueError):
-        sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(2)), 8, update="lazy",
-                          graph=True)
-    be = CudaShardBackend(A.clone(), 0, 1, 0, rp.PivotRule("rplu", rp.RngState(2)), 8,
-                          lazy_block=3)
-    tot = be.begin().clone()
-    with pytest.raises(Exception):
-        be.select(-1, tot)
+@pytest.mark.parametrize("dtype,lazy_block,gram", [(torch.float64, -1, True), (torch.float64, 5, True),
+                                                   (torch.float64, 4, False), (torch.float32, 6, False),
+                                                   (torch.complex128, 3, False)])
+def test_world1_lazy_block_graph(dtype, lazy_block, gram, cuda_device, monkeypatch):
+    """Delayed-update shards with one whole flush block (kernels with
+    block-relative steps + collectives) captured in a CUDA graph and replayed:
+    bit-identical to the eager single-GPU loop for full blocks + a trailing
+    partial block, for a run shorter than two blocks, and across a tol stop
+    inside a replayed block."""
+    A = gen.c1_dense(11, n=390, m=305)
+    if dtype == torch.complex128:
+        A = A + 1j * gen.c1_dense(12, n=390, m=305)
+    A = torch.from_numpy(A).to("cuda", dtype)
+    for steps, tol in ((77, 0.0), (19, 0.0), (250, 0.4)):
+        tr = sharded_eliminate(A, 0, rp.PivotRule("rplu", rp.RngState(3)), steps, stop_tol=tol,
+                               update="lazy", lazy_block=lazy_block, graph=True)
+        ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(3)), steps, stop_tol=tol,
+                           update="eager")
+        assert tr.lazy_block > 0
+        assert tr.pivots == ref.pivots and tr.tol_stop == ref.tol_stop
+        assert torch.equal(tr.L, ref.L) and torch.equal(tr.U, ref.U)
+        assert torch.equal(tr.residual_device, ref.residual_device)
+        np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-13)
+
+
+def test_emulated_shards_block_positions(cuda_device):
+    """3 emulated shards driven with block-relative steps (t = -1 - position,
+    the form a captured block replays) after an explicit first block."""
+    A = gen.c1_dense(9, n=420, m=256)
+    steps, world, b, seed = 40, 3, 4, 9
+    bes = []
+    for r in range(world):
+        lo, hi = shard_rows(A.shape[0], world, r)
+        R = torch.from_numpy(np.ascontiguousarray(A[lo:hi])).cuda()
+        bes.append(CudaShardBackend(R, lo, world, r, rp.PivotRule("rplu", rp.RngState(seed)),
+                                    steps, ctx=_ffi.Context(0), lazy_block=b))
+    assert all(be.block_len == b for be in bes)
+    totals = torch.cat([be.begin().clone() for be in bes])
+    for t in range(steps + 1):
+        tt = t if t < b or t == steps else -1 - (t % b)
+        ms = [be.select(-1 if tt < 0 else tt, totals).clone() for be in bes]
+        if t == steps:
+            break
+        msg = ms[0]
+        for x in ms[1:]:
+            msg = msg + x
+        totals = torch.cat([be.update(tt, msg).clone() for be in bes])
+    res = [be.finish() for be in bes]
+    ref = oracle.eliminate_real(A, "rplu", steps, seed=seed)
+    assert res[0]["pivots"] == ref["pivots"]
+    L = torch.cat([r["L_local"] for r in res], dim=0).cpu().numpy()
+    np.testing.assert_array_equal(L, ref["L"])
+    np.testing.assert_array_equal(res[0]["U"].cpu().numpy(), ref["U"])
 
 
 @pytest.mark.parametrize("world,lazy_block", [(2, 0), (3, 0), (2, 4), (3, 5), (8, 0), (8, 6)])
