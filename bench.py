@@ -405,11 +405,12 @@ def run_cur_arm(args, cfg):
                    "l2": "generated entries; points only in HBM (48 MB per side)"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "gauss_gemv_kernel (K7 full generated GEMV g = A l)",
+                     "kernel": "gauss_gemv_dot_kernel (K7 full generated GEMV g = A l, dot-product exponent form)",
                      "algorithmic_flops_per_launch": evals * flops_per_eval,
                      "avg_launch_ms": avg_s * 1e3, "evals_per_s": evals / avg_s,
                      "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)",
-                     "note": "13 flop/eval counts exp as one op; the exp costs ~17 DFMA"},
+                     "note": "13 flop/eval counts exp as one op; an entry costs 14 FP64-pipe instructions "
+                             "(4 exponent + 3 reduction + 5 polynomial + scale + accumulate)"},
         "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"one Gaussian-kernel apply on {rows} of {n} rows "
                                    f"({dt:.2f}s), extrapolated to the reference's 6 full "

@@ -98,7 +98,8 @@ def upload(a, dev):
     out = torch.empty(a.shape, dtype=t.dtype, device=dev)
     c = ctx(dev)
     import os
-    threads = max(1, min(8, len(os.sched_getaffinity(0))))
+    threads = max(1, min(int(os.environ.get("RPLU_UPLOAD_THREADS", "16")),
+                         len(os.sched_getaffinity(0))))
     _ffi.check(c._lib.rplu_upload(c.handle, ctypes.c_void_p(out.data_ptr()),
                                   ctypes.c_void_p(a.ctypes.data), a.nbytes, threads,
                                   stream_handle(dev)))

@@ -710,23 +710,40 @@ __device__ __forceinline__ void gram_mass_update(const DenseParams& p, long long
   p.masses[i] = mass > 0.0 ? mass : 0.0;
 }
 
-// G[t - t0][s - t0] = U_t . U_s for the pending s (one CTA per s, fixed order)
-__global__ void __launch_bounds__(256) lazy_gram_kernel(DenseParams p) {
+// G[t - t0][s - t0] = U_t . U_s for the pending s (one CTA of 1024 threads
+// per s; 8 independent loads in flight per thread -- with 256 threads and a
+// serial load-FMA loop the kernel was L2-latency bound at 23 us per step at
+// m = 32768 -- then a fixed-order reduction: deterministic)
+__global__ void __launch_bounds__(1024) lazy_gram_kernel(DenseParams p) {
   if (!p.st->active) return;
   const long long t = lz_t(p), g0 = lz_g0(p), s = g0 + blockIdx.x, m = p.m;
   const double* U = reinterpret_cast<const double*>(p.U);
   const double* ut = U + t * p.ldu;
   const double* us = U + s * p.ldu;
-  double acc = 0.0;
-  for (long long k = threadIdx.x; k < m; k += blockDim.x) acc = fma(ut[k], us[k], acc);
-  acc = warp_sum(acc);
-  __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  constexpr int NT = 1024, UN = 8;
+  double acc[UN];
+#pragma unroll
+  for (int u = 0; u < UN; ++u) acc[u] = 0.0;
+  for (long long k0 = threadIdx.x; k0 < m; k0 += (long long)NT * UN) {
+    double a[UN], b[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const long long k = k0 + (long long)u * NT;
+      a[u] = k < m ? ut[k] : 0.0;
+      b[u] = k < m ? us[k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) acc[u] = fma(a[u], b[u], acc[u]);
+  }
+  double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  v = warp_sum(v);
+  __shared__ double red[NT / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double v = 0.0;
-    for (int w = 0; w < 8; ++w) v += red[w];
-    p.gmat[(t - g0) * kLazyMaxBlock + blockIdx.x] = v;
+    double r = 0.0;
+    for (int w = 0; w < NT / 32; ++w) r += red[w];
+    p.gmat[(t - g0) * kLazyMaxBlock + blockIdx.x] = r;
   }
 }
 
@@ -1613,7 +1630,7 @@ static int gram_step(const DenseParams& p, long long t0, cudaStream_t s) {
   if constexpr (std::is_same<T, double>::value) {
     DenseParams q = p;
     q.gram_t0 = t0;
-    lazy_gram_kernel<<<(unsigned)(p.t - t0 + 1), 256, 0, s>>>(q);
+    lazy_gram_kernel<<<(unsigned)(p.t - t0 + 1), 1024, 0, s>>>(q);
     q.t0 = p.t;  // the pass's one "pending" U row is U_t
     return launch_lazy_pass4_w<double, false, 1, 64, false, true>(q, s);
   } else {

@@ -8,6 +8,8 @@
 #   launches:CONFIG       ncu launch list (gpu__time_duration) of one bench run
 #   full:CONFIG:KERNEL[:COUNT[:SKIP[:ARGS]]]  ncu --set full of KERNEL (regex) in a bench run
 #                         (COUNT launches after skipping SKIP matching ones)
+#   lite:...              as full:, without the instrumented source-counter passes
+#   shard1[:ENV=V ...]    bench.py under torchrun with one rank (world-1 sharded C3 over NCCL)
 #   py:SCRIPT[:ARGS]      python SCRIPT ARGS
 # Logs go to gpurun_out/TAG/; the parity log to gpurun_out/TAG/parity.jsonl.
 TAG=$1; shift
@@ -43,6 +45,16 @@ for step in "$@"; do
       timeout 2400 ncu --set full --clock-control none --import-source on -k "regex:$kern" -s "$skip" -c "$cnt" \
         -o "$OUT/$i.full_${cfg}" python bench.py --config "$cfg" --steps 1 --warmup 1 $fargs \
         > "$OUT/$i.full_$cfg.log" 2>&1 ;;
+    lite)   # as full, without the instrumented (SourceCounters) passes: for multi-second kernels
+      cfg=${rest%%:*}; r2=${rest#*:}; kern=${r2%%:*}; cnt=1; skip=0; fargs=""
+      if [[ $r2 == *:* ]]; then r3=${r2#*:}; cnt=${r3%%:*};
+        if [[ $r3 == *:* ]]; then r4=${r3#*:}; skip=${r4%%:*}; [[ $r4 == *:* ]] && fargs=${r4#*:}; fi; fi
+      timeout 2400 ncu --section SpeedOfLight --section ComputeWorkloadAnalysis \
+        --section MemoryWorkloadAnalysis --section InstructionStats --section LaunchStats \
+        --section Occupancy --section SchedulerStats --section WarpStateStats \
+        --clock-control none -k "regex:$kern" -s "$skip" -c "$cnt" \
+        -o "$OUT/$i.lite_${cfg}" python bench.py --config "$cfg" --steps 1 --warmup 1 $fargs \
+        > "$OUT/$i.lite_$cfg.log" 2>&1 ;;
     shard1)   # world-1 sharded C3 over NCCL (torchrun, one rank); rest = env assignments
       envs=""; [[ $rest != shard1 ]] && envs=$rest
       env $envs timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
