@@ -257,8 +257,9 @@ def run_cauchy_arm(args, cfg):
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
-    # graph-captured loop for small sizes; K5 durations then from a second,
-    # per-launch-evented pass (as in the dense leg)
+    # small sizes run the resident loop (one cooperative launch) or a
+    # graph-captured step loop; K5 durations then come from the resident
+    # loop's phase stamps or from a second, per-launch-evented pass
     graphable = float(n) * n * p <= 256.0 * 1024 * 1024
     ev0.record()
     for _ in range(args.steps):
@@ -267,17 +268,30 @@ def run_cauchy_arm(args, cfg):
     ev1.record()
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
-    if graphable:
-        stats = [one_run(True).kernel_stats for _ in range(args.steps)]
+    launches = sum(s["kernel_launches"] for s in stats)
+    resident = graphable and all(s["kernel_launches"] == 2 for s in stats)
     clk = clocks.stop()
     k = tr.rank
     value = args.steps * k / (total_ms / 1e3)
-    mass_ms = sum(s["masses_ms"] for s in stats)
-    mass_n = sum(s["masses_launches"] for s in stats)
     flops = float(n) * n * (8 * p + 8)
+    peak = _ffi.fp64_peak_tflops(0)
+    phases = None
+    if resident:
+        phases = _trace_phases(
+            "import sys; sys.path.insert(0, %r); import torch; import bench;"
+            "import paper_2601_22344_b200 as rp;"
+            "x, y, G, B = bench._cauchy_input(%r);"
+            "M = rp.CauchyLikeMatrix(x, y, G, B, check_points=False);"
+            "[rp.structured_eliminate(M, 'rplu', %d, rng=rp.RngState(%d)) for _ in range(3)];"
+            "torch.cuda.synchronize()" % (REPO, cfg, rank, seed), "resident cauchy loop")
+        mass_ms, mass_n = phases.get("masses", float("nan")) * 1e-3, 1
+    else:
+        if graphable:
+            stats = [one_run(True).kernel_stats for _ in range(args.steps)]
+        mass_ms = sum(s["masses_ms"] for s in stats)
+        mass_n = sum(s["masses_launches"] for s in stats)
     avg_s = mass_ms / mass_n / 1e3
     achieved = flops / avg_s / 1e12
-    peak = _ffi.fp64_peak_tflops(0)
     # e2e: host generators in, host trace out (the reference-facing call);
     # one untimed call first, as for `value` (the kept-steps configuration
     # captures its own CUDA graph on first use)
@@ -323,16 +337,22 @@ def run_cauchy_arm(args, cfg):
                    "l2": "generated entries; no matrix in HBM"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "cauchy_mass_kernel (K5 generated-entry row masses)",
+                     "kernel": ("cauchy_resident_kernel, mass phase (K5 arithmetic on the CTA's "
+                                "resident rows; one cooperative launch per run, latency-bound "
+                                "step: see phases_us_per_step)" if resident else
+                                "cauchy_mass_kernel (K5 generated-entry row masses)"),
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": avg_s * 1e3,
-                     "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)"},
+                     "peak_source": "measured FP64 DFMA probe (rplu_diag_fp64_peak)",
+                     **({"phases_us_per_step": phases,
+                         "launch_timing": "CTA 0's globaltimer stamps of the same run in a child "
+                                          "process (RPLU_PERSIST_TRACE=1)"} if resident else {})},
         "step_breakdown_ms": {"masses_per_pivot": mass_ms / mass_n,
                               "total_per_pivot": total_ms / (args.steps * k)},
         "cpu_baseline": {"value": cb_v, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": sample + f"; CPU: {model}"},
         "e2e": {"value": trh.rank / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": sum(s["kernel_launches"] for s in stats),
+        "gpu_launches": launches,
         "near_boundary_draws": tr.near_boundary_draws,
         "clocks": clk,
     }
@@ -980,19 +1000,14 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     print(json.dumps(line), flush=True)
 
 
-def _resident_phases(n, rank, seed):
-    """Per-phase microseconds of the C1 resident loop (RPLU_PERSIST_TRACE=1:
-    CTA 0's globaltimer stamps), from a child process (the trace switch is
-    read once per process)."""
-    code = ("import sys; sys.path.insert(0, %r); import torch; import paper_2601_22344_b200 as rp;"
-            "from paper_2601_22344_b200 import gen;"
-            "A = torch.from_numpy(gen.c1_dense(%d, n=%d)).cuda();"
-            "[rp.eliminate(A, rp.PivotRule('rplu', rp.RngState(%d)), %d) for _ in range(3)];"
-            "torch.cuda.synchronize()") % (REPO, seed, n, seed, rank)
+def _trace_phases(code, marker):
+    """Per-phase microseconds printed by a resident loop under
+    RPLU_PERSIST_TRACE=1 (CTA 0's globaltimer stamps), from a child process
+    running `code` (the trace switch is read once per process)."""
     try:
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                            timeout=300, env=dict(os.environ, RPLU_PERSIST_TRACE="1"))
-        lines = [x for x in r.stderr.splitlines() if "resident loop" in x]
+        lines = [x for x in r.stderr.splitlines() if marker in x]
         toks = lines[-1].split("):", 1)[1].split()
         out, k = {}, 0
         while k + 1 < len(toks):       # "row cdf 1.40 row find 2.0 ..." -> names with spaces
@@ -1008,6 +1023,16 @@ def _resident_phases(n, rank, seed):
         return out
     except Exception as exc:  # diagnostics only
         return {"error": str(exc)[:200]}
+
+
+def _resident_phases(n, rank, seed):
+    """Per-phase microseconds of the C1 resident loop."""
+    code = ("import sys; sys.path.insert(0, %r); import torch; import paper_2601_22344_b200 as rp;"
+            "from paper_2601_22344_b200 import gen;"
+            "A = torch.from_numpy(gen.c1_dense(%d, n=%d)).cuda();"
+            "[rp.eliminate(A, rp.PivotRule('rplu', rp.RngState(%d)), %d) for _ in range(3)];"
+            "torch.cuda.synchronize()") % (REPO, seed, n, seed, rank)
+    return _trace_phases(code, "resident loop")
 
 
 def main():

@@ -98,7 +98,9 @@ def upload(a, dev):
     out = torch.empty(a.shape, dtype=t.dtype, device=dev)
     c = ctx(dev)
     import os
-    threads = max(1, min(int(os.environ.get("RPLU_UPLOAD_THREADS", "16")),
+    # 8 staging threads measured best on the 16-vCPU B200 hosts (52 GB/s against
+    # 54 GB/s for a pinned source; 4: 36, 12: 48, 16: 46 -- scripts/time_upload.py)
+    threads = max(1, min(int(os.environ.get("RPLU_UPLOAD_THREADS", "8")),
                          len(os.sched_getaffinity(0))))
     _ffi.check(c._lib.rplu_upload(c.handle, ctypes.c_void_p(out.data_ptr()),
                                   ctypes.c_void_p(a.ctypes.data), a.nbytes, threads,

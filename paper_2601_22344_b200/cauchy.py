@@ -424,12 +424,16 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
 
 
 def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=None,
-                         keep_steps=False, *, host_steps=True, time_kernels=False):
+                         keep_steps=False, *, host_steps=True, time_kernels=False,
+                         persistent=True):
     """Pivoted elimination of a Cauchy-like matrix via generator updates
     (cauchy.py:177-256), exact-row-norm (plan=None) path on the device.
 
     Consumes the caller's RngState exactly as the reference: one uniform for
     the row draw, one for the column draw, one more per column resample.
+    Small problems (the generators fit in shared memory, displacement rank
+    <= 2) run the whole loop as one resident cooperative launch;
+    ``persistent=False`` keeps the per-step kernels (K5 / select / update).
     """
     if rule not in ("rplu", "c2plu"):
         raise ValueError(f"unknown structured rule {rule!r}")
@@ -467,7 +471,8 @@ def structured_eliminate(M, rule, rank, stop_tol=0.0, nu=5.0, plan=None, rng=Non
         uniforms=block.pointer() if block else None,
         n_uniforms=block.values.size if block else 0,
         stream=torch.cuda.current_stream(dev).cuda_stream,
-        flags=_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
+        flags=(_ffi.FLAG_TIME_KERNELS if time_kernels else 0)
+        | (0 if persistent else _ffi.FLAG_STEPWISE))
     i64p = ctypes.POINTER(ctypes.c_int64)
     f64p = ctypes.POINTER(ctypes.c_double)
     out = _ffi.CauchyOut(rows=rows.ctypes.data_as(i64p), cols=cols.ctypes.data_as(i64p),

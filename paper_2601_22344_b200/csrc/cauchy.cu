@@ -16,6 +16,7 @@
 // memory tile of (y_j, B_j) (column side), so a step is FP64-pipe bound.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <string.h>
@@ -700,6 +701,452 @@ int cauchy_norms_impl(rplu_ctx* ctx, int p, long long n, long long m, const void
   return RPLU_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Resident Cauchy-like loop for small problems (BASELINE configs[1], C2):
+// ONE cooperative launch for the whole pivot loop and ONE grid barrier per
+// pivot step (the per-step launches above spend ~41 us per step at C2 on
+// three dependent kernels: masses 22, single-CTA select 13, update 4.5).
+//
+// Every CTA (one per SM, 512 threads) owns a contiguous row block of the
+// generators and keeps, for the whole run, in shared memory: its rows of G
+// and x, and a full private copy of B (plus |B_j|^2 for displacement rank 1)
+// that it updates itself every step.  Per step:
+//   1. masses of the CTA's rows from its shared-memory state (4 rows per
+//      thread x strided columns, per-row sums in a fixed order) -> global,
+//      double-buffered by step parity;
+//   2. the grid barrier;
+//   3. every CTA makes the SAME draws redundantly from the same data with the
+//      same code (stop rules, row CDF over the n masses, the pivot row
+//      generated from the global copy of G_i and the CTA's own B, column CDF
+//      in shared memory, relative zero-pivot guard with one resample) -- so
+//      nothing has to be broadcast and no second barrier is needed;
+//   4. every CTA updates its own G rows (and publishes them in the other of
+//      two global G buffers for the next steps' pivot-row lookups) and ALL of
+//      its private B copy.
+// CTA 0 records the outputs.  The arithmetic of every entry, row, column and
+// update is the per-step kernels' (numpy Smith division / products); the
+// summation order of the masses and the CDF width (512 instead of 1024
+// threads) differ, which moves draws only within rounding of a CDF boundary
+// (counted as near-boundary draws, as everywhere).
+namespace {
+
+constexpr int kResNT = 512;   // threads per CTA
+constexpr int kResRPT = 4;    // rows per thread in the mass phase
+
+struct CauchyResArgs {
+  CauchyParams q;
+  double* mbuf;       // [2][n] row masses (step parity)
+  double2* gbuf;      // [n * P] second global copy of G (ping-pong with q.G)
+  unsigned* sync;     // grid-barrier counter
+  double2* rglob;     // [m] the step's pivot row (each CTA generates a slice)
+  double* wglob;      // [m] its weights |r_j|^2
+  double* amaxg;      // [ctas] per-CTA max |r_j| of the slice
+  int rows_cta;       // rows per CTA (multiple of kResRPT)
+  long long* trace;   // optional CTA-0 phase timestamps [1024][8]
+};
+
+// dynamic shared memory: B | |B|^2 (P == 1) | weights / mass partials / row
+// masses | G rows | x rows | y (when it fits: YS)
+__host__ __device__ inline long long cauchy_res_wlen(long long n, long long m, int rows_cta) {
+  const int rg = rows_cta / kResRPT, cg = kResNT / (rg > 0 ? rg : 1);
+  long long w = (long long)rows_cta * cg;
+  if (m > w) w = m;
+  if (n > w) w = n;
+  return (w + 1) & ~1LL;
+}
+__host__ __device__ inline size_t cauchy_res_smem(long long n, long long m, int p, int rows_cta,
+                                                  bool ys) {
+  const long long me = (m + 1) & ~1LL;
+  return (size_t)m * p * 16 + (p == 1 ? (size_t)me * 8 : 0) +
+         (size_t)cauchy_res_wlen(n, m, rows_cta) * 8 + (size_t)rows_cta * (p + 1) * 16 +
+         (ys ? (size_t)m * 16 : 0);
+}
+
+__device__ __forceinline__ long long res_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int P, bool YS>
+__global__ void __launch_bounds__(kResNT, 1) cauchy_resident_kernel(CauchyResArgs a) {
+  constexpr int B = kResNT;
+  const CauchyParams& q = a.q;
+  extern __shared__ __align__(16) unsigned char res_smem[];
+  const long long n = q.n, m = q.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_cta = a.rows_cta, RG = rows_cta / kResRPT, CG = B / RG;
+  double2* sB = reinterpret_cast<double2*>(res_smem);
+  double* sbb = reinterpret_cast<double*>(sB + m * P);
+  double* sw = sbb + (P == 1 ? ((m + 1) & ~1LL) : 0);
+  double2* sg = reinterpret_cast<double2*>(sw + cauchy_res_wlen(n, m, rows_cta));
+  double2* sx = sg + (long long)rows_cta * P;
+  double2* sy = sx + rows_cta;   // YS: the column points, read in every phase
+  auto ycol = [&](long long j) -> double2 { return YS ? sy[j] : __ldg(q.y + j); };
+  __shared__ CdfSmem<B> sm;
+  __shared__ double s_red[B / 32];
+  __shared__ double s_val;
+
+  const long long row0 = (long long)blockIdx.x * rows_cta;
+  const int nrows = (int)max(0LL, min((long long)rows_cta, n - row0));
+  const bool lead = blockIdx.x == 0;
+  const bool tracing = a.trace != nullptr && lead && tid == 0;
+
+  // resident state
+  for (long long k = tid; k < m * P; k += B) sB[k] = q.Bt[k];
+  if constexpr (YS) {
+    for (long long j = tid; j < m; j += B) sy[j] = q.y[j];
+  }
+  if constexpr (P == 1) {
+    for (long long j = tid; j < m; j += B) {
+      const double2 bj = q.Bt[j];
+      sbb[j] = fma(bj.x, bj.x, bj.y * bj.y);
+    }
+  }
+  for (int k = tid; k < rows_cta; k += B) {
+    const long long i = (k < nrows) ? row0 + k : 0;   // padding rows repeat row 0 (never stored)
+    sx[k] = q.x[i];
+#pragma unroll
+    for (int l = 0; l < P; ++l) sg[k * P + l] = q.G[i * P + l];
+  }
+  __syncthreads();
+
+  auto block_max = [&](double v) -> double {   // block-uniform maximum
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    double r = s_red[0];
+#pragma unroll
+    for (int w = 1; w < B / 32; ++w) r = fmax(r, s_red[w]);
+    return r;
+  };
+
+  // loop state, identical in every thread of every CTA
+  long long ucount = 0, near = 0, done = 0, err_i = -1, err_j = -1, pi = -1, pj = -1;
+  int status = kRunning;
+  double u0 = 0.0;
+  unsigned nbar = 0;
+  const double2* Gcur = q.G;
+  double2* Gnext = a.gbuf;
+
+  for (long long t = 0; t < q.rank; ++t) {
+    double* M = a.mbuf + (size_t)(t & 1) * n;
+    if (tracing && t < 1024) a.trace[8 * t + 0] = res_clock();
+    // ---- 1. masses of this CTA's rows -------------------------------------
+    {
+      const int rg = tid / CG, cg = tid - rg * CG;
+      if (rg < RG) {
+        double2 xr[kResRPT], g[kResRPT][P];
+        double acc[kResRPT];
+#pragma unroll
+        for (int r = 0; r < kResRPT; ++r) {
+          xr[r] = sx[rg * kResRPT + r];
+#pragma unroll
+          for (int l = 0; l < P; ++l) g[r][l] = sg[(rg * kResRPT + r) * P + l];
+          acc[r] = 0.0;
+        }
+#pragma unroll 2
+        for (long long j = cg; j < m; j += CG) {
+          const double2 yj = ycol(j);
+          if constexpr (P == 1) {
+            const double bbj = sbb[j];
+            double den[kResRPT];
+#pragma unroll
+            for (int r = 0; r < kResRPT; ++r) {
+              const double dr = xr[r].x - yj.x, di = xr[r].y - yj.y;
+              den[r] = fma(dr, dr, di * di);
+            }
+#pragma unroll
+            for (int r = 0; r < kResRPT; ++r) acc[r] = fma(bbj, rcp_nr(den[r]), acc[r]);
+          } else {
+            double2 b[P];
+#pragma unroll
+            for (int l = 0; l < P; ++l) b[l] = sB[j * P + l];
+#pragma unroll
+            for (int r = 0; r < kResRPT; ++r) {
+              const double dr = xr[r].x - yj.x, di = xr[r].y - yj.y;
+              const double den = fma(dr, dr, di * di);
+              double re = 0.0, im = 0.0;
+#pragma unroll
+              for (int l = 0; l < P; ++l) {
+                re = fma(g[r][l].x, b[l].x, re);
+                re = fma(-g[r][l].y, b[l].y, re);
+                im = fma(g[r][l].x, b[l].y, im);
+                im = fma(g[r][l].y, b[l].x, im);
+              }
+              const double num = fma(re, re, im * im);
+              acc[r] = fma(num, rcp_nr(den), acc[r]);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kResRPT; ++r) {
+          if constexpr (P == 1) acc[r] *= fma(g[r][0].x, g[r][0].x, g[r][0].y * g[r][0].y);
+          sw[(rg * kResRPT + r) * CG + cg] = acc[r];
+        }
+      }
+      __syncthreads();
+      // per-row sum over the CG column groups: lane-strided partial sums, then
+      // a fixed shuffle tree (deterministic)
+      for (int lr = warp; lr < nrows; lr += B / 32) {
+        double v = 0.0;
+        for (int c = lane; c < CG; c += 32) v += sw[lr * CG + c];
+        v = warp_sum(v);
+        if (lane == 0) M[row0 + lr] = v;
+      }
+    }
+    if (tracing && t < 1024) a.trace[8 * t + 1] = res_clock();
+    // ---- 2. the step's one grid barrier ------------------------------------
+    grid_barrier(a.sync, gridDim.x * (++nbar));
+    if (tracing && t < 1024) a.trace[8 * t + 2] = res_clock();
+    // ---- 3a. stop rules and the row draw (cauchy_select_row_dev) ------------
+    // the n masses once from L2 into shared memory (the mass partials there
+    // were consumed before the barrier), then CDF / maximum / search from it
+    double mx = 0.0;
+    for (long long k = tid; k < n; k += B) {
+      const double v = __ldcg(M + k);
+      sw[k] = v;
+      mx = fmax(mx, v);
+    }
+    const double umax = block_max(mx);   // (its barriers publish sw)
+    auto wrow = [&](long long k) { return sw[k]; };
+    Cdf<B> cr = cdf_build<B>(wrow, n, sm);
+    if (lead && tid == 0) {
+      q.bmax[t] = umax;
+      q.bsum[t] = cr.total;
+    }
+    if (t == 0) u0 = umax;
+    if (umax <= 0.0) { status = kDegenerate; break; }
+    if (q.stop_tol > 0.0 && umax <= q.stop_tol * q.stop_tol * u0) { status = kTolStop; break; }
+    long long i;
+    if (q.rule == RPLU_RULE_RPLU) {
+      if (ucount + 1 > q.n_uniforms) { status = kUniformsExhausted; break; }
+      const double u1 = q.uniforms[ucount];
+      i = cdf_find<B>(wrow, n, cr, u1, sm);
+      const double tol = kNearBoundaryRel * cr.total, tg = u1 * cr.total;
+      if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+      ucount += 1;
+    } else {
+      i = block_argmax<B>(wrow, n, nullptr);
+    }
+    pi = i;
+    if (tracing && t < 1024) a.trace[8 * t + 3] = res_clock();
+    // ---- 3b. pivot row r_j = (G_i . B_j) / (x_i - y_j), weights |r_j|^2 -----
+    // Generated ONCE per step, a slice per CTA (two Smith divisions, one more
+    // division and a square root per entry: generating all m entries in every
+    // CTA cost 5.8 us of FP64-pipe time per step at C2), exchanged through
+    // global memory behind the step's second grid barrier.
+    double2 gi[P];
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+      const double* gp = reinterpret_cast<const double*>(Gcur + i * P + l);
+      gi[l] = make_double2(__ldcg(gp), __ldcg(gp + 1));
+    }
+    const double2 xi = q.x[i];
+    auto rgen = [&](long long j) -> double2 {
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double2 b = sB[j * P + l];
+        re = fma(gi[l].x, b.x, fma(-gi[l].y, b.y, re));
+        im = fma(gi[l].x, b.y, fma(gi[l].y, b.x, im));
+      }
+      const double2 yj = ycol(j);
+      return cdiv_np(make_double2(re, im), make_double2(xi.x - yj.x, xi.y - yj.y));
+    };
+    {
+      const long long per = (m + gridDim.x - 1) / gridDim.x;
+      const long long j0 = (long long)blockIdx.x * per, j1 = min(m, j0 + per);
+      double amax = 0.0;
+      for (long long j = j0 + tid; j < j1; j += B) {
+        const double2 r = rgen(j);
+        a.rglob[j] = r;
+        if (q.Rout) q.Rout[t * m + j] = r;
+        const double ab = cabs_np(r);
+        a.wglob[j] = ab * ab;
+        amax = fmax(amax, ab);
+      }
+      if (per <= 32) {   // the slice sits in warp 0: no CTA barrier
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (tid == 0) a.amaxg[blockIdx.x] = amax;
+      } else {
+        const double cmax = block_max(amax);
+        if (tid == 0) a.amaxg[blockIdx.x] = cmax;
+      }
+    }
+    grid_barrier(a.sync, gridDim.x * (++nbar));
+    double amax = 0.0;
+    for (long long j = tid; j < m; j += B) sw[j] = __ldcg(a.wglob + j);   // row masses consumed
+    for (int c = tid; c < (int)gridDim.x; c += B) amax = fmax(amax, __ldcg(a.amaxg + c));
+    const double rmax = block_max(amax);   // (its barriers also publish sw)
+    auto rget = [&](long long j) -> double2 {
+      const double* rp = reinterpret_cast<const double*>(a.rglob + j);
+      return make_double2(__ldcg(rp), __ldcg(rp + 1));
+    };
+    if (tracing && t < 1024) a.trace[8 * t + 4] = res_clock();
+    // ---- 3c. column draw with the relative zero-pivot guard ------------------
+    const double thr = kPivotRelTol * rmax;
+    auto wcol = [&](long long k) { return sw[k]; };
+    auto wabs = [&](long long k) { return cabs_np(rget(k)); };
+    long long j;
+    bool zero = false;
+    double2 apiv = make_double2(0.0, 0.0);   // r_j of the accepted column
+    if (q.rule == RPLU_RULE_RPLU) {
+      Cdf<B> cc = cdf_build<B>(wcol, m, sm);
+      int attempt = 0;
+      bool exhausted = false;
+      for (;;) {
+        if (ucount + 1 > q.n_uniforms) { exhausted = true; break; }
+        const double u2 = q.uniforms[ucount];
+        ucount += 1;
+        j = cdf_find<B>(wcol, m, cc, u2, sm);
+        const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;
+        if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
+        __syncthreads();
+        apiv = rget(j);
+        if (cabs_np(apiv) > thr) break;
+        if (attempt++ == 1) { zero = true; break; }
+      }
+      if (exhausted) { status = kUniformsExhausted; break; }
+    } else {
+      j = block_argmax<B>(wabs, m, nullptr);
+      apiv = rget(j);
+      if (!(cabs_np(apiv) > thr)) zero = true;
+    }
+    if (zero) {
+      status = kZeroPivot;
+      err_i = i;
+      err_j = j;
+      break;
+    }
+    pj = j;
+    const CDivCoef cf = cdiv_coef(apiv);
+    if (lead && tid == 0) {
+      q.rows[t] = i;
+      q.cols[t] = j;
+      if (q.Aout) q.Aout[t] = apiv;
+    }
+    done = t + 1;
+    if (tracing && t < 1024) a.trace[8 * t + 5] = res_clock();
+    // ---- 4. generator update (cauchy_update_kernel's arithmetic) -------------
+    double2 bj[P];
+#pragma unroll
+    for (int l = 0; l < P; ++l) bj[l] = sB[j * P + l];
+    const double2 yj = ycol(j);
+    __syncthreads();   // every thread holds B_j before any column changes
+    if (tid < rows_cta) {
+      double2 g[P];
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        g[l] = sg[tid * P + l];
+        re = fma(g[l].x, bj[l].x, fma(-g[l].y, bj[l].y, re));
+        im = fma(g[l].x, bj[l].y, fma(g[l].y, bj[l].x, im));
+      }
+      const double2 xk = sx[tid];
+      const double2 c = cdiv_np(make_double2(re, im), make_double2(xk.x - yj.x, xk.y - yj.y));
+      const bool valid = tid < nrows;
+      if (valid && q.Cout) q.Cout[t * n + row0 + tid] = c;
+      const double2 ca = cdiv_apply(c, cf);
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double2 pr = cmul_np(ca, gi[l]);
+        g[l] = make_double2(__dsub_rn(g[l].x, pr.x), __dsub_rn(g[l].y, pr.y));
+        sg[tid * P + l] = g[l];
+        if (valid) Gnext[(row0 + tid) * P + l] = g[l];
+      }
+    }
+#pragma unroll 4
+    for (long long l2 = tid; l2 < m; l2 += B) {
+      const double2 ra = cdiv_apply(rget(l2), cf);
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double2 b = sB[l2 * P + l];
+        const double2 pr = cmul_np(bj[l], ra);
+        const double2 nb = make_double2(__dsub_rn(b.x, pr.x), __dsub_rn(b.y, pr.y));
+        sB[l2 * P + l] = nb;
+        if constexpr (P == 1) sbb[l2] = fma(nb.x, nb.x, nb.y * nb.y);
+      }
+    }
+    __syncthreads();
+    {  // the other global G buffer takes over
+      const double2* tmp = Gcur;
+      Gcur = Gnext;
+      Gnext = const_cast<double2*>(tmp);
+    }
+    if (tracing && t < 1024) a.trace[8 * t + 6] = res_clock();
+  }
+
+  // every CTA leaves the loop at the same step; after one more barrier nobody
+  // reads the global generators any more and the final state goes back
+  grid_barrier(a.sync, gridDim.x * (++nbar));
+  for (int k = tid; k < nrows * P; k += B) q.G[row0 * P + k] = sg[k];
+  if (lead) {
+    for (long long k = tid; k < m * P; k += B) q.Bt[k] = sB[k];
+    if (tid == 0) {
+      DevState* st = q.st;
+      st->ucount = ucount;
+      st->near_boundary = near;
+      st->pi = pi;
+      st->pj = pj;
+      st->err_i = err_i;
+      st->err_j = err_j;
+      st->done = done;
+      st->active = 0;
+      st->status = status;
+      st->fro0 = u0;
+    }
+  }
+}
+
+}  // namespace
+
+// Resident-loop geometry for (n, m, p): CTAs, rows per CTA, shared memory
+// (0 CTAs: the problem does not fit).
+static int cauchy_resident_plan(int p, long long n, long long m, int sm_count, int* rows_cta,
+                                size_t* smem, bool* ys) {
+  if (p < 1 || p > 2 || n < 1 || m < 1) return 0;   // p > 2: 4 rows of G per thread spill
+  long long ctas = std::min<long long>(sm_count, (n + kResRPT - 1) / kResRPT);
+  const long long rows = (n + ctas * kResRPT - 1) / (ctas * kResRPT) * kResRPT;
+  if (rows > kResNT) return 0;   // one thread per own row in the update
+  ctas = (n + rows - 1) / rows;
+  *rows_cta = (int)rows;
+  static const size_t cap = [] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return (size_t)(optin > 8192 ? optin - 8192 : 0);   // static shared + reserve
+  }();
+  *ys = cauchy_res_smem(n, m, p, (int)rows, true) <= cap;   // y resident too when it fits
+  *smem = cauchy_res_smem(n, m, p, (int)rows, *ys);
+  return *smem <= cap ? (int)ctas : 0;
+}
+
+template <int P, bool YS>
+static int cauchy_resident_launch(rplu_ctx* ctx, const CauchyResArgs& a, int ctas, size_t smem,
+                                  cudaStream_t s) {
+  auto kern = cauchy_resident_kernel<P, YS>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    RPLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int per_sm = 0;
+  RPLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kResNT, smem));
+  if (per_sm < 1 || (long long)per_sm * ctx->sm_count < ctas) {
+    set_error("resident Cauchy loop does not fit on the device");
+    return RPLU_ERR_CUDA;
+  }
+  CauchyResArgs arg = a;
+  void* args[] = {&arg};
+  RPLU_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)ctas), dim3(kResNT), args,
+                                        smem, s));
+  return RPLU_OK;
+}
+
 __global__ void cauchy_init_state(DevState* st) {
   st->ucount = 0;
   st->near_boundary = 0;
@@ -773,6 +1220,69 @@ int cauchy_run_impl(rplu_ctx* ctx, const rplu_cauchy_args* a, rplu_cauchy_out* o
   // per-step GPU time of tens of microseconds: capture the loop as one graph
   const bool graph = (a->flags & (RPLU_FLAG_NO_GRAPH | RPLU_FLAG_TIME_KERNELS)) == 0 &&
                      (double)n * (double)m * p <= 256.0 * 1024 * 1024 && K >= 4;
+  // small problems: the whole loop in one cooperative launch (resident
+  // generators, one grid barrier per step) unless per-kernel timing or
+  // per-step launches were asked for (RPLU_CAUCHY_RESIDENT=0 disables)
+  int res_rows = 0;
+  size_t res_smem = 0;
+  bool res_ys = false;
+  static const bool res_env = [] {
+    const char* e = getenv("RPLU_CAUCHY_RESIDENT");
+    return !(e && e[0] == '0');
+  }();
+  const int res_ctas =
+      (res_env && (a->flags & (RPLU_FLAG_TIME_KERNELS | RPLU_FLAG_STEPWISE)) == 0 && K >= 1 &&
+       (double)n * (double)m * p <= 256.0 * 1024 * 1024)
+          ? cauchy_resident_plan(p, n, m, ctx->sm_count, &res_rows, &res_smem, &res_ys)
+          : 0;
+  if (res_ctas > 0) {
+    CauchyResArgs ra{};
+    ra.q = q;
+    ra.rows_cta = res_rows;
+    if ((rc = ctx->masses2.ensure(sizeof(double) * 2 * (size_t)n))) return rc;
+    if ((rc = ctx->scratch[3].ensure(sizeof(double2) * std::max<size_t>((size_t)n * p, 16)))) return rc;
+    if ((rc = ctx->gbar.ensure(2 * sizeof(unsigned)))) return rc;
+    ra.q.gsnap = nullptr;
+    ra.mbuf = reinterpret_cast<double*>(ctx->masses2.ptr);
+    ra.gbuf = reinterpret_cast<double2*>(ctx->scratch[3].ptr);
+    ra.sync = reinterpret_cast<unsigned*>(ctx->gbar.ptr);
+    ra.rglob = q.rbuf;                                   // scratch[1]: m double2
+    ra.wglob = q.wbuf;                                   // scratch[2]: m doubles
+    if ((rc = ctx->csync.ensure(std::max(sync_bytes, sizeof(double) * (size_t)res_ctas)))) return rc;
+    ra.amaxg = reinterpret_cast<double*>(ctx->csync.ptr);
+    RPLU_CUDA(cudaMemsetAsync(ctx->gbar.ptr, 0, 2 * sizeof(unsigned), s));
+    static const bool tracing = getenv("RPLU_PERSIST_TRACE") != nullptr;
+    if (tracing) {
+      RPLU_CUDA(cudaMalloc(&ra.trace, sizeof(long long) * 8 * 1024));
+      RPLU_CUDA(cudaMemsetAsync(ra.trace, 0, sizeof(long long) * 8 * 1024, s));
+    }
+    cauchy_init_state<<<1, 1, 0, s>>>(q.st);
+    if (p == 1)
+      rc = res_ys ? cauchy_resident_launch<1, true>(ctx, ra, res_ctas, res_smem, s)
+                  : cauchy_resident_launch<1, false>(ctx, ra, res_ctas, res_smem, s);
+    else
+      rc = res_ys ? cauchy_resident_launch<2, true>(ctx, ra, res_ctas, res_smem, s)
+                  : cauchy_resident_launch<2, false>(ctx, ra, res_ctas, res_smem, s);
+    if (rc) return rc;
+    launches = 2;
+    if (tracing) {
+      std::vector<long long> h(8 * 1024);
+      RPLU_CUDA(cudaMemcpyAsync(h.data(), ra.trace, sizeof(long long) * h.size(),
+                                cudaMemcpyDeviceToHost, s));
+      RPLU_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ra.trace);
+      const char* names[6] = {"masses", "barrier", "row draw", "pivot row", "col draw", "update"};
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      long long k = 0;
+      for (; k < 1024 && k < K && h[8 * k + 6] != 0; ++k)
+        for (int ph = 0; ph < 6; ++ph) acc[ph] += (double)(h[8 * k + ph + 1] - h[8 * k + ph]);
+      if (k > 0) {
+        fprintf(stderr, "[rplu] resident cauchy loop, CTA 0, %lld steps (us/step):", k);
+        for (int ph = 0; ph < 6; ++ph) fprintf(stderr, " %s %.2f", names[ph], acc[ph] / k / 1e3);
+        fprintf(stderr, "\n");
+      }
+    }
+  } else
   rc = run_maybe_graph(ctx, s, graph, 1, [&](cudaStream_t qs) -> int {
     RPLU_CUDA(cudaMemsetAsync(ctx->csync.ptr, 0, sync_bytes, qs));
     cauchy_init_state<<<1, 1, 0, qs>>>(q.st);

@@ -171,6 +171,36 @@ def test_vs_oracle_reduced(n, p, K, seed, cuda_device):
         assert np.abs(c / a - rc / ra).max() <= 1e-10 * np.abs(rc / ra).max()
 
 
+@pytest.mark.parametrize("n,m,p,rule,K,tol", [
+    (4096, 4096, 1, "rplu", 60, 0.0), (700, 523, 2, "rplu", 48, 0.0), (300, 300, 1, "c2plu", 30, 0.0),
+    (1000, 640, 1, "rplu", 200, 1e-3), (5, 9, 2, "rplu", 5, 0.0), (2600, 1500, 2, "c2plu", 16, 0.0)])
+def test_resident_loop_matches_stepwise(n, m, p, rule, K, tol, cuda_device):
+    """The resident cooperative loop (one launch, one grid barrier per step)
+    against the per-step kernels on the same inputs: same pivots, stop flags
+    and uniform consumption; columns, rows, pivot values and the final
+    generators to rounding (the mass summation order differs, nothing else)."""
+    if p == 1 and n == m:
+        x, y, G, B = gen.c2_cauchy(4, n=n)
+    else:
+        x, y, G, B = gen.c4_cauchy_like(4, n=n, m=m, p=p)
+    M = rp.CauchyLikeMatrix(x, y, G, B, check_points=False)
+    r1, r2 = rp.RngState(11), rp.RngState(11)
+    a = rp.structured_eliminate(M, rule, K, stop_tol=tol, rng=r1, keep_steps=True)
+    b = rp.structured_eliminate(M, rule, K, stop_tol=tol, rng=r2, keep_steps=True,
+                                persistent=False)
+    assert a.row_indices == b.row_indices and a.col_indices == b.col_indices
+    assert a.tol_stop == b.tol_stop and a.degenerate_stop == b.degenerate_stop
+    assert r1.uniform() == r2.uniform()
+    np.testing.assert_allclose(a.bound_maxes, b.bound_maxes, rtol=1e-12)
+    np.testing.assert_allclose(a.bound_sums, b.bound_sums, rtol=1e-12)
+    for (ca, ra, aa), (cb, rb, ab) in zip(a.steps, b.steps):
+        np.testing.assert_array_equal(ra, rb)      # same generators in -> same bits
+        np.testing.assert_array_equal(ca, cb)
+        assert aa == ab
+    np.testing.assert_array_equal(a.residual.G.cpu().numpy(), b.residual.G.cpu().numpy())
+    np.testing.assert_array_equal(a.residual.Bt.cpu().numpy(), b.residual.Bt.cpu().numpy())
+
+
 def test_c2plu_rule(cuda_device):
     x, y, G, B = gen.c4_cauchy_like(2, n=128, p=3)
     ref = oracle.structured_eliminate(x, y, G, B, "c2plu", 20)
