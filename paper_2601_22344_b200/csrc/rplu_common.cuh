@@ -511,17 +511,11 @@ __device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
   }
 }
 // sync[0]: grid-barrier arrivals
-// The arrival is a reduction without a return value (red.release): the
-// arriving thread starts polling at once instead of first waiting a full L2
-// round trip for the old value an atomicAdd would bring back.
-__device__ __forceinline__ void red_release_add_u32(unsigned* a, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    red_release_add_u32(bar, 1u);
+    atomicAdd(bar, 1u);
     wait_count(bar, target);
     __threadfence();
   }
