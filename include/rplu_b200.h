@@ -61,8 +61,8 @@ extern "C" {
 #define RPLU_FLAG_LAZY 4         /* dense: force the delayed-update loop */
 #define RPLU_FLAG_EAGER 8        /* dense: force the eager (update every step) loop;
                                     default: delayed updates when R exceeds L2 */
-#define RPLU_FLAG_STEPWISE 16   /* dense: per-step launches even where the whole loop would run
-                                    as one persistent cooperative launch */
+#define RPLU_FLAG_STEPWISE 16   /* dense / Cauchy-like: per-step launches even where the whole
+                                    loop would run as one resident cooperative launch */
 #define RPLU_FLAG_NO_GRAM 64    /* dense fp64 delayed-update loop: compute each step's
                                     masses by applying the pending terms (2q FP64 operations
                                     per element) instead of from the Gram form (one dot

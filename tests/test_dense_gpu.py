@@ -254,6 +254,36 @@ def test_ragged_shapes_and_stride(cuda_device):
         np.testing.assert_array_equal(tr.U, ref["U"])
 
 
+@pytest.mark.parametrize("shape,dtype", [((1449, 1450), np.float64), ((3001, 2999), np.float32),
+                                         ((1100, 1001), np.complex128), ((20_000_003,), np.float64)])
+def test_pageable_upload_ring(shape, dtype, cuda_device, monkeypatch):
+    """rplu_upload (worker pool, streaming stores, pinned ring): pageable
+    arrays above the direct-copy threshold arrive bit for bit, for sizes that
+    do not divide into the 64-byte granules / pieces, unaligned sources and
+    every staging thread count."""
+    from paper_2601_22344_b200 import _device
+    rs = np.random.default_rng(5)
+    n = int(np.prod(shape))
+    raw = rs.standard_normal(2 * n + 3)
+    a = (raw[:n] + 1j * raw[n:2 * n]).astype(dtype) if np.issubdtype(dtype, np.complexfloating) \
+        else raw[:n].astype(dtype)
+    a = a.reshape(shape)
+    assert a.nbytes >= 16 << 20
+    dev = torch.device("cuda", 0)
+    for threads in ("1", "3", "8", "16"):
+        monkeypatch.setenv("RPLU_UPLOAD_THREADS", threads)
+        t = _device.upload(a, dev)
+        torch.cuda.synchronize()
+        assert torch.equal(t.cpu(), torch.from_numpy(a))
+    # a source that is not 16-byte aligned (a view one element into a buffer)
+    buf = np.empty(n + 1, dtype=dtype)
+    v = buf[1:]
+    v[:] = a.reshape(-1)
+    t = _device.upload(v, dev)
+    torch.cuda.synchronize()
+    assert torch.equal(t.cpu(), torch.from_numpy(v))
+
+
 def test_device_tensor_inputs_stay_on_device(cuda_device):
     A = torch.from_numpy(gen.c1_dense(0, n=256)).cuda()
     tr = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(0)), 32)
