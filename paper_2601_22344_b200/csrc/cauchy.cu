@@ -839,6 +839,9 @@ __global__ void __launch_bounds__(kResNT, 1) cauchy_resident_kernel(CauchyResArg
   for (long long t = 0; t < q.rank; ++t) {
     double* M = a.mbuf + (size_t)(t & 1) * n;
     if (tracing && t < 1024) a.trace[8 * t + 0] = res_clock();
+    // the step's uniforms, fetched ahead of the draws that consume them
+    const bool pre = q.rule == RPLU_RULE_RPLU && ucount + 2 <= q.n_uniforms;
+    const double u1p = pre ? q.uniforms[ucount] : 0.0, u2p = pre ? q.uniforms[ucount + 1] : 0.0;
     // ---- 1. masses of this CTA's rows -------------------------------------
     {
       const int rg = tid / CG, cg = tid - rg * CG;
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(kResNT, 1) cauchy_resident_kernel(CauchyResArg
     long long i;
     if (q.rule == RPLU_RULE_RPLU) {
       if (ucount + 1 > q.n_uniforms) { status = kUniformsExhausted; break; }
-      const double u1 = q.uniforms[ucount];
+      const double u1 = pre ? u1p : q.uniforms[ucount];
       i = cdf_find<B>(wrow, n, cr, u1, sm);
       const double tol = kNearBoundaryRel * cr.total, tg = u1 * cr.total;
       if (fabs(sm.lo_c - tg) <= tol || fabs(sm.hi_c - tg) <= tol) near++;
@@ -1006,7 +1009,7 @@ __global__ void __launch_bounds__(kResNT, 1) cauchy_resident_kernel(CauchyResArg
       bool exhausted = false;
       for (;;) {
         if (ucount + 1 > q.n_uniforms) { exhausted = true; break; }
-        const double u2 = q.uniforms[ucount];
+        const double u2 = (pre && attempt == 0) ? u2p : q.uniforms[ucount];
         ucount += 1;
         j = cdf_find<B>(wcol, m, cc, u2, sm);
         const double tol = kNearBoundaryRel * cc.total, tg = u2 * cc.total;

@@ -297,11 +297,34 @@ __device__ long long cdf_find_target(const WF& wf, long long n, const Cdf<BLOCK>
         const long long k = base + 32 * u + lane;
         xs[u] = (k < hi) ? wf(k) : 0.0;
       }
+      // CTAs of <= 512 threads (register budget >= 128): the slabs' inclusive
+      // scans all interleaved round by round -- the same shuffle-add sequence
+      // per slab as warp_incl_scan, so identical values; one after the other
+      // they are the draw's longest serial chain (C2 resident loop: 3.6 -> 3.3
+      // us per draw).  With 1024 threads (64 registers) the eight live scans
+      // spill and the draws got slower (C1 resident loop 58k -> 50k steps/s),
+      // so those kernels scan slab by slab.
+      constexpr bool kInterleave = BLOCK <= 512;
+      double ps[kCdfUnroll];
+      if constexpr (kInterleave) {
+#pragma unroll
+        for (int u = 0; u < kCdfUnroll; ++u) ps[u] = xs[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+          for (int u = 0; u < kCdfUnroll; ++u) {
+            const double y = __shfl_up_sync(0xffffffffu, ps[u], o);
+            if (lane >= o) ps[u] += y;
+          }
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kCdfUnroll; ++u) {
         const long long sb = base + 32 * u;
         if (done || sb >= hi) break;
-        const double p = warp_incl_scan(xs[u]);
+        double p;
+        if constexpr (kInterleave) p = ps[u];
+        else p = warp_incl_scan(xs[u]);
         const double ck = cbase + (ex + (run + p));
         const unsigned hit = __ballot_sync(0xffffffffu, (sb + lane < hi) && ck > target);
         if (hit) {
