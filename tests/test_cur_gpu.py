@@ -79,6 +79,24 @@ def test_gauss_operator_matches_host(cuda_device):
     np.testing.assert_allclose(got, K[:, [1, 2, 499]] @ w.cpu().numpy(), rtol=1e-13, atol=1e-15)
 
 
+def test_gauss_gemv_wide_box_takes_difference_form(cuda_device):
+    """K7 chooses its exponent form on the device from the points' bounding
+    box: a box that is wide against the bandwidth (K r2 >= 8000, here ~1e5)
+    must take the difference form (the dot-product form would lose the
+    exponent's low bits); a narrow one takes the dot-product form.  Both
+    against the host product, and row norms against the host's."""
+    rs = np.random.default_rng(2)
+    for scale, n, m in ((6.0, 900, 700), (1.0, 1300, 1100)):
+        P = scale * rs.random((n, 3))
+        Q = P[rs.integers(0, n, m)] + 0.05 * rs.standard_normal((m, 3))   # near pairs exist
+        op = rp.GaussianKernelOperator(P, Q)
+        K = oracle.GaussianKernelHost(P, Q).materialize()
+        v = rs.standard_normal(m)
+        ref = K @ v
+        np.testing.assert_allclose(op.apply(v), ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+        np.testing.assert_allclose(op.row_norms(), np.einsum("ij,ij->i", K, K), rtol=1e-12)
+
+
 def test_cur_matches_dense_pivots(cuda_device):
     """SPEC acceptance 7: CUR-form index sets equal the dense two-stage RPLU
     pivots (both on the GPU) on 60x60 planted instances."""
