@@ -125,7 +125,17 @@ __global__ void gauss_geo_kernel(const double* __restrict__ part, int nparts, do
   }
 }
 
-template <int RPT, int TJ, bool SQUARE, int CU = 2>
+// FACT (GEMV only): the per-point parts of the exponent are factored out of
+// the entry, e_ij = A_i B_j E(t_ij) with A_i = exp(-|p~_i|^2), B_j =
+// exp(-|q~_j|^2) and t_ij = p~_i . q~~_j, so that g_i = A_i sum_j (B_j v_j)
+// E(t_ij): the column weight w_j = B_j v_j is formed once per tile column and
+// A_i once per row, and the entry needs a bare 3-term dot product (DMUL + 2
+// DFMA) -- 13 FP64-pipe instructions instead of 14 and 4 doubles per column
+// in shared memory instead of 5.  Every term of a row carries the same factor
+// 1/A_i, so the relative sizes of the summands (and the rounding of the sum)
+// are unchanged; K r2 < 8000 keeps A_i, B_j >= 2^-250 and E <= 2^500 inside
+// the double range.
+template <int RPT, int TJ, bool SQUARE, int CU = 2, bool FACT = false>
 __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
                                                              const double* __restrict__ v,
                                                              double* __restrict__ partial,
@@ -133,13 +143,16 @@ __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
                                                              const double* __restrict__ geo) {
   constexpr int NT = 256;
   if (!(geo[3] < kDotRange)) return;
-  __shared__ __align__(16) double sq[TJ * 6];
+  static_assert(!(FACT && SQUARE), "the factored form is for the GEMV");
+  constexpr int SQ = FACT ? 4 : 6;   // doubles per tile column
+  __shared__ __align__(16) double sq[TJ * SQ];
   const double c0x = geo[0], c0y = geo[1], c0z = geo[2];
   const long long row_base = (long long)blockIdx.x * NT * RPT;
   const long long cols_per = (op.m + splits - 1) / splits;
   const long long j0 = (long long)blockIdx.y * cols_per;
   const long long j1 = min(op.m, j0 + cols_per);
   const ExpTab tl = exp2tab_lane_comp();
+  const ExpTab tp = exp2tab_lane();   // plain table for the per-point factors (FACT)
   double px[RPT], py[RPT], pz[RPT], pa[RPT], acc[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -148,22 +161,31 @@ __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
     px[r] = op.c * (op.P[ii * 3 + 0] - c0x);
     py[r] = op.c * (op.P[ii * 3 + 1] - c0y);
     pz[r] = op.c * (op.P[ii * 3 + 2] - c0z);
-    pa[r] = -kExpK * fma(pz[r], pz[r], fma(py[r], py[r], px[r] * px[r]));
+    const double p2 = fma(pz[r], pz[r], fma(py[r], py[r], px[r] * px[r]));
+    pa[r] = FACT ? exp_neg(p2, tp) : -kExpK * p2;   // A_i, or a_i in table units
     acc[r] = 0.0;
   }
   for (long long jt = j0; jt < j1; jt += TJ) {
     const int cnt = (int)min((long long)TJ, j1 - jt);
     __syncthreads();
-    for (int cc = threadIdx.x; cc < cnt; cc += NT) {
-      const long long j = jt + cc;
+    // (warp-uniform trip count: the factored form's exp shuffles need every lane)
+    for (int cb = 0; cb < TJ; cb += NT) {
+      const int cc = cb + (int)threadIdx.x;
+      const long long j = min(jt + cc, j1 - 1);
       const double qx = op.c * (op.Q[j * 3 + 0] - c0x);
       const double qy = op.c * (op.Q[j * 3 + 1] - c0y);
       const double qz = op.c * (op.Q[j * 3 + 2] - c0z);
-      sq[cc * 6 + 0] = (2.0 * kExpK) * qx;
-      sq[cc * 6 + 1] = (2.0 * kExpK) * qy;
-      sq[cc * 6 + 2] = (2.0 * kExpK) * qz;
-      sq[cc * 6 + 3] = -kExpK * fma(qz, qz, fma(qy, qy, qx * qx));
-      sq[cc * 6 + 4] = SQUARE ? 1.0 : v[j];
+      const double q2 = fma(qz, qz, fma(qy, qy, qx * qx));
+      double last;
+      if constexpr (FACT) last = exp_neg(q2, tp) * v[j];   // w_j = B_j v_j
+      else last = -kExpK * q2;                             // b_j in table units
+      if (cc < cnt) {
+        sq[cc * SQ + 0] = (2.0 * kExpK) * qx;
+        sq[cc * SQ + 1] = (2.0 * kExpK) * qy;
+        sq[cc * SQ + 2] = (2.0 * kExpK) * qz;
+        sq[cc * SQ + 3] = last;
+        if constexpr (!FACT) sq[cc * SQ + 4] = SQUARE ? 1.0 : v[j];
+      }
     }
     __syncthreads();
     // CU columns x RPT rows = E independent entries per trip, every stage
@@ -174,27 +196,30 @@ __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
       double y[E], e[E], vj[CU];
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
-        const double qz = sq[(cc + u) * 6 + 2], qb = sq[(cc + u) * 6 + 3];
+        const double qz = sq[(cc + u) * SQ + 2], qb = sq[(cc + u) * SQ + 3];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(pz[r], qz, qb);
+        for (int r = 0; r < RPT; ++r) y[u * RPT + r] = FACT ? pz[r] * qz : fma(pz[r], qz, qb);
+        if constexpr (FACT) vj[u] = qb;   // the column weight w_j
       }
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
-        const double qy = sq[(cc + u) * 6 + 1];
+        const double qy = sq[(cc + u) * SQ + 1];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(py[r], qy, y[u * RPT + r]);
       }
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
-        const double qx = sq[(cc + u) * 6 + 0];
-        vj[u] = sq[(cc + u) * 6 + 4];
+        const double qx = sq[(cc + u) * SQ + 0];
+        if constexpr (!FACT) vj[u] = sq[(cc + u) * SQ + 4];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) y[u * RPT + r] = fma(px[r], qx, y[u * RPT + r]);
       }
+      if constexpr (!FACT) {
 #pragma unroll
-      for (int u = 0; u < CU; ++u)
+        for (int u = 0; u < CU; ++u)
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) y[u * RPT + r] += pa[r];
+          for (int r = 0; r < RPT; ++r) y[u * RPT + r] += pa[r];
+      }
       exp_tab_units_v<E>(y, e, tl);
 #pragma unroll
       for (int u = 0; u < CU; ++u)
@@ -204,12 +229,13 @@ __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
                           : fma(e[u * RPT + r], vj[u], acc[r]);
     }
     for (; cc < cnt; ++cc) {   // tile tail (cnt % CU columns)
-      const double qx = sq[cc * 6 + 0], qy = sq[cc * 6 + 1], qz = sq[cc * 6 + 2];
-      const double qb = sq[cc * 6 + 3], vj = sq[cc * 6 + 4];
+      const double qx = sq[cc * SQ + 0], qy = sq[cc * SQ + 1], qz = sq[cc * SQ + 2];
+      const double qb = sq[cc * SQ + 3], vj = FACT ? qb : sq[cc * SQ + (FACT ? 3 : 4)];
       double y[RPT], e[RPT];
 #pragma unroll
       for (int r = 0; r < RPT; ++r)
-        y[r] = fma(px[r], qx, fma(py[r], qy, fma(pz[r], qz, qb))) + pa[r];
+        y[r] = FACT ? fma(px[r], qx, fma(py[r], qy, pz[r] * qz))
+                    : fma(px[r], qx, fma(py[r], qy, fma(pz[r], qz, qb))) + pa[r];
       exp_tab_units_v<RPT>(y, e, tl);
 #pragma unroll
       for (int r = 0; r < RPT; ++r) acc[r] = SQUARE ? fma(e[r], e[r], acc[r]) : fma(e[r], vj, acc[r]);
@@ -218,7 +244,7 @@ __global__ void __launch_bounds__(256) gauss_gemv_dot_kernel(GaussOp op,
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     long long i = row_base + threadIdx.x + (long long)r * NT;
-    if (i < op.n) partial[(long long)blockIdx.y * op.n + i] = acc[r];
+    if (i < op.n) partial[(long long)blockIdx.y * op.n + i] = FACT ? acc[r] * pa[r] : acc[r];
   }
 }
 
@@ -412,9 +438,19 @@ static void gemv_launch(const GaussOp& op, const double* v, double* part, int sp
     else gauss_gemv_dot_kernel<RPT, TJ, true, 4><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
     gauss_gemv_kernel<RPT, TJ, true><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
   } else {
-    if (cu == 1) gauss_gemv_dot_kernel<RPT, TJ, false, 1><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
-    else if (cu == 2) gauss_gemv_dot_kernel<RPT, TJ, false, 2><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
-    else gauss_gemv_dot_kernel<RPT, TJ, false, 4><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    static const bool fact = [] {   // RPLU_GEMV_FACT=0: unfactored exponent (14 FP64 per entry)
+      const char* e = getenv("RPLU_GEMV_FACT");
+      return !(e && atoi(e) == 0);
+    }();
+    if (fact) {
+      if (cu == 1) gauss_gemv_dot_kernel<RPT, TJ, false, 1, true><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+      else if (cu == 2) gauss_gemv_dot_kernel<RPT, TJ, false, 2, true><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+      else gauss_gemv_dot_kernel<RPT, TJ, false, 4, true><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    } else {
+      if (cu == 1) gauss_gemv_dot_kernel<RPT, TJ, false, 1><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+      else if (cu == 2) gauss_gemv_dot_kernel<RPT, TJ, false, 2><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+      else gauss_gemv_dot_kernel<RPT, TJ, false, 4><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
+    }
     gauss_gemv_kernel<RPT, TJ, false><<<grid, 256, 0, s>>>(op, v, part, splits, geo);
   }
 }
