@@ -130,7 +130,7 @@ __global__ void gauss_geo_kernel(const double* __restrict__ part, int nparts, do
 // exp(-|q~_j|^2) and t_ij = p~_i . q~~_j, so that g_i = A_i sum_j (B_j v_j)
 // E(t_ij): the column weight w_j = B_j v_j is formed once per tile column and
 // A_i once per row, and the entry needs a bare 3-term dot product (DMUL + 2
-// DFMA) -- 13 FP64-pipe instructions instead of 14 and 4 doubles per column
+// DFMA) -- one FP64-pipe instruction less per entry and 4 doubles per column
 // in shared memory instead of 5.  Every term of a row carries the same factor
 // 1/A_i, so the relative sizes of the summands (and the rounding of the sum)
 // are unchanged; K r2 < 8000 keeps A_i, B_j >= 2^-250 and E <= 2^500 inside

@@ -60,33 +60,6 @@ __device__ __forceinline__ double exp_neg(double d2, ExpTab tab) {
   return k < -32700 ? 0.0 : e;                 // k < -32*1021.9: below 1e-307
 }
 
-// exp(y ln2/32) for an exponent y <= 0 already in table units (the dot-product
-// form of K7 builds y = -K |p'-q'|^2 as a_i + b_j + p'.q'' in 4 FP64 ops): the
-// shifter add, the exact k subtraction and the exact reduced argument are
-// three DADDs, so an entry costs 14 FP64-pipe operations.  The caller
-// guarantees y > -32000 (no underflow cut, no compare / select).
-__device__ __forceinline__ double exp_tab_units(double y, ExpTab tab) {
-  const double shifter = 6755399441055744.0;
-  const double sft = y + shifter;
-  const double kd = sft - shifter;
-  const int k = __double2loint(sft);
-  const double s = y - kd;                     // exact, |s| <= 1/2
-  double p = 3.9736907164886624e-11;
-  p = fma(p, s, 9.172616497450463e-09);
-  p = fma(p, s, 1.6938509725336998e-06);
-  p = fma(p, s, 0.00023459619819720352);
-  p = fma(p, s, 0.021660849392498283);
-  p = fma(p, s, 1.0);
-  const double t = __shfl_sync(0xffffffffu, tab, k & 31);
-  const double ts = __hiloint2double(__double2hiint(t) + ((k >> 5) << 20), __double2loint(t));
-  return p * ts;
-}
-
-// The same for E independent exponents, written stage by stage across the
-// E entries so that the E dependency chains are interleaved in program order
-// (a DFMA's dependent-issue latency is ~16 cycles on B200 and the FP64 pipe
-// takes a warp instruction every 2: one chain per warp leaves the pipe at
-// 6 warps / 16 cycles = 73% busy, as ncu measured on the first version).
 // polynomial coefficients as constant-bank operands (as immediates they were
 // re-materialised into uniform registers every trip: ~1 extra issue slot per
 // entry)
@@ -97,14 +70,20 @@ static __constant__ double kExpPoly[5] = {3.9736907164886624e-11, 9.172616497450
 template <int E>
 __device__ __forceinline__ void exp_tab_units_v(const double (&y)[E], double (&e)[E],
                                                 ExpTab tab) {
-  const double shifter = 6755399441055744.0;
-  double sft[E], s[E], p[E];
+  // k = round(y) and the reduced argument s = y - k (exact, |s| <= 1/2).  The
+  // rounding and the integer come from the conversion unit (FRND.F64,
+  // F2I.F64: both round to nearest even, so they agree) instead of the
+  // shifter trick's two DADDs: the FP64 pipe keeps 11 instructions per entry
+  // of the factored GEMV (3 dot + 1 subtract + 5 polynomial + scale +
+  // accumulate) (same box, n = m = 10^6: 903 against 929 ms).
+  double s[E], p[E];
+  int k[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) sft[i] = y[i] + shifter;
+  for (int i = 0; i < E; ++i) s[i] = rint(y[i]);
 #pragma unroll
-  for (int i = 0; i < E; ++i) s[i] = sft[i] - shifter;
+  for (int i = 0; i < E; ++i) k[i] = __double2int_rn(y[i]);
 #pragma unroll
-  for (int i = 0; i < E; ++i) s[i] = y[i] - s[i];                 // exact, |s| <= 1/2
+  for (int i = 0; i < E; ++i) s[i] = y[i] - s[i];
 #pragma unroll
   for (int i = 0; i < E; ++i) p[i] = fma(kExpPoly[0], s[i], kExpPoly[1]);
 #pragma unroll
@@ -119,15 +98,14 @@ __device__ __forceinline__ void exp_tab_units_v(const double (&y)[E], double (&e
   // word has (lane << 15) subtracted, so adding k << 15 = (n << 20) + (j << 15)
   // to the word fetched from lane j = k mod 32 (the shuffle takes the index
   // modulo 32 itself) lands exactly on 2^n 2^(j/32): one integer instruction
-  // and two shuffles per entry beside the 14 FP64 ones.  Every FP64 warp
+  // and two shuffles per entry beside the FP64 ones.  Every FP64 warp
   // instruction holds the SM sub-partition's dispatch port for two cycles, so
-  // each further instruction costs 1/28 of the entry's time.
+  // each further instruction costs about 1/22 of the entry's FP64 time.
 #pragma unroll
   for (int i = 0; i < E; ++i) {
-    const int k = __double2loint(sft[i]);
-    const int hi = __shfl_sync(0xffffffffu, __double2hiint(tab), k);
-    const int lo = __shfl_sync(0xffffffffu, __double2loint(tab), k);
-    e[i] = p[i] * __hiloint2double(hi + (k << 15), lo);
+    const int hi = __shfl_sync(0xffffffffu, __double2hiint(tab), k[i]);
+    const int lo = __shfl_sync(0xffffffffu, __double2loint(tab), k[i]);
+    e[i] = p[i] * __hiloint2double(hi + (k[i] << 15), lo);
   }
 }
 

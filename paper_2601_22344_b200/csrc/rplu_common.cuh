@@ -77,6 +77,23 @@ __device__ __forceinline__ double cabs_np(double2 a) {
 }
 
 // ---------------------------------------------------------------------------
+// fast FP64 reciprocal: MUFU.RCP64H seed (relative error <= 2^-19.9 over 2^30
+// samples on B200, scripts/probes/rcp_probe.cu) + ONE cubic step
+//   e = 1 - d r0,  r1 = r0 (1 + e + e^2)      (error e^3 ~ 2^-60 + rounding)
+// in three DFMA: <= 2 ulp (0.03% of arguments differ from the correctly
+// rounded 1/d at all).  Two Newton steps reproduce the correctly rounded
+// value for every sample but cost four DFMA -- one of K5's 9 (p = 1) or 27
+// (p = 4) FP64 instructions per generated entry.  The masses are sums of
+// ~m such terms and only feed the sampling weights.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fma(-d, r, 1.0);
+  const double t = fma(e, e, e);
+  return fma(r, t, r);
+}
+
+// ---------------------------------------------------------------------------
 // scalar traits
 
 template <typename T> struct Scalar;
