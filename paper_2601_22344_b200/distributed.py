@@ -114,10 +114,17 @@ def _run_sharded_block_graph(backend, steps, group, block):
     if nblocks >= 2 and backend.active():
         torch.cuda.synchronize(backend.dev)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for pos in range(block):
-                step(-1 - pos)
-        for k in range(1, nblocks):
+        try:
+            with torch.cuda.graph(g):
+                for pos in range(block):
+                    step(-1 - pos)
+        except RuntimeError:
+            # capture refused (e.g. a collective backend that cannot be
+            # captured): nothing of the block has run, the device step
+            # counter is untouched -- carry on with explicit steps
+            g = None
+            torch.cuda.synchronize(backend.dev)
+        for k in range(1, nblocks if g is not None else 0):
             g.replay()
             t += block
             if k % 2 == 0 and k + 1 < nblocks and not backend.active():
