@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <thread>
@@ -73,12 +74,16 @@ void build_tree(const double* p, int64_t n, int64_t leaf_size, Tree& t) {
   for (int64_t i = 0; i < n; ++i) pts[i] = Pt{p[2 * i], p[2 * i + 1], i};
   t.pbeg = {0};
   t.pend = {n};
+  // a node's points sit in `pts` or in `tmp` (side 0 / 1): the partition
+  // scatters them into the other array, so nothing is copied back
+  std::vector<uint8_t> side = {0};
   std::vector<uint8_t> cls(n);
   std::vector<int64_t> todo = {0};
   while (!todo.empty()) {
     const int64_t k = todo.back();
     todo.pop_back();
-    Pt* idx = pts.data() + t.pbeg[k];
+    Pt* idx = (side[k] ? tmp : pts).data() + t.pbeg[k];
+    Pt* dst = (side[k] ? pts : tmp).data() + t.pbeg[k];
     const int64_t cnt = t.pend[k] - t.pbeg[k];
     bool same = true;
     const double rx = idx[0].x, ry = idx[0].y;
@@ -102,8 +107,7 @@ void build_tree(const double* p, int64_t n, int64_t leaf_size, Tree& t) {
     }
     int64_t off[4] = {0, count[0], count[0] + count[1], count[0] + count[1] + count[2]};
     const int64_t start[4] = {off[0], off[1], off[2], off[3]};
-    for (int64_t q = 0; q < cnt; ++q) tmp[off[cls[q]]++] = idx[q];
-    std::copy(tmp.begin(), tmp.begin() + cnt, idx);
+    for (int64_t q = 0; q < cnt; ++q) dst[off[cls[q]]++] = idx[q];
     const double bx[4] = {t.x0[k], cx, t.x0[k], cx};
     const double by[4] = {cy, cy, t.y0[k], t.y0[k]};
     std::vector<int64_t> kids;
@@ -117,13 +121,17 @@ void build_tree(const double* p, int64_t n, int64_t leaf_size, Tree& t) {
       t.children.emplace_back();
       t.pbeg.push_back(t.pbeg[k] + start[q]);
       t.pend.push_back(t.pbeg[k] + start[q] + count[q]);
+      side.push_back((uint8_t)(side[k] ^ 1));
       kids.push_back(c);
       todo.push_back(c);
     }
     t.children[k] = kids;
   }
-  t.order.resize(n);
-  for (int64_t q = 0; q < n; ++q) t.order[q] = pts[q].i;
+  t.order.resize(n);   // the leaves tile [0, n)
+  for (int64_t k : t.leaves) {
+    const Pt* from = (side[k] ? tmp : pts).data();
+    for (int64_t q = t.pbeg[k]; q < t.pend[k]; ++q) t.order[q] = from[q].i;
+  }
 }
 
 // (d_min^2, d_max^2) between square ia of tree a and square ib of tree b
@@ -174,56 +182,145 @@ int rplu_plan_build(const double* x, int64_t n, const double* y, int64_t m, doub
     for (int64_t k = leaf; k != -1; k = tgt.parent[k]) under[k].push_back(leaf);
   std::vector<int64_t> slot(tgt.x0.size(), -1);
   for (size_t q = 0; q < tgt.leaves.size(); ++q) slot[tgt.leaves[q]] = (int64_t)q;
-  std::vector<std::vector<std::pair<int64_t, double>>> agg(tgt.leaves.size());
-  std::vector<std::vector<int64_t>> exact(tgt.leaves.size());
-  std::vector<std::pair<int64_t, int64_t>> todo = {{0, 0}};
-  while (!todo.empty()) {
-    const auto st = todo.back();
-    todo.pop_back();
-    const int64_t s = st.first, t = st.second;
-    double dmin2, dmax2;
+  // The dual traversal (Alg C.1) in the reference's order -- a stack whose
+  // last pushed pair is visited first -- split into independent subtrees: the
+  // top kSplitDepth levels are expanded on this thread into the list of
+  // subtree roots IN VISITING ORDER, worker threads traverse the subtrees
+  // into private record lists, and the records are appended to the per-leaf
+  // lists in root order, so every list comes out exactly as the sequential
+  // traversal writes it (115 -> ~30 ms at 2^20 points per side).
+  struct AggRec { int64_t slot, node; double alpha; };
+  struct ExRec { int64_t slot, node; };
+  struct Task {
+    int64_t s, t;
+    std::vector<AggRec> agg;
+    std::vector<ExRec> ex;
+    bool coincide = false;
+    int64_t ca = -1, cb = -1;
+  };
+  auto admissible = [&](int64_t s, int64_t t, double& dmin2) {
+    double dmax2;
     box_dist2(src, s, tgt, t, dmin2, dmax2);
-    if (dmin2 > 0.0 && dmax2 <= nu * dmin2) {
-      for (int64_t leaf : under[t]) {
-        double lmin2, lmax2;
-        box_dist2(src, s, tgt, leaf, lmin2, lmax2);
-        agg[slot[leaf]].push_back({s, 1.0 / lmin2});
-      }
-      continue;
-    }
+    return dmin2 > 0.0 && dmax2 <= nu * dmin2;
+  };
+  // children of a non-terminal pair in PUSH order (the reference pushes them
+  // in this order and pops the last one first)
+  auto push_order = [&](int64_t s, int64_t t, std::vector<std::pair<int64_t, int64_t>>& out) {
     const bool s_leaf = src.children[s].empty(), t_leaf = tgt.children[t].empty();
-    if (s_leaf && t_leaf) {
-      if (dmin2 == 0.0) {  // coincident target / source points (treebounds.py:183-194)
-        for (int64_t qa = 0; qa < tgt.npts(t); ++qa)
-          for (int64_t qb = 0; qb < src.npts(s); ++qb) {
-            const int64_t a = tgt.pts(t)[qa], b = src.pts(s)[qb];
-            if (x[2 * a] == y[2 * b] && x[2 * a + 1] == y[2 * b + 1]) {
-              if (coincident) { coincident[0] = a; coincident[1] = b; }
-              rplu::set_error("coincident target / source points");
-              delete h;
-              return RPLU_ERR_ARG;
-            }
-          }
-      }
-      exact[slot[t]].push_back(s);
-      continue;
-    }
     if ((tgt.size[t] >= src.size[s] && !t_leaf) || s_leaf) {
-      for (int64_t c : tgt.children[t]) todo.push_back({s, c});
+      for (int64_t c : tgt.children[t]) out.push_back({s, c});
     } else {
-      for (int64_t c : src.children[s]) todo.push_back({c, t});
+      for (int64_t c : src.children[s]) out.push_back({c, t});
+    }
+  };
+  auto run_task = [&](Task& task) {
+    std::vector<std::pair<int64_t, int64_t>> todo = {{task.s, task.t}};
+    while (!todo.empty()) {
+      const auto st = todo.back();
+      todo.pop_back();
+      const int64_t s = st.first, t = st.second;
+      double dmin2;
+      if (admissible(s, t, dmin2)) {
+        for (int64_t leaf : under[t]) {
+          double lmin2, lmax2;
+          box_dist2(src, s, tgt, leaf, lmin2, lmax2);
+          task.agg.push_back({slot[leaf], s, 1.0 / lmin2});
+        }
+        continue;
+      }
+      const bool s_leaf = src.children[s].empty(), t_leaf = tgt.children[t].empty();
+      if (s_leaf && t_leaf) {
+        if (dmin2 == 0.0) {  // coincident target / source points (treebounds.py:183-194)
+          for (int64_t qa = 0; qa < tgt.npts(t) && !task.coincide; ++qa)
+            for (int64_t qb = 0; qb < src.npts(s); ++qb) {
+              const int64_t a = tgt.pts(t)[qa], b = src.pts(s)[qb];
+              if (x[2 * a] == y[2 * b] && x[2 * a + 1] == y[2 * b + 1]) {
+                task.coincide = true;
+                task.ca = a;
+                task.cb = b;
+                break;
+              }
+            }
+          if (task.coincide) return;
+        }
+        task.ex.push_back({slot[t], s});
+        continue;
+      }
+      push_order(s, t, todo);
+    }
+  };
+  constexpr int kSplitDepth = 4;
+  std::vector<Task> tasks;
+  {
+    struct Item { int64_t s, t; int depth; };
+    std::vector<Item> st = {{0, 0, 0}};
+    std::vector<std::pair<int64_t, int64_t>> kids;
+    while (!st.empty()) {
+      const Item it = st.back();
+      st.pop_back();
+      double dmin2;
+      const bool term = admissible(it.s, it.t, dmin2) ||
+                        (src.children[it.s].empty() && tgt.children[it.t].empty());
+      if (term || it.depth == kSplitDepth) {
+        tasks.emplace_back();
+        tasks.back().s = it.s;
+        tasks.back().t = it.t;
+        continue;
+      }
+      kids.clear();
+      push_order(it.s, it.t, kids);
+      for (const auto& c : kids) st.push_back({c.first, c.second, it.depth + 1});
     }
   }
-  h->agg_start.push_back(0);
-  h->ex_start.push_back(0);
-  for (size_t q = 0; q < tgt.leaves.size(); ++q) {
-    for (const auto& e : agg[q]) {
-      h->agg_node.push_back(e.first);
-      h->agg_alpha.push_back(e.second);
+  {
+    unsigned hw = std::thread::hardware_concurrency();
+    const int nthreads = (int)std::max(1u, std::min(std::min(hw ? hw : 1u, 8u),
+                                                    (unsigned)tasks.size()));
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+      for (size_t k = next.fetch_add(1); k < tasks.size(); k = next.fetch_add(1)) run_task(tasks[k]);
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < nthreads; ++w) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+  }
+  // records -> CSR lists per target leaf, in visiting order (count, prefix,
+  // fill: two passes over the records; appending them to one vector per leaf
+  // and flattening those cost 120 ms at 2^20 points per side)
+  const size_t nleaf = tgt.leaves.size();
+  for (const Task& task : tasks) {   // the first coincidence in visiting order wins, as in the reference
+    if (task.coincide) {
+      if (coincident) { coincident[0] = task.ca; coincident[1] = task.cb; }
+      rplu::set_error("coincident target / source points");
+      delete h;
+      return RPLU_ERR_ARG;
     }
-    h->agg_start.push_back((int64_t)h->agg_node.size());
-    h->ex_node.insert(h->ex_node.end(), exact[q].begin(), exact[q].end());
-    h->ex_start.push_back((int64_t)h->ex_node.size());
+  }
+  h->agg_start.assign(nleaf + 1, 0);
+  h->ex_start.assign(nleaf + 1, 0);
+  for (const Task& task : tasks) {
+    for (const AggRec& r : task.agg) ++h->agg_start[r.slot + 1];
+    for (const ExRec& r : task.ex) ++h->ex_start[r.slot + 1];
+  }
+  for (size_t q = 0; q < nleaf; ++q) {
+    h->agg_start[q + 1] += h->agg_start[q];
+    h->ex_start[q + 1] += h->ex_start[q];
+  }
+  h->agg_node.resize((size_t)h->agg_start[nleaf]);
+  h->agg_alpha.resize((size_t)h->agg_start[nleaf]);
+  h->ex_node.resize((size_t)h->ex_start[nleaf]);
+  {
+    std::vector<int64_t> ca(h->agg_start.begin(), h->agg_start.end() - 1);
+    std::vector<int64_t> ce(h->ex_start.begin(), h->ex_start.end() - 1);
+    for (const Task& task : tasks) {
+      for (const AggRec& r : task.agg) {
+        const int64_t k = ca[r.slot]++;
+        h->agg_node[k] = r.node;
+        h->agg_alpha[k] = r.alpha;
+      }
+      for (const ExRec& r : task.ex) h->ex_node[ce[r.slot]++] = r.node;
+    }
   }
   *out = h;
   return RPLU_OK;
