@@ -85,6 +85,42 @@ def run_sharded(backend, steps, group=None, poll_every=32, step_hook=None):
     return backend.finish()
 
 
+class _capture:
+    """CUDA-graph capture of the enclosed launches on a side stream.
+
+    torch.cuda.graph() would do: it also runs gc.collect() and
+    torch.cuda.empty_cache() on entry, which hands every cached block back to
+    the driver -- at C3 size the next call then pays a fresh 8.6 GB cudaMalloc
+    for its residual copy (0.1-0.3 s, more than a tenth of the run).  The
+    shard kernels launch on torch's current stream, which this switches."""
+
+    def __init__(self, graph, dev):
+        self.graph, self.dev = graph, dev
+        self.stream = torch.cuda.Stream(dev)
+
+    def __enter__(self):
+        torch.cuda.synchronize(self.dev)
+        self.stream.wait_stream(torch.cuda.current_stream(self.dev))
+        self._ctx = torch.cuda.stream(self.stream)
+        self._ctx.__enter__()
+        self.graph.capture_begin()
+        return self
+
+    def __exit__(self, et, ev, tb):
+        try:
+            if et is None:
+                self.graph.capture_end()
+            else:       # leave capture mode without keeping the graph
+                try:
+                    self.graph.capture_end()
+                except RuntimeError:
+                    pass
+        finally:
+            self._ctx.__exit__(et, ev, tb)
+        torch.cuda.current_stream(self.dev).wait_stream(self.stream)
+        return False
+
+
 def _run_sharded_block_graph(backend, steps, group, block):
     """Delayed-update shards: one whole block of `block` steps (per step the
     select kernels, the allreduce, post + pivot column + read pass -- the
@@ -115,7 +151,7 @@ def _run_sharded_block_graph(backend, steps, group, block):
         torch.cuda.synchronize(backend.dev)
         g = torch.cuda.CUDAGraph()
         try:
-            with torch.cuda.graph(g):
+            with _capture(g, backend.dev):
                 for pos in range(block):
                     step(-1 - pos)
         except RuntimeError:
@@ -157,7 +193,7 @@ def run_sharded_graph(backend, steps, group=None, chunk=32):
     # the current stream, which the capture context switches for us
     torch.cuda.synchronize(backend.dev)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with _capture(g, backend.dev):
         msg = backend.select(-1, totals)
         if dist.is_initialized():
             dist.all_reduce(msg, op=dist.ReduceOp.SUM, group=group)
