@@ -57,7 +57,7 @@ for step in "$@"; do
         > "$OUT/$i.lite_$cfg.log" 2>&1 ;;
     shard1)   # world-1 sharded C3 over NCCL (torchrun, one rank); rest = env assignments
       envs=""; [[ $rest != shard1 ]] && envs=$rest
-      env $envs timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
+      env RPLU_FORCE_SHARDED=1 $envs timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
         --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 2 --warmup 1 \
         > "$OUT/$i.shard1.log" 2>&1 ;;
     py)
