@@ -67,6 +67,11 @@ struct DenseParams {
   // only carry their differences (t - t0 = pending terms before this step).
   int rel;
   long long u_rows;    // rows of U the tensor map may cover (rel mode)
+  // TMA pass: residual rows per work item (<= 32; 0 = 32).  Fewer rows per
+  // item let the item count fill whole waves of the 148 persistent CTAs on
+  // short row blocks (4096 shard rows: 147 items of 28 rows instead of 128
+  // of 32 on 148 CTAs).
+  int pass_rows;
 };
 
 __device__ __forceinline__ long long lz_t(const DenseParams& p) {
@@ -794,7 +799,9 @@ __global__ void __launch_bounds__(288, 1)
 
   const long long n = p.n, m = p.m, ld = p.ld;
   const long long nchunks = (m + CW - 1) / CW;
-  const long long nblocks = (n + ROWS - 1) / ROWS;
+  // rows per work item: the stage layout stays ROWS rows, an item fills RB
+  const int RB = (p.pass_rows > 0 && p.pass_rows < ROWS) ? p.pass_rows : ROWS;
+  const long long nblocks = (n + RB - 1) / RB;
   const T* Lt = reinterpret_cast<const T*>(p.Lt);
   const long long l_row0 = lz_t0(p);
 
@@ -814,7 +821,7 @@ __global__ void __launch_bounds__(288, 1)
       auto store_item = [&](long long j) {
         const long long rbj = blockIdx.x + (j / nchunks) * gridDim.x, cj = j % nchunks;
         const V* sj = tiles + (size_t)(j % STAGES) * (ROWS + QC) * TX;
-        tma_store_2d(&tmR, (int)(cj * WORDS), (int)(rbj * ROWS), sj, pol_r);
+        tma_store_2d(&tmR, (int)(cj * WORDS), (int)(rbj * RB), sj, pol_r);
         bulk_commit();
       };
       for (long long rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
@@ -827,8 +834,8 @@ __global__ void __launch_bounds__(288, 1)
               bulk_wait_read_all();  // the store has read the stage
             }
           }
-          mbar_expect_tx(&full[stage], (unsigned)C::STAGE);
-          tma_load_2d(st, &tmR, (int)(c * WORDS), (int)(rb * ROWS), &full[stage], pol_r);
+          mbar_expect_tx(&full[stage], (unsigned)((RB + QC) * C::LINE));
+          tma_load_2d(st, &tmR, (int)(c * WORDS), (int)(rb * RB), &full[stage], pol_r);
           tma_load_2d(st + ROWS * TX, &tmU, (int)(c * WORDS), u_row0, &full[stage], pol_u);
           if (++stage == STAGES) {
             stage = 0;
@@ -854,15 +861,15 @@ __global__ void __launch_bounds__(288, 1)
   int k = 0;  // row blocks done by this CTA
   long long prev_row0 = -1;
   for (long long rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++k) {
-    const long long row0 = rb * ROWS;
+    const long long row0 = rb * RB;
     const int buf = k & 1;
     T* L = Ls + buf * QC * ROWS;
     for (int idx = threadIdx.x; idx < QC * ROWS; idx += C::NCW * 32) {
       const int s = idx / ROWS, r = idx % ROWS;
-      L[idx] = (row0 + r < n) ? Lt[(l_row0 + s) * n + row0 + r] : S::zero();
+      L[idx] = (r < RB && row0 + r < n) ? Lt[(l_row0 + s) * n + row0 + r] : S::zero();
     }
     consumer_bar();  // L visible; red[buf^1] of the previous block complete
-    if (prev_row0 >= 0 && threadIdx.x < ROWS) {
+    if (prev_row0 >= 0 && threadIdx.x < RB) {
       const double* rd = red + (buf ^ 1) * C::NCW * RPT;
       const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
       if (prev_row0 + threadIdx.x < n) {
@@ -874,7 +881,7 @@ __global__ void __launch_bounds__(288, 1)
       }
     }
     const long long myrow0 = row0 + ty * RPT;
-    const int nr = (int)max(0LL, min((long long)RPT, n - myrow0));
+    const int nr = (int)max(0LL, min(min((long long)RPT, (long long)(RB - ty * RPT)), n - myrow0));
     double acc[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
@@ -953,7 +960,7 @@ __global__ void __launch_bounds__(288, 1)
     prev_row0 = row0;
   }
   consumer_bar();
-  if (prev_row0 >= 0 && threadIdx.x < ROWS) {
+  if (prev_row0 >= 0 && threadIdx.x < RB) {
     const double* rd = red + ((k - 1) & 1) * C::NCW * RPT;
     const int g = threadIdx.x / RPT, r = threadIdx.x % RPT;
     if (prev_row0 + threadIdx.x < n) {
@@ -1526,17 +1533,33 @@ static int launch_lazy_pass4_w(const DenseParams& p, cudaStream_t s) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
-  const long long nblocks = (p.n + C::ROWS - 1) / C::ROWS;
+  // rows per work item: the count that minimises waves x rows on the
+  // persistent CTAs (ties keep the larger item); RPLU_PASS_ROWS overrides
+  static const int rows_env = env_int("RPLU_PASS_ROWS", 0);
+  int rb_rows = C::ROWS;
+  if (rows_env >= 8 && rows_env <= C::ROWS) {
+    rb_rows = rows_env;
+  } else {
+    long long best = -1;
+    for (int r = C::ROWS; r >= C::ROWS - 8; --r) {
+      const long long items = (p.n + r - 1) / r;
+      const long long cost = ((items + sm_count() - 1) / sm_count()) * r;
+      if (best < 0 || cost < best) { best = cost; rb_rows = r; }
+    }
+  }
+  DenseParams pp = p;
+  pp.pass_rows = rb_rows;
+  const long long nblocks = (p.n + rb_rows - 1) / rb_rows;
   const long long g = nblocks < sm_count() ? nblocks : sm_count();
   if (g <= 0 || p.m <= 0) return RPLU_OK;
   CUtensorMap tmR, tmU;
   const long long urows = p.rel ? p.u_rows : p.t0 + QC;  // U rows 0 .. t0+QC-1 exist
-  if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, C::ROWS, C::LINE) ||
+  if (!make_row_map(&tmR, p.R, (int)sizeof(T), p.n, p.m, p.ld, rb_rows, C::LINE) ||
       !make_row_map(&tmU, p.U, (int)sizeof(T), urows, p.m, p.ldu, QC, C::LINE)) {
     set_error("cuTensorMapEncodeTiled failed for the delayed-update pass");
     return RPLU_ERR_CUDA;
   }
-  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED, DOT><<<(unsigned)g, 288, C::SMEM, s>>>(p, tmR,
+  lazy_pass4_kernel<T, VEC, FLUSH, QC, TXW, FUSED, DOT><<<(unsigned)g, 288, C::SMEM, s>>>(pp, tmR,
                                                                                        tmU);
   return RPLU_OK;
 }
