@@ -942,9 +942,10 @@ def run_b200_arm(args, cfg, dist, rank_id, world):
     d2h = tr_h.L.nbytes + tr_h.U.nbytes + 16 * tr_h.steps + 8 * (tr_h.steps + 1)
     same = tr_h.pivots == tr.pivots
 
-    # CPU baseline: oracle port on the same bytes, bounded sample (2 pivot steps)
+    # CPU baseline: oracle port on the same bytes, bounded sample (~10 s of CPU
+    # work at C3 size: 24 pivot steps at ~2.2 steps/s on 16 threads)
     model, cores = _cpu_info()
-    cpu_steps = 2 if n > 8192 else 10
+    cpu_steps = min(24 if n > 8192 else 100, rank)
     A64 = A_host.astype(np.float64) if tdtype == torch.float32 else A_host.copy()
     del host_t
     cb_v, cb_dt = cpu_baseline(A64, rank, seed, cpu_steps, cores)
