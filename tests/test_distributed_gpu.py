@@ -86,6 +86,25 @@ def test_c_group_driver_world1(update, cuda_device):
     assert rng.uniform() == ref2.uniform()
 
 
+@pytest.mark.parametrize("graph_env", ["0", "1"])
+def test_c_group_driver_lazy_graph_and_plain_loop(graph_env, cuda_device, monkeypatch):
+    """The C group driver's delayed-update loop with its multi-device block
+    graph (RPLU_GROUP_GRAPH unset / 1) and with the plain step loop (0), across
+    a trailing partial block and a tol stop inside a replayed block."""
+    from paper_2601_22344_b200.distributed import group_eliminate
+    monkeypatch.setenv("RPLU_GROUP_GRAPH", graph_env)
+    A = torch.from_numpy(gen.c1_dense(13, n=520, m=400)).cuda()
+    for steps, tol in ((75, 0.0), (300, 0.4)):
+        ref = rp.eliminate(A, rp.PivotRule("rplu", rp.RngState(8)), steps, stop_tol=tol,
+                           update="eager")
+        tr = group_eliminate(A, rp.PivotRule("rplu", rp.RngState(8)), steps, devices=[0],
+                             stop_tol=tol, update="lazy")
+        assert tr.pivots == ref.pivots and tr.tol_stop == ref.tol_stop
+        assert torch.equal(tr.L, ref.L) and torch.equal(tr.U, ref.U)
+        assert torch.equal(tr.residual_device, ref.residual_device)
+        np.testing.assert_allclose(tr.resid_fro, ref.resid_fro, rtol=1e-12)
+
+
 @pytest.mark.parametrize("dtype,lazy_block,gram", [(torch.float64, -1, True), (torch.float64, 5, True),
                                                    (torch.float64, 4, False), (torch.float32, 6, False),
                                                    (torch.complex128, 3, False)])
