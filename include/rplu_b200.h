@@ -372,6 +372,13 @@ int rplu_cauchy_plan_row(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const v
 int rplu_cauchy_plan_update(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
                             const void* y, void* G, void* Bt, int64_t i, int64_t j,
                             const void* rbuf, void* Cout, void* Rout, void* stream);
+/* One proposal of the rejection loop (cauchy.py:236-250) in a single host
+ * synchronisation: i = sample_index(bounds, u), then rplu_cauchy_plan_row for
+ * that i.  out5 = {i, near-boundary flag of the draw, sum_j |r_j|^2,
+ * max_j |r_j|, bounds[i]}. */
+int rplu_cauchy_plan_propose(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                             const void* y, void* G, void* Bt, const double* bounds, double u,
+                             void* rbuf, double* wbuf, double* out5, void* stream);
 
 /* Host-native interaction-plan build (no GPU needed), replacing the Python
  * quadtrees and dual traversal of rplu.treebounds.build_plan
@@ -520,6 +527,12 @@ int rplu_diag_dmma_peak(rplu_ctx* ctx, double* tflops, double* best_ms);
  * a CDF boundary. */
 int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
                       int64_t* out_index, int32_t* near_boundary, void* stream);
+/* The same draw plus the element gather[index] of a device complex128 array
+ * (value[0..1] = re, im) in one host synchronisation: the plan path's column
+ * draw and pivot value. */
+int rplu_sample_index_gather(rplu_ctx* ctx, const double* weights, int64_t n, double u,
+                             const void* gather, int64_t* out_index, int32_t* near_boundary,
+                             double* value, void* stream);
 
 /* The same search against an ABSOLUTE target in [0, total] (first index whose
  * running sum exceeds target; clamp / walk-back as above): the owner shard's

@@ -206,6 +206,11 @@ SIGNATURES = {
                                             c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rplu_cauchy_plan_update": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                                c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "rplu_cauchy_plan_propose": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                                c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp]),
+    "rplu_sample_index_gather": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_vp,
+                                                ctypes.POINTER(c_i64), ctypes.POINTER(c_i32),
+                                                c_vp, c_vp]),
     "rplu_plan_build": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_dbl, c_i64, c_vp,
                                        ctypes.POINTER(c_vp)]),
     "rplu_plan_counts": (ctypes.c_int, [c_vp, c_vp]),

@@ -348,6 +348,31 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
             u.data_ptr() if u is not None else None, out3.ctypes.data, stream_h))
         last_rmax[0] = float(out3[1])
         return float(out3[0]), float(out3[1]), float(out3[2])
+
+    out5 = np.zeros(5)
+
+    def propose(u, uniform):
+        """i ~ u and its pivot row in one host synchronisation; returns
+        (i, ||r||^2, u_i)"""
+        _ffi.check(c._lib.rplu_cauchy_plan_propose(
+            c.handle, p, n, m, cur.x.data_ptr(), cur.y.data_ptr(), cur.G.data_ptr(),
+            cur.Bt.data_ptr(), u.data_ptr(), float(uniform), rbuf.data_ptr(), wbuf.data_ptr(),
+            out5.ctypes.data, stream_h))
+        tr.near_boundary_draws += int(out5[1])
+        last_rmax[0] = float(out5[3])
+        return int(out5[0]), float(out5[2]), float(out5[4])
+
+    val2 = np.zeros(2)
+
+    def draw_column(uniform):
+        """j ~ |r|^2 and the pivot value r_j in one host synchronisation"""
+        j64, near = ctypes.c_int64(-1), ctypes.c_int32(0)
+        _ffi.check(c._lib.rplu_sample_index_gather(
+            c.handle, ctypes.c_void_p(wbuf.data_ptr()), m, float(uniform),
+            ctypes.c_void_p(rbuf.data_ptr()), ctypes.byref(j64), ctypes.byref(near),
+            val2.ctypes.data, stream_h))
+        tr.near_boundary_draws += int(near.value)
+        return int(j64.value), complex(val2[0], val2[1])
     try:
         for _ in range(rank):
             u = tree_bounds_device(plan, cur)
@@ -367,8 +392,7 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
             else:
                 i = None
                 for _p in range(cap):
-                    ii = sample_index(u, stream.next())
-                    rho, _, ui = row(ii, u)
+                    ii, rho, ui = propose(u, stream.next())
                     tr.proposals += 1
                     if abs(rho - ui) <= 1e-12 * ui:
                         tr.near_tie_acceptances += 1
@@ -386,15 +410,14 @@ def _structured_eliminate_plan(M, rule, rank, stop_tol, nu, plan, rng, keep_step
             rmax = last_rmax[0]
             if rule == "c2plu":
                 j = int(torch.argmax(wbuf))
+                a = complex(rbuf[j].item())
             else:
-                j = sample_index(wbuf, stream.next())
+                j, a = draw_column(stream.next())
             thr = PIVOT_REL_TOL * rmax
-            a = complex(rbuf[j].item())
             if abs(a) <= thr:
                 if rule == "c2plu":
                     raise ZeroDivisionError(f"pivot ({i}, {j}) is numerically zero")
-                j = sample_index(wbuf, stream.next())
-                a = complex(rbuf[j].item())
+                j, a = draw_column(stream.next())
                 if abs(a) <= thr:
                     raise ZeroDivisionError(
                         f"pivot ({i}, {j}) is numerically zero after resampling")

@@ -907,6 +907,40 @@ int rplu_sample_index(rplu_ctx* ctx, const double* weights, int64_t n, double u,
   return RPLU_OK;
 }
 
+int rplu_sample_index_gather(rplu_ctx* ctx, const double* weights, int64_t n, double u,
+                             const void* gather, int64_t* out_index, int32_t* near_boundary,
+                             double* value, void* stream) {
+  if (!ctx || !out_index || !gather || !value) {
+    set_error("rplu_sample_index_gather: NULL argument");
+    return RPLU_ERR_ARG;
+  }
+  if (n <= 0 || !weights) { set_error("weights must be a nonempty 1-D array"); return RPLU_ERR_ARG; }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  long long idx = -1;
+  int near = 0;
+  int rc = sample_index_gather_impl(ctx, weights, n, u, gather, &idx, &near, value,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (rc) return rc;
+  *out_index = idx;
+  if (near_boundary) *near_boundary = near;
+  return RPLU_OK;
+}
+
+int rplu_cauchy_plan_propose(rplu_ctx* ctx, int32_t p, int64_t n, int64_t m, const void* x,
+                             const void* y, void* G, void* Bt, const double* bounds, double u,
+                             void* rbuf, double* wbuf, double* out5, void* stream) {
+  if (!ctx || p < 1 || p > 8 || n < 1 || m < 1 || !x || !y || !G || !Bt || !rbuf || !wbuf ||
+      !out5 || !bounds) {
+    set_error("rplu_cauchy_plan_propose: bad argument");
+    return RPLU_ERR_ARG;
+  }
+  DeviceGuard g(ctx->device);
+  if (g.rc) return g.rc;
+  return cauchy_plan_propose_impl(ctx, p, n, m, x, y, G, Bt, bounds, u, rbuf, wbuf, out5,
+                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
 int rplu_sample_target(rplu_ctx* ctx, const double* weights, int64_t n, double target,
                        int64_t* out_index, int32_t* near_boundary, void* stream) {
   if (!ctx || !out_index) { set_error("rplu_sample_target: NULL argument"); return RPLU_ERR_ARG; }

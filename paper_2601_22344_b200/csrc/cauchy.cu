@@ -617,7 +617,8 @@ static int plan_params(rplu_ctx* ctx, int p, long long n, long long m, const voi
   int rc;
   if ((rc = ctx->state.ensure(sizeof(DevState)))) return rc;
   q.st = reinterpret_cast<DevState*>(ctx->state.ptr);
-  if ((rc = ctx->csync.ensure(256))) return rc;
+  // layout: [0,8) row-max bits | [16, 16 + 32 p) G_i / B_j snapshot | [512, 544) read-back slots
+  if ((rc = ctx->csync.ensure(1024))) return rc;
   q.rmax_bits = reinterpret_cast<unsigned long long*>(ctx->csync.ptr);
   gsnap = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctx->csync.ptr) + 16);
   return RPLU_OK;
@@ -646,6 +647,69 @@ int cauchy_plan_row_impl(rplu_ctx* ctx, int p, long long n, long long m, const v
   memcpy(&rmax, &rbits, sizeof(rmax));
   host3[1] = rmax;
   host3[2] = bi;
+  return RPLU_OK;
+}
+
+// the proposal's row index from a device-side draw (first 8 bytes of its
+// SampleOut): st->pi <- idx, *bi <- bounds[idx], row-max slot cleared
+__global__ void cauchy_plan_init_dev_kernel(DevState* st, const long long* didx, long long n,
+                                            const double* bounds, double* bi,
+                                            unsigned long long* rmax_bits) {
+  long long i = *didx;
+  if (i < 0 || i >= n) i = 0;   // a failed draw: the host raises after the read-back
+  st->active = 1;
+  st->status = kRunning;
+  st->pi = i;
+  *bi = bounds[i];
+  *rmax_bits = 0ull;
+}
+
+// Proposal of the plan path in ONE host synchronisation: i ~ bounds (uniform
+// u), pivot row i into rbuf / wbuf, host5 = {i, near-boundary flag, sum |r|^2,
+// max |r|, bounds[i]} (sample_index + rplu_cauchy_plan_row took two).
+int cauchy_plan_propose_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                             const void* y, void* G, void* Bt, const double* bounds, double u,
+                             void* rbuf, double* wbuf, double* host5, cudaStream_t s) {
+  CauchyParams q;
+  double2* gsnap;
+  int rc;
+  if ((rc = plan_params(ctx, p, n, m, x, y, G, Bt, rbuf, wbuf, q, gsnap))) return rc;
+  double* bi_slot = reinterpret_cast<double*>(reinterpret_cast<char*>(ctx->csync.ptr) + 528);
+  const int row_blocks = (int)std::min<long long>((m + 255) / 256, 8LL * ctx->sm_count);
+  const void* d0 = nullptr;
+  const void* d1 = nullptr;
+  auto after_draw = [&](const void* d) -> int {
+    count_launches(2);
+    cauchy_plan_init_dev_kernel<<<1, 1, 0, s>>>(q.st, reinterpret_cast<const long long*>(d), n,
+                                                bounds, bi_slot, q.rmax_bits);
+    RPLU_P_SWITCH(p, (cauchy_row_kernel<PP><<<row_blocks, 256, 0, s>>>(q)));
+    RPLU_CUDA(cudaGetLastError());
+    return RPLU_OK;
+  };
+  if ((rc = sample_two_launch(ctx, bounds, n, u, after_draw, wbuf, m, s, &d0, &d1))) return rc;
+  unsigned char h0[kSampleOutBytes], h1[kSampleOutBytes];
+  unsigned long long rbits = 0;
+  double bi = 0.0;
+  RPLU_CUDA(cudaMemcpyAsync(h0, d0, kSampleOutBytes, cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaMemcpyAsync(h1, d1, kSampleOutBytes, cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaMemcpyAsync(&rbits, q.rmax_bits, sizeof(rbits), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaMemcpyAsync(&bi, bi_slot, sizeof(bi), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  long long idx = -1;
+  int near = 0;
+  double rho = 0.0;
+  if ((rc = sample_out_unpack(h0, &idx, &near, nullptr))) return rc;   // bad bounds: raises as sample_index does
+  if ((rc = sample_out_unpack(h1, nullptr, nullptr, &rho))) {
+    // an all-zero row is not an error here: rho = 0 (the caller's acceptance test handles it)
+    rho = 0.0;
+  }
+  double rmax = 0.0;
+  memcpy(&rmax, &rbits, sizeof(rmax));
+  host5[0] = (double)idx;
+  host5[1] = (double)near;
+  host5[2] = rho;
+  host5[3] = rmax;
+  host5[4] = bi;
   return RPLU_OK;
 }
 

@@ -2049,6 +2049,7 @@ struct SampleOut {
   int near;
   double total;  // the CDF's total (the draw's own summation order)
 };
+static_assert(sizeof(SampleOut) == kSampleOutBytes, "SampleOut layout (rplu_internal.h)");
 
 // mode 0: u in [0,1) scaled by the CDF total (sample_index); mode 1: u is an
 // absolute target in [0, total] (the owner shard's draw of a sharded
@@ -2129,15 +2130,23 @@ __global__ void __launch_bounds__(1024) sample_chunked_kernel(const double* w, l
   }
 }
 
-int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
-                      long long* idx, int* near, double* total, cudaStream_t s) {
+// Enqueue one draw into result slot `slot` (0 or 1) of the context's sample
+// scratch and return the device address of its SampleOut (no host
+// synchronisation): callers chain further kernels on the drawn index and read
+// everything back with one synchronisation.
+static int sample_index_launch(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
+                               int slot, cudaStream_t s, SampleOut** dout) {
   int rc;
   const long long nch = (n + kChunk - 1) / kChunk;
-  if ((rc = ctx->scratch[7].ensure(sizeof(SampleOut) + 16 + sizeof(double) * nch))) return rc;
-  SampleOut* d = reinterpret_cast<SampleOut*>(ctx->scratch[7].ptr);
+  // per slot: SampleOut | neg flag (16 B) | chunk totals; slots of equal size
+  const size_t per = (sizeof(SampleOut) + 16 + sizeof(double) * (size_t)nch + 63) & ~size_t(63);
+  // (the scratch only grows: a later, smaller draw keeps the larger stride
+  // consistent because both slots are addressed from the call's own `per`)
+  if ((rc = ctx->scratch[7].ensure(2 * per))) return rc;
+  char* base = reinterpret_cast<char*>(ctx->scratch[7].ptr) + (size_t)slot * per;
+  SampleOut* d = reinterpret_cast<SampleOut*>(base);
   if (n >= kChunkedMinN) {
-    int* neg = reinterpret_cast<int*>(reinterpret_cast<char*>(ctx->scratch[7].ptr) +
-                                      sizeof(SampleOut));
+    int* neg = reinterpret_cast<int*>(base + sizeof(SampleOut));
     double* ctot = reinterpret_cast<double*>(reinterpret_cast<char*>(neg) + 16);
     RPLU_CUDA(cudaMemsetAsync(neg, 0, sizeof(int), s));
     count_launches(2);
@@ -2148,11 +2157,94 @@ int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int
     sample_index_kernel<<<1, 1024, 0, s>>>(w, n, u, mode, d);
   }
   RPLU_CUDA(cudaGetLastError());
+  *dout = d;
+  return RPLU_OK;
+}
+
+static int sample_status(const SampleOut& h) {
+  if (h.status == 1) { set_error("weights must be nonnegative"); return RPLU_ERR_ARG; }
+  if (h.status == 2) { set_error("all weights are zero; nothing to sample"); return RPLU_ERR_ARG; }
+  return RPLU_OK;
+}
+
+int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
+                      long long* idx, int* near, double* total, cudaStream_t s) {
+  SampleOut* d = nullptr;
+  int rc;
+  if ((rc = sample_index_launch(ctx, w, n, u, mode, 0, s, &d))) return rc;
   SampleOut h;
   RPLU_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   RPLU_CUDA(cudaStreamSynchronize(s));
-  if (h.status == 1) { set_error("weights must be nonnegative"); return RPLU_ERR_ARG; }
-  if (h.status == 2) { set_error("all weights are zero; nothing to sample"); return RPLU_ERR_ARG; }
+  if ((rc = sample_status(h))) return rc;
+  if (idx) *idx = h.idx;
+  if (near) *near = h.near;
+  if (total) *total = h.total;
+  return RPLU_OK;
+}
+
+// value[0..1] <- gather[idx] of the draw in `d` (complex128 element)
+__global__ void sample_gather_kernel(const SampleOut* d, const double2* gather, long long n,
+                                     double2* value) {
+  const long long i = d->idx;
+  *value = (d->status == 0 && i >= 0 && i < n) ? gather[i] : make_double2(0.0, 0.0);
+}
+
+// sample_index(w, u) and the element gather[idx] of a complex128 array in one
+// host synchronisation (the plan path's column draw + pivot value).
+int sample_index_gather_impl(rplu_ctx* ctx, const double* w, long long n, double u,
+                             const void* gather, long long* idx, int* near, double* value2,
+                             cudaStream_t s) {
+  SampleOut* d = nullptr;
+  int rc;
+  if ((rc = sample_index_launch(ctx, w, n, u, 0, 0, s, &d))) return rc;
+  if ((rc = ctx->csync.ensure(1024))) return rc;
+  double2* slot = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctx->csync.ptr) + 512);
+  count_launches(1);
+  sample_gather_kernel<<<1, 1, 0, s>>>(d, reinterpret_cast<const double2*>(gather), n, slot);
+  RPLU_CUDA(cudaGetLastError());
+  SampleOut h;
+  double2 v;
+  RPLU_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaMemcpyAsync(&v, slot, sizeof(v), cudaMemcpyDeviceToHost, s));
+  RPLU_CUDA(cudaStreamSynchronize(s));
+  if ((rc = sample_status(h))) return rc;
+  *idx = h.idx;
+  if (near) *near = h.near;
+  value2[0] = v.x;
+  value2[1] = v.y;
+  return RPLU_OK;
+}
+
+// Plan-path proposal: draw i ~ bounds with u, then hand the drawn index to the
+// caller's row kernels on the device (init(d) is enqueued by the caller
+// through `after_draw`), total of wbuf in slot 1; one synchronisation in the
+// caller.  Returns the two device result slots.
+int sample_two_launch(rplu_ctx* ctx, const double* w0, long long n0, double u0,
+                      const std::function<int(const void*)>& after_draw, const double* w1,
+                      long long n1, cudaStream_t s, const void** d0, const void** d1) {
+  SampleOut* a = nullptr;
+  SampleOut* b = nullptr;
+  int rc;
+  // size the scratch for the larger of the two draws first, so that both
+  // slots use one stride
+  const long long nmax = n0 > n1 ? n0 : n1;
+  {
+    const long long nch = (nmax + kChunk - 1) / kChunk;
+    const size_t per = (sizeof(SampleOut) + 16 + sizeof(double) * (size_t)nch + 63) & ~size_t(63);
+    if ((rc = ctx->scratch[7].ensure(2 * per))) return rc;
+  }
+  if ((rc = sample_index_launch(ctx, w0, n0, u0, 0, 0, s, &a))) return rc;
+  if ((rc = after_draw(a))) return rc;
+  if ((rc = sample_index_launch(ctx, w1, n1, 0.0, 2, 1, s, &b))) return rc;
+  *d0 = a;
+  *d1 = b;
+  return RPLU_OK;
+}
+
+int sample_out_unpack(const void* host_copy, long long* idx, int* near, double* total) {
+  const SampleOut& h = *reinterpret_cast<const SampleOut*>(host_copy);
+  int rc;
+  if ((rc = sample_status(h))) return rc;
   if (idx) *idx = h.idx;
   if (near) *near = h.near;
   if (total) *total = h.total;

@@ -116,6 +116,18 @@ void set_error(const std::string& msg);
 void count_launches(long long k);
 
 // standalone draw (dense.cu): mode 0 u*total, 1 absolute target, 2 total only
+// draws chained on the device (dense.cu): see sample_index_launch
+constexpr size_t kSampleOutBytes = 24;   // sizeof(SampleOut)
+int sample_index_gather_impl(rplu_ctx* ctx, const double* w, long long n, double u,
+                             const void* gather, long long* idx, int* near, double* value2,
+                             cudaStream_t s);
+int sample_two_launch(rplu_ctx* ctx, const double* w0, long long n0, double u0,
+                      const std::function<int(const void*)>& after_draw, const double* w1,
+                      long long n1, cudaStream_t s, const void** d0, const void** d1);
+int sample_out_unpack(const void* host_copy, long long* idx, int* near, double* total);
+int cauchy_plan_propose_impl(rplu_ctx* ctx, int p, long long n, long long m, const void* x,
+                             const void* y, void* G, void* Bt, const double* bounds, double u,
+                             void* rbuf, double* wbuf, double* host5, cudaStream_t s);
 int sample_index_impl(rplu_ctx* ctx, const double* w, long long n, double u, int mode,
                       long long* idx, int* near, double* total, cudaStream_t s);
 int cuda_fail(cudaError_t e, const char* where);
